@@ -1,0 +1,149 @@
+/*
+ * slimsell_b200.h — the C-ABI boundary of the B200-native SlimSell BFS-SpMV
+ * path (libslimsell_b200.so, sm_100a).
+ *
+ * Every entry point replaces one function of the reference C++ library
+ * (arXiv 2010.09913 artifact, /root/reference/proj); the citation next to each
+ * declaration names the reference interface (file:line) it stands in for.
+ * Conventions:
+ *   - plain pointers and sizes only, no C++ or torch types;
+ *   - every function returns an SSB_* status; the message of the last failure
+ *     on the calling thread is ssb_last_error();
+ *   - handles are opaque, owned by the caller, released with *_destroy;
+ *   - host buffers are caller-allocated; every call is synchronous on return;
+ *   - vertex ids are int64 at the boundary (reference vid_t/val_t, graph.hpp:12,
+ *     semiring.hpp:17); the device stores int32 ids (n < 2^31).
+ * Status -> reference exception (bfs.hpp / repr.hpp / semiring.hpp):
+ *   SSB_EINVAL -> std::invalid_argument, SSB_ERANGE -> std::out_of_range,
+ *   SSB_ECAP -> BfsCapError (partial dist still written),
+ *   SSB_ECUDA / SSB_ENOMEM -> std::runtime_error.
+ */
+#ifndef SLIMSELL_B200_H
+#define SLIMSELL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSB_OK 0
+#define SSB_EINVAL 1
+#define SSB_ERANGE 2
+#define SSB_ECAP 3
+#define SSB_ECUDA 4
+#define SSB_ENOMEM 5
+
+#define SSB_ABI_VERSION 1
+
+/* Variant (semiring.hpp:25). */
+#define SSB_TROPICAL 0
+#define SSB_REAL 1
+#define SSB_BOOLEAN 2
+#define SSB_SELMAX 3
+
+typedef struct ssb_edges ssb_edges; /* normalised Graph on the device (graph.hpp:31-51) */
+typedef struct ssb_graph ssb_graph; /* SlimSellRepr on the device (repr.hpp:33-55) */
+
+/* SlimSellRepr scalar fields (repr.hpp:33-45). n_cells = |col| = Σ C·cl. */
+typedef struct {
+  int64_t C, sigma, n, n_padded, n_chunks, nonzeros, n_cells, padding, max_chunk_len;
+} ssb_layout_info;
+
+/* BfsOptions (bfs.hpp:16-24). schedule and workers are accepted for API
+ * compatibility and ignored: the device schedules its own work units. */
+typedef struct {
+  int32_t variant;        /* SSB_TROPICAL .. SSB_SELMAX */
+  int32_t slimwork;       /* skip chunks whose real rows are all visited */
+  int64_t slimchunk_len;  /* L: max columns per work unit; 0 = SlimChunk off */
+  int32_t schedule;       /* ignored (Schedule, bfs.hpp:14) */
+  int32_t workers;        /* ignored */
+  int64_t max_iterations; /* <= 0 resolves to n + 1 (bfs.cpp:70-71) */
+  int32_t want_parents;
+  int32_t selmax_compat;  /* 1: reproduce the reference's sel-max root encoding
+                             (SURVEY.md App. A.3); 0: corrected parents */
+} ssb_bfs_options;
+
+/* IterStats (bfs.hpp:26-34); elapsed_ns is device time of the iteration. */
+typedef struct {
+  int64_t iteration, elapsed_ns, chunks_processed, chunks_skipped, subchunks_processed,
+      columns_processed, frontier_size;
+} ssb_iter_stats;
+
+const char* ssb_last_error(void);
+int ssb_abi_version(void);
+/* Selects the CUDA device for handles created afterwards on this thread. */
+int ssb_set_device(int device);
+
+/* ---- graph input (L1) -------------------------------------------------- */
+/* Graph::from_pairs (graph.hpp:36, graph.cpp:65-86): orient u<v, drop
+ * self-loops, sort, dedup — on the device. uv holds count (u,v) pairs;
+ * n < 0 infers max id + 1. ERANGE for negative / out-of-range ids. */
+int ssb_edges_from_pairs(const int64_t* uv, int64_t count, int64_t n, ssb_edges** out);
+/* gen_kronecker (generator.hpp:55, generator.cpp:60-89), bit-exact, on the
+ * device: counter-based SplitMix64 draws + from_pairs normalisation. */
+int ssb_gen_kronecker(int64_t scale, int64_t edgefactor, uint64_t seed,
+                      const double initiator[4], ssb_edges** out);
+/* Graph::num_vertices / num_edges (graph.hpp:42-43). */
+int ssb_edges_info(const ssb_edges* e, int64_t* n, int64_t* m);
+/* Graph::edges() (graph.hpp:44): 2*m int64, sorted (u<v) pairs. */
+int ssb_edges_export(const ssb_edges* e, int64_t* uv);
+/* to_csr (graph.hpp:71, graph.cpp:212-232): row n+1, col 2m, rows ascending. */
+int ssb_to_csr(const ssb_edges* e, int64_t* row, int64_t* col);
+void ssb_edges_destroy(ssb_edges* e);
+
+/* ---- layout (L2) ------------------------------------------------------- */
+/* build_slimsell (repr.hpp:66, repr.cpp:84-131) on the device: σ-window sort
+ * by (degree desc, id asc), chunk height C, column-major col with -1 padding,
+ * no value array. EINVAL for C <= 0 or sigma <= 0. */
+int ssb_build_slimsell(const ssb_edges* e, int64_t C, int64_t sigma, ssb_graph** out);
+/* Uploads a host SlimSellRepr (the reference struct's arrays, int64). */
+int ssb_graph_from_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
+                          const int64_t* col, int64_t n_cells, const int64_t* cs,
+                          const int64_t* cl, int64_t n_chunks, const int64_t* perm,
+                          ssb_graph** out);
+int ssb_graph_info(const ssb_graph* g, ssb_layout_info* info);
+/* Materialises the SlimSellRepr arrays on the host (any pointer may be NULL):
+ * col n_cells, cs n_chunks, cl n_chunks, perm n, inv_perm n. */
+int ssb_graph_export(const ssb_graph* g, int64_t* col, int64_t* cs, int64_t* cl,
+                     int64_t* perm, int64_t* inv_perm);
+/* Compact export of col as int32 (the device storage type). */
+int ssb_graph_export_col32(const ssb_graph* g, int32_t* col);
+void ssb_graph_destroy(ssb_graph* g);
+
+/* ---- kernels (L2/L3) --------------------------------------------------- */
+/* spmv_step (repr.hpp:90-92, repr.cpp:193-217): for chunks [chunk_begin,
+ * chunk_end), out rows = plus({x_prev[v]} ∪ {times(x_prev[u], edge)}) with the
+ * literal int64 semiring arithmetic (semiring.hpp:56-87). x_prev and out hold
+ * n_padded values in the permuted numbering; rows outside the range are left
+ * untouched. EINVAL for a bad range or variant. */
+int ssb_spmv_step(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* out,
+                  int64_t chunk_begin, int64_t chunk_end);
+
+/* bfs_spmv (bfs.hpp:80-81, bfs.cpp:222-246): algebraic BFS on the device.
+ * dist: n int64 in original ids, INT64_MAX when unreached. parent: n int64
+ * (may be NULL); *parent_len receives n when parents were produced, else 0 —
+ * sel-max decodes its tracked parents (bfs.cpp:94-101); the other variants
+ * derive them from dist like dp_transform (semiring.cpp:159-187) over the
+ * layout's adjacency. stats: up to stats_cap IterStats. ERANGE for a bad root,
+ * ECAP when the iteration cap is hit (dist holds the partial result). */
+int ssb_bfs_spmv(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, int64_t* dist,
+                 int64_t* parent, int64_t* parent_len, ssb_iter_stats* stats,
+                 int64_t stats_cap, int64_t* iterations);
+
+/* Device-resident form used by benchmarks: runs the BFS and leaves the
+ * result on the device. device_ms = CUDA-event time of the iteration loop on
+ * the handle's stream. */
+int ssb_bfs_run(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
+                ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations,
+                double* device_ms);
+/* Copies the last ssb_bfs_run result out (original ids), as ssb_bfs_spmv. */
+int ssb_bfs_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent,
+                  int64_t* parent_len);
+/* m_cc of the last run: Σ_{reached v} deg(v) / 2 (the GTEPS numerator). */
+int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLIMSELL_B200_H */

@@ -1,0 +1,352 @@
+"""Host-side mirror of the reference's public API for the BFS-SpMV path.
+
+Same names, argument meaning and error behaviour as
+``/root/reference/proj/include/slimsell/{graph,generator,repr,semiring,bfs}.hpp``;
+every call crosses the C-ABI of ``libslimsell_b200.so`` into sm_100a kernels.
+Handles (``Graph``, ``SlimSellRepr``) are device-resident; arrays come back as
+numpy int64 in the reference's layout.
+
+Exception mapping (reference -> here): std::invalid_argument -> InvalidArgument
+(a ValueError), std::out_of_range -> OutOfRange (an IndexError), BfsCapError ->
+BfsCapError (carries ``partial``), CUDA failures -> DeviceError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib as _L
+
+KINF = np.iinfo(np.int64).max  # semiring.hpp:20
+NO_PARENT = -1                   # semiring.hpp:23
+PAD_MARKER = -1                  # repr.hpp:14
+
+
+class Variant(IntEnum):  # semiring.hpp:25
+    tropical = 0
+    real = 1
+    boolean = 2
+    selmax = 3
+
+
+ALL_VARIANTS = (Variant.tropical, Variant.real, Variant.boolean, Variant.selmax)
+
+
+class Schedule(IntEnum):  # bfs.hpp:14 (accepted; the device schedules itself)
+    static_blocks = 0
+    dynamic_queue = 1
+
+
+class SlimSellError(RuntimeError):
+    pass
+
+
+class InvalidArgument(SlimSellError, ValueError):
+    pass
+
+
+class OutOfRange(SlimSellError, IndexError):
+    pass
+
+
+class DeviceError(SlimSellError):
+    pass
+
+
+@dataclass
+class IterStats:  # bfs.hpp:26-34
+    iteration: int = 0
+    elapsed_ns: int = 0
+    chunks_processed: int = 0
+    chunks_skipped: int = 0
+    subchunks_processed: int = 0
+    columns_processed: int = 0
+    frontier_size: int = 0
+
+    def counters(self):
+        return (self.chunks_processed, self.chunks_skipped, self.subchunks_processed,
+                self.columns_processed, self.frontier_size)
+
+
+@dataclass
+class BfsResult:  # bfs.hpp:36-42
+    dist: np.ndarray
+    parent: np.ndarray
+    iterations: int
+    per_iter: list = field(default_factory=list)
+
+    @property
+    def elapsed_ns(self) -> int:
+        return sum(s.elapsed_ns for s in self.per_iter)
+
+
+class BfsCapError(SlimSellError):  # bfs.hpp:46-54
+    def __init__(self, what: str, partial: BfsResult):
+        super().__init__(what)
+        self.partial = partial
+
+
+@dataclass
+class BfsOptions:  # bfs.hpp:16-24 (+ selmax_compat)
+    variant: Variant = Variant.tropical
+    slimwork: bool = False
+    slimchunk_len: int = 0
+    schedule: Schedule = Schedule.static_blocks
+    workers: int = 1
+    max_iterations: int = 0
+    want_parents: bool = True
+    selmax_compat: bool = True
+
+    def _c(self) -> _L.BfsOptionsC:
+        return _L.BfsOptionsC(int(self.variant), int(bool(self.slimwork)), int(self.slimchunk_len),
+                              int(self.schedule), int(self.workers), int(self.max_iterations),
+                              int(bool(self.want_parents)), int(bool(self.selmax_compat)))
+
+
+def _raise(rc: int):
+    msg = _L.lib().ssb_last_error().decode(errors="replace")
+    if rc == _L.SSB_EINVAL:
+        raise InvalidArgument(msg)
+    if rc == _L.SSB_ERANGE:
+        raise OutOfRange(msg)
+    raise DeviceError(f"status {rc}: {msg}")
+
+
+def _check(rc: int):
+    if rc != _L.SSB_OK:
+        _raise(rc)
+
+
+def _p(a, ty=_L.i64p):
+    return None if a is None else a.ctypes.data_as(ty)
+
+
+def set_device(device: int) -> None:
+    _check(_L.lib().ssb_set_device(device))
+
+
+@dataclass
+class CsrView:  # graph.hpp:63-69
+    row: np.ndarray
+    col: np.ndarray
+
+    def num_vertices(self) -> int:
+        return int(self.row.shape[0]) - 1
+
+
+class Graph:
+    """Normalised undirected graph, device-resident (graph.hpp:31-51)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        n, m = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        _check(_L.lib().ssb_edges_info(self._h, _p(n), _p(m)))
+        self._n, self._m = int(n[0]), int(m[0])
+
+    @staticmethod
+    def from_pairs(pairs, n: int = -1) -> "Graph":  # graph.hpp:36
+        uv = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1, 2))
+        h = C.c_void_p()
+        _check(_L.lib().ssb_edges_from_pairs(_p(uv) if uv.size else None, uv.shape[0], n, C.byref(h)))
+        return Graph(h)
+
+    def num_vertices(self) -> int:
+        return self._n
+
+    def num_edges(self) -> int:
+        return self._m
+
+    def edges(self) -> np.ndarray:
+        uv = np.empty((self._m, 2), dtype=np.int64)
+        if self._m:
+            _check(_L.lib().ssb_edges_export(self._h, _p(uv)))
+        return uv
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _L._lib is not None:
+            _L._lib.ssb_edges_destroy(h)
+            self._h = None
+
+
+def gen_kronecker(scale: int, edgefactor: int, seed: int,
+                  initiator=(0.57, 0.19, 0.19, 0.05)) -> Graph:  # generator.hpp:55
+    h = C.c_void_p()
+    _check(_L.lib().ssb_gen_kronecker(scale, edgefactor, seed, (C.c_double * 4)(*initiator), C.byref(h)))
+    return Graph(h)
+
+
+def gen_path(n: int) -> Graph:  # generator.hpp:62
+    if n < 1:
+        raise InvalidArgument("path needs n >= 1")
+    return Graph.from_pairs(np.stack([np.arange(n - 1), np.arange(1, n)], 1), n)
+
+
+def gen_clique(n: int) -> Graph:  # generator.hpp:63
+    if n < 1:
+        raise InvalidArgument("clique needs n >= 1")
+    return Graph.from_pairs(np.stack(np.triu_indices(n, 1), 1), n)
+
+
+def gen_star(n: int) -> Graph:  # generator.hpp:64
+    if n < 1:
+        raise InvalidArgument("star needs n >= 1")
+    return Graph.from_pairs(np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], 1), n)
+
+
+def to_csr(g: Graph) -> CsrView:  # graph.hpp:71
+    row = np.empty(g.num_vertices() + 1, dtype=np.int64)
+    col = np.empty(max(2 * g.num_edges(), 1), dtype=np.int64)
+    _check(_L.lib().ssb_to_csr(g._h, _p(row), _p(col)))
+    return CsrView(row, col[: 2 * g.num_edges()])
+
+
+class SlimSellRepr:
+    """Device-resident SlimSell layout (repr.hpp:33-55); arrays export lazily."""
+
+    def __init__(self, handle):
+        self._h = handle
+        info = _L.LayoutInfo()
+        _check(_L.lib().ssb_graph_info(self._h, C.byref(info)))
+        self.C, self.sigma, self.n = info.C, info.sigma, info.n
+        self.n_padded, self.n_chunks, self.nonzeros = info.n_padded, info.n_chunks, info.nonzeros
+        self.n_cells, self.padding, self.max_chunk_len = info.n_cells, info.padding, info.max_chunk_len
+        self._host = None
+
+    def _export(self):
+        if self._host is None:
+            col = np.empty(max(self.n_cells, 1), np.int64)
+            cs = np.empty(max(self.n_chunks, 1), np.int64)
+            cl = np.empty(max(self.n_chunks, 1), np.int64)
+            perm = np.empty(max(self.n, 1), np.int64)
+            inv = np.empty(max(self.n, 1), np.int64)
+            _check(_L.lib().ssb_graph_export(self._h, _p(col), _p(cs), _p(cl), _p(perm), _p(inv)))
+            self._host = dict(col=col[: self.n_cells], cs=cs[: self.n_chunks], cl=cl[: self.n_chunks],
+                              perm=perm[: self.n], inv_perm=inv[: self.n])
+        return self._host
+
+    col = property(lambda self: self._export()["col"])
+    cs = property(lambda self: self._export()["cs"])
+    cl = property(lambda self: self._export()["cl"])
+    perm = property(lambda self: self._export()["perm"])
+    inv_perm = property(lambda self: self._export()["inv_perm"])
+
+    def col32(self) -> np.ndarray:
+        out = np.empty(max(self.n_cells, 1), np.int32)
+        _check(_L.lib().ssb_graph_export_col32(self._h, _p(out, _L.i32p)))
+        return out[: self.n_cells]
+
+    def chunk_row_begin(self, chunk: int) -> int:  # repr.hpp:47
+        return chunk * self.C
+
+    def chunk_row_end(self, chunk: int) -> int:  # repr.hpp:51-54
+        return min((chunk + 1) * self.C, self.n)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _L._lib is not None:
+            _L._lib.ssb_graph_destroy(h)
+            self._h = None
+
+
+def build_slimsell(g: Graph, C_: int, sigma: int) -> SlimSellRepr:  # repr.hpp:66
+    h = C.c_void_p()
+    _check(_L.lib().ssb_build_slimsell(g._h, C_, sigma, C.byref(h)))
+    return SlimSellRepr(h)
+
+
+def repr_from_layout(n, C_, sigma, nonzeros, col, cs, cl, perm) -> SlimSellRepr:
+    """Upload a host SlimSellRepr's arrays (e.g. one built by the reference)."""
+    col, cs, cl, perm = (np.ascontiguousarray(a, dtype=np.int64) for a in (col, cs, cl, perm))
+    h = C.c_void_p()
+    _check(_L.lib().ssb_graph_from_layout(n, C_, sigma, nonzeros, _p(col) if col.size else None,
+                                          col.shape[0], _p(cs) if cs.size else None,
+                                          _p(cl) if cl.size else None, cs.shape[0],
+                                          _p(perm) if perm.size else None, C.byref(h)))
+    return SlimSellRepr(h)
+
+
+def spmv_step(r: SlimSellRepr, variant: Variant, x_prev, out=None, chunk_begin: int = 0,
+              chunk_end: int | None = None) -> np.ndarray:  # repr.hpp:90-98
+    x = np.ascontiguousarray(x_prev, dtype=np.int64)
+    if x.shape[0] != r.n_padded:
+        raise InvalidArgument(f"x_prev length {x.shape[0]}, expected {r.n_padded}")
+    if out is None:
+        out = np.zeros(r.n_padded, dtype=np.int64)
+    elif out.shape[0] != r.n_padded or out.dtype != np.int64 or not out.flags.c_contiguous:
+        raise InvalidArgument(f"out length {out.shape[0]}, expected {r.n_padded}")
+    ce = r.n_chunks if chunk_end is None else chunk_end
+    if r.n_padded == 0:
+        return out
+    _check(_L.lib().ssb_spmv_step(r._h, int(variant), _p(x), _p(out), chunk_begin, ce))
+    return out
+
+
+def _stats_list(buf, k):
+    return [IterStats(s.iteration, s.elapsed_ns, s.chunks_processed, s.chunks_skipped,
+                      s.subchunks_processed, s.columns_processed, s.frontier_size) for s in buf[:k]]
+
+
+def bfs_spmv(r: SlimSellRepr, root: int, opts: BfsOptions | None = None,
+             csr_for_parents: CsrView | None = None) -> BfsResult:  # bfs.hpp:80-81
+    """Algebraic BFS on the device. As the reference: sel-max always produces
+    parents when opts.want_parents; the other variants only when a CSR is
+    passed (they are derived from the distances, dp_transform semantics)."""
+    opts = opts or BfsOptions()
+    want = bool(opts.want_parents) and (opts.variant == Variant.selmax or csr_for_parents is not None)
+    o = opts._c()
+    o.want_parents = int(want)
+    n = r.n
+    dist = np.empty(max(n, 1), np.int64)
+    parent = np.empty(max(n, 1), np.int64)
+    plen = np.zeros(1, np.int64)
+    iters = np.zeros(1, np.int64)
+    cap = 4096
+    stats = (_L.IterStatsC * cap)()
+    rc = _L.lib().ssb_bfs_spmv(r._h, int(root), C.byref(o), _p(dist), _p(parent), _p(plen),
+                               stats, cap, _p(iters))
+    if rc not in (_L.SSB_OK, _L.SSB_ECAP):
+        _raise(rc)
+    k = int(iters[0])
+    if k > cap:  # very deep BFS: fetch all records
+        stats = (_L.IterStatsC * k)()
+        # rerun is not needed: stats beyond cap are dropped by the C-ABI; report what we have
+        k = cap
+    res = BfsResult(dist[:n].copy(), parent[: int(plen[0])].copy(), int(iters[0]), _stats_list(stats, k))
+    if rc == _L.SSB_ECAP:
+        raise BfsCapError(_L.lib().ssb_last_error().decode(), res)
+    return res
+
+
+class DeviceBfs:
+    """Benchmark-facing form: BFS results stay on the device (ssb_bfs_run)."""
+
+    def __init__(self, r: SlimSellRepr):
+        self.r = r
+        self._stats = (_L.IterStatsC * 4096)()
+
+    def run(self, root: int, opts: BfsOptions):
+        it = np.zeros(1, np.int64)
+        ms = C.c_double()
+        o = opts._c()
+        rc = _L.lib().ssb_bfs_run(self.r._h, int(root), C.byref(o), self._stats, 4096, _p(it), C.byref(ms))
+        if rc not in (_L.SSB_OK, _L.SSB_ECAP):
+            _raise(rc)
+        k = int(it[0])
+        return k, float(ms.value), _stats_list(self._stats, min(k, 4096)), rc
+
+    def fetch(self, want_parents: bool, dist=None, parent=None):
+        n = self.r.n
+        dist = np.empty(n, np.int64) if dist is None else dist
+        parent = np.empty(n, np.int64) if parent is None else parent
+        plen = np.zeros(1, np.int64)
+        _check(_L.lib().ssb_bfs_fetch(self.r._h, int(want_parents), _p(dist), _p(parent), _p(plen)))
+        return dist, parent[: int(plen[0])]
+
+    def edges_traversed(self) -> int:
+        m = np.zeros(1, np.int64)
+        _check(_L.lib().ssb_bfs_edges_traversed(self.r._h, _p(m)))
+        return int(m[0])

@@ -1,0 +1,928 @@
+// The BFS-SpMV engine on the device (north_star subsystems 2-4).
+//
+// Reference: bfs_spmv / BfsEngine (bfs.cpp:53-155, 222-246), the kernel
+// slim_segment_impl (repr.cpp:20-35), post_process_rows (semiring.cpp:90-124),
+// should_skip_chunk (semiring.cpp:130-150), is_converged (semiring.cpp:152-157),
+// plan_subchunks / combine_chunks (bfs.cpp:10-22, 205-220), selmax_parents
+// (bfs.cpp:94-101), dp_transform (semiring.cpp:159-187).
+//
+// State encoding: under BFS initial conditions every value
+// that reaches an output is a function of 1-bit state, so the engine keeps
+//   visited  — 1 bit per padded row (chunk i <-> word i when C = 32),
+//   F[2]     — the frontier of the previous / current iteration,
+//   S[3]     — a coarse summary of F (1 bit per 2^gshift words) for the part
+//              of F that does not fit in shared memory,
+//   level / parent — int32 per row, written once when the row is reached.
+// The per-semiring product for an unvisited row becomes
+//   tropical  min_u (d_u + 1)  -> "some frontier neighbour" -> d = k
+//   real      Σ f_u ≠ 0        -> "some frontier neighbour"
+//   boolean   ∨ f_u            -> "some frontier neighbour"
+//   sel-max   max_u (pos_u+1)  -> the largest frontier-neighbour position,
+//             i.e. the LAST hit of the row's ascending column list.
+// Visited rows never change any output, SlimWork skips chunks whose real rows
+// are all visited, and convergence is "no row newly reached" for every variant.
+//
+// Two engines:
+//  * C = 32 (warp width): one persistent cooperative kernel runs all
+//    iterations. Each CTA stages the frontier prefix + summary in shared
+//    memory, warps pull SlimChunk tasks (≤ 32 work units) from a per-iteration
+//    atomic counter, and each 8-lane group streams one unit column-major with
+//    128-bit loads (lane = 4 rows of one column), gathering frontier bits from
+//    shared memory. Split chunks combine through global atomics; the last unit
+//    finalises. Iterations are separated by grid.sync().
+//  * any other C: a straightforward row-per-thread engine driven from the
+//    host (the reference's small-C parity configurations).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <memory>
+
+#include "ssb_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ssb {
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kUnitsPerTask = 32;
+constexpr int kStatW = 8;  // int64 per iteration record
+// record: 0 frontier_size, 1 chunks_processed, 2 chunks_skipped,
+//         3 subchunks_processed, 4 columns_processed, 5 elapsed_ns
+constexpr int kItersPerLaunch = 1024;
+
+int env_int(const char* name, int def) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : def;
+}
+
+int grid_for(int64_t items, int threads = 256) {
+  const int64_t want = (items + threads - 1) / threads;
+  const int64_t cap = int64_t(num_sms()) * 32;
+  return int(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+#define GRID_STRIDE(i, count)                                                       \
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (count); \
+       i += int64_t(gridDim.x) * blockDim.x)
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0;" : "=l"(p));
+  return p;
+}
+
+// Streaming 128-bit load of col: read-only for the kernel, not kept in L1,
+// marked evict-first in L2 so the 8.5 GB stream does not push the frontier
+// bitmap out of the 126 MB L2.
+__device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+struct Args32 {
+  const int32_t* col;
+  const int64_t* cs;
+  const int32_t* cl;
+  const ssb_unit* units;
+  const int32_t* task_begin;
+  const int32_t* split_units;
+  uint32_t* split_hit;
+  int32_t* split_best;
+  uint32_t* split_count;
+  uint32_t* visited;
+  uint32_t* F0;
+  uint32_t* F1;
+  uint32_t* S0;
+  uint32_t* S1;
+  uint32_t* S2;
+  int32_t* level;
+  int32_t* parent;
+  int64_t* stats;      // [kItersPerLaunch][kStatW]
+  uint32_t* task_ctr;  // [kItersPerLaunch]
+  int32_t n_tasks;
+  int32_t n_chunks;
+  int32_t PW;      // frontier prefix words staged in shared memory
+  int32_t SW;      // summary words staged in shared memory
+  int32_t gshift;  // summary granularity: 2^gshift frontier words per bit
+  int32_t L;       // slimchunk_len for the subchunk counter (0 = off)
+  int32_t slimwork;
+  int32_t root_code;  // sel-max parent position recorded at iteration 1
+  uint32_t last_real;  // real-row mask of the last chunk
+  int32_t k_begin;
+  int32_t k_end;
+};
+
+// Frontier bit of permuted vertex c (c >= 0): prefix from shared memory,
+// the rest only when the shared summary says its word group is non-empty.
+__device__ __forceinline__ uint32_t probe(int32_t c, const uint32_t* fine, const uint32_t* summ,
+                                          const uint32_t* Fc, int32_t PW, int32_t gshift) {
+  const int32_t w = c >> 5;
+  uint32_t word;
+  if (w < PW) {
+    word = fine[w];
+  } else {
+    const int32_t gi = (w - PW) >> gshift;
+    word = ((summ[gi >> 5] >> (gi & 31)) & 1u) ? Fc[w] : 0u;
+  }
+  return (word >> (c & 31)) & 1u;
+}
+
+template <bool kSelMax>
+__device__ __forceinline__ void take_cells(const int4 v, const uint32_t* fine, const uint32_t* summ,
+                                           const uint32_t* Fc, int32_t PW, int32_t gshift,
+                                           uint32_t& hit, int32_t (&best)[4]) {
+  const int32_t c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (c[q] >= 0) {
+      const uint32_t b = probe(c[q], fine, summ, Fc, PW, gshift);
+      if (kSelMax) {
+        // ascending columns: the last hit is the max frontier position
+        best[q] = b ? c[q] : best[q];
+      } else {
+        hit |= b << q;
+      }
+    }
+  }
+}
+
+template <bool kSelMax>
+__global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
+  extern __shared__ uint4 smem_v4[];
+  uint32_t* fine = reinterpret_cast<uint32_t*>(smem_v4);
+  uint32_t* summ = fine + a.PW;
+  __shared__ unsigned long long blk[5];
+
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int grp = lane >> 3;  // 8-lane group: one work unit
+  const int lg = lane & 7;    // rows 4*lg .. 4*lg+3 of the unit's chunk
+  const uint32_t gmask = 0xffu << (grp * 8);
+  const uint64_t pol = evict_first_policy();
+  uint64_t t_prev = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
+
+  for (int32_t k = a.k_begin; k < a.k_end; ++k) {
+    const int32_t rec = k - a.k_begin;
+    const uint32_t* Fc = ((k - 1) & 1) ? a.F1 : a.F0;
+    uint32_t* Fn = (k & 1) ? a.F1 : a.F0;
+    const int32_t km3 = (k - 1) % 3;
+    const uint32_t* Sc = km3 == 0 ? a.S0 : (km3 == 1 ? a.S1 : a.S2);
+    uint32_t* Sn = (k % 3) == 0 ? a.S0 : ((k % 3) == 1 ? a.S1 : a.S2);
+    uint32_t* Sx = ((k + 1) % 3) == 0 ? a.S0 : (((k + 1) % 3) == 1 ? a.S1 : a.S2);
+
+    // -- stage the frontier prefix and the summary into shared memory -------
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(Fc);
+      uint4* dst = smem_v4;
+      for (int i = threadIdx.x; i < (a.PW >> 2); i += kThreads) dst[i] = src[i];
+      const uint4* ssrc = reinterpret_cast<const uint4*>(Sc);
+      uint4* sdst = reinterpret_cast<uint4*>(summ);
+      for (int i = threadIdx.x; i < (a.SW >> 2); i += kThreads) sdst[i] = ssrc[i];
+      // clear the summary buffer of iteration k+1 (last read at k-1)
+      for (int i = blockIdx.x * kThreads + threadIdx.x; i < a.SW; i += gridDim.x * kThreads)
+        Sx[i] = 0u;
+      if (threadIdx.x < 5) blk[threadIdx.x] = 0ull;
+    }
+    __syncthreads();
+
+    unsigned long long c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
+
+    for (;;) {
+      int32_t t = 0;
+      if (lane == 0) t = int32_t(atomicAdd(&a.task_ctr[rec], 1u));
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= a.n_tasks) break;
+      const int32_t ub = a.task_begin[t], ue = a.task_begin[t + 1];
+
+      // window: lane l owns unit ub + l
+      const int32_t u = ub + lane;
+      const bool has = u < ue;
+      ssb_unit U = {0, 0, 0, -1};
+      uint32_t vis = 0, realm = 0;
+      bool skip = false;
+      if (has) {
+        U = a.units[u];
+        vis = a.visited[U.chunk];
+        realm = U.chunk == a.n_chunks - 1 ? a.last_real : 0xffffffffu;
+        skip = a.slimwork && vis == realm;  // should_skip_chunk
+        if (U.col_begin == 0) {
+          if (skip) {
+            ++c_skip;
+            Fn[U.chunk] = 0u;
+          } else {
+            const int32_t len = U.split < 0 ? U.col_len : a.cl[U.chunk];
+            ++c_proc;
+            c_cols += uint32_t(len);
+            if (a.L > 0 && len > 0) c_sub += uint32_t((len + a.L - 1) / a.L);
+          }
+        }
+      }
+      uint32_t active = __ballot_sync(0xffffffffu, has && !skip);
+
+      while (active) {
+        // the next (up to) four active units, one per 8-lane group
+        int32_t src = -1;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int32_t f = active ? __ffs(active) - 1 : -1;
+          if (g == grp) src = f;
+          if (active) active &= active - 1;
+        }
+        const int32_t sl = src < 0 ? 0 : src;
+        const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
+        const int32_t cb = __shfl_sync(0xffffffffu, U.col_begin, sl);
+        const int32_t len = src < 0 ? 0 : __shfl_sync(0xffffffffu, U.col_len, sl);
+        const int32_t split = __shfl_sync(0xffffffffu, U.split, sl);
+        const uint32_t uvis = __shfl_sync(0xffffffffu, vis, sl);
+        const uint32_t ureal = __shfl_sync(0xffffffffu, realm, sl);
+        int32_t maxlen = len;
+        maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, 8));
+        maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, 16));
+
+        const int4* p = reinterpret_cast<const int4*>(a.col + (src < 0 ? 0 : a.cs[chunk]) +
+                                                      int64_t(cb) * 32) + lg;
+        uint32_t hit = 0;
+        int32_t best[4] = {-1, -1, -1, -1};
+        int32_t j = 0;
+        for (; j + 4 <= maxlen; j += 4) {
+          int4 v[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            v[x] = (j + x < len) ? ld_stream(p + int64_t(j + x) * 8, pol) : make_int4(-1, -1, -1, -1);
+#pragma unroll
+          for (int x = 0; x < 4; ++x) take_cells<kSelMax>(v[x], fine, summ, Fc, a.PW, a.gshift, hit, best);
+        }
+        for (; j < maxlen; ++j) {
+          const int4 v = j < len ? ld_stream(p + int64_t(j) * 8, pol) : make_int4(-1, -1, -1, -1);
+          take_cells<kSelMax>(v, fine, summ, Fc, a.PW, a.gshift, hit, best);
+        }
+        if (kSelMax) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hit |= uint32_t(best[q] >= 0) << q;
+        }
+        // 32-bit row mask of the unit (rows 4*lg+q)
+        uint32_t m = hit << (4 * lg);
+        m |= __shfl_xor_sync(0xffffffffu, m, 1);
+        m |= __shfl_xor_sync(0xffffffffu, m, 2);
+        m |= __shfl_xor_sync(0xffffffffu, m, 4);
+
+        // SlimChunk combine (bfs.cpp:205-220): partial results of a split chunk
+        // meet in a scratch slot; the unit that arrives last finalises.
+        bool fin = src >= 0 && split < 0;
+        const bool sp = src >= 0 && split >= 0;
+        if (sp) {
+          if (lg == 0 && m) atomicOr(&a.split_hit[split], m);
+          if (kSelMax) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (best[q] >= 0) atomicMax(&a.split_best[split * 32 + 4 * lg + q], best[q]);
+          }
+          __threadfence();
+        }
+        __syncwarp();
+        uint32_t last = 0;
+        if (sp && lg == 0) {
+          const uint32_t arrived = atomicAdd(&a.split_count[split], 1u) + 1u;
+          last = arrived == uint32_t(a.split_units[split]);
+        }
+        last = __shfl_sync(0xffffffffu, last, grp * 8);
+        if (sp && last) {
+          __threadfence();
+          fin = true;
+          if (lg == 0) {
+            m = atomicExch(&a.split_hit[split], 0u);
+            a.split_count[split] = 0u;
+          }
+          m = __shfl_sync(gmask, m, grp * 8, 32);
+          if (kSelMax) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) best[q] = atomicExch(&a.split_best[split * 32 + 4 * lg + q], -1);
+          }
+        }
+        // finalise the chunk (post_process_rows, semiring.cpp:90-124)
+        if (fin) {
+          const uint32_t newly = m & ~uvis & ureal;
+          if (lg == 0) {
+            Fn[chunk] = newly;
+            if (newly) {
+              a.visited[chunk] = uvis | newly;
+              if (chunk >= a.PW) {
+                const int32_t gi = (chunk - a.PW) >> a.gshift;
+                atomicOr(&Sn[gi >> 5], 1u << (gi & 31));
+              }
+              c_front += __popc(newly);
+            }
+          }
+          if (newly) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int32_t r = 4 * lg + q;
+              if ((newly >> r) & 1u) {
+                const int64_t row = int64_t(chunk) * 32 + r;
+                a.level[row] = k;
+                if (kSelMax) a.parent[row] = k == 1 ? a.root_code : best[q];
+              }
+            }
+          }
+        }
+      }
+    }
+
+    // -- iteration counters: warp -> block -> grid --------------------------
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c_front += __shfl_xor_sync(0xffffffffu, c_front, o);
+      c_proc += __shfl_xor_sync(0xffffffffu, c_proc, o);
+      c_skip += __shfl_xor_sync(0xffffffffu, c_skip, o);
+      c_sub += __shfl_xor_sync(0xffffffffu, c_sub, o);
+      c_cols += __shfl_xor_sync(0xffffffffu, c_cols, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&blk[0], c_front);
+      atomicAdd(&blk[1], c_proc);
+      atomicAdd(&blk[2], c_skip);
+      atomicAdd(&blk[3], c_sub);
+      atomicAdd(&blk[4], c_cols);
+    }
+    __syncthreads();
+    if (threadIdx.x < 5)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[rec * kStatW + threadIdx.x]),
+                blk[threadIdx.x]);
+    grid.sync();
+    const int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const uint64_t t = globaltimer();
+      a.stats[rec * kStatW + 5] = int64_t(t - t_prev);
+      t_prev = t;
+    }
+    if (front == 0) break;  // is_converged: no row newly reached
+  }
+}
+
+// ---- generic engine (any C) ------------------------------------------------
+
+struct ArgsG {
+  const int32_t* col;
+  const int64_t* cs;
+  const int32_t* cl;
+  int64_t C, n, n_chunks;
+  uint8_t* vis;    // n_padded
+  uint8_t* fcur;   // n_padded
+  uint8_t* fnext;  // n_padded
+  uint8_t* skip;   // n_chunks
+  int32_t* level;
+  int32_t* parent;
+  unsigned long long* stats;  // one record
+  int32_t L, slimwork, root_code, k, selmax;
+};
+
+__global__ void gen_chunk_kernel(ArgsG a) {
+  unsigned long long proc = 0, skp = 0, sub = 0, cols = 0;
+  GRID_STRIDE(i, a.n_chunks) {
+    bool s = false;
+    if (a.slimwork) {
+      s = true;
+      const int64_t r1 = min((i + 1) * a.C, a.n);
+      for (int64_t r = i * a.C; r < r1 && s; ++r) s = a.vis[r] != 0;
+    }
+    a.skip[i] = s;
+    if (s) ++skp;
+    else {
+      ++proc;
+      cols += uint32_t(a.cl[i]);
+      if (a.L > 0 && a.cl[i] > 0) sub += uint32_t((a.cl[i] + a.L - 1) / a.L);
+    }
+  }
+  if (proc) atomicAdd(&a.stats[1], proc);
+  if (skp) atomicAdd(&a.stats[2], skp);
+  if (sub) atomicAdd(&a.stats[3], sub);
+  if (cols) atomicAdd(&a.stats[4], cols);
+}
+
+__global__ void gen_sweep_kernel(ArgsG a) {
+  unsigned long long front = 0;
+  GRID_STRIDE(r, a.n_chunks * a.C) {
+    const int64_t ch = r / a.C, lane = r % a.C;
+    uint8_t nw = 0;
+    if (!a.skip[ch]) {
+      const int32_t* cells = a.col + a.cs[ch] + lane;
+      int32_t best = -1;
+      for (int32_t j = 0; j < a.cl[ch]; ++j) {
+        const int32_t c = cells[int64_t(j) * a.C];
+        if (c >= 0 && a.fcur[c]) best = c;
+      }
+      if (best >= 0 && r < a.n && !a.vis[r]) {
+        nw = 1;
+        a.vis[r] = 1;
+        a.level[r] = a.k;
+        if (a.selmax) a.parent[r] = a.k == 1 ? a.root_code : best;
+        ++front;
+      }
+    }
+    a.fnext[r] = nw;
+  }
+  if (front) atomicAdd(&a.stats[0], front);
+}
+
+// ---- shared init / epilogue kernels ---------------------------------------
+
+__global__ void set_root_kernel(uint32_t* visited, uint32_t* F0, uint32_t* S0, int32_t* level,
+                                int32_t* parent, int32_t root_pos, int32_t root_code, int32_t PW,
+                                int32_t gshift) {
+  const int32_t w = root_pos >> 5;
+  visited[w] |= 1u << (root_pos & 31);
+  F0[w] |= 1u << (root_pos & 31);
+  if (S0 && w >= PW) {
+    const int32_t gi = (w - PW) >> gshift;
+    S0[gi >> 5] |= 1u << (gi & 31);
+  }
+  level[root_pos] = 0;
+  parent[root_pos] = root_code;
+}
+
+__global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_padded,
+                                     uint32_t* __restrict__ bits) {
+  GRID_STRIDE(w, (n_padded + 31) / 32) {
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t r = w * 32 + b;
+      if (r < n_padded && vis[r]) v |= 1u << b;
+    }
+    bits[w] = v;
+  }
+}
+
+// permute_out (repr.cpp:247-253) + selmax_parents (bfs.cpp:94-101): results in
+// original ids; sel-max positions decode through perm exactly like the
+// reference, including its root encoding when compat is on.
+__global__ void unpermute_kernel(const uint32_t* __restrict__ visited,
+                                 const int32_t* __restrict__ level,
+                                 const int32_t* __restrict__ parent,
+                                 const int32_t* __restrict__ perm, int64_t n, int selmax_parents,
+                                 int64_t* __restrict__ dist, int64_t* __restrict__ par) {
+  GRID_STRIDE(p, n) {
+    const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
+    const int32_t o = perm[p];
+    dist[o] = reached ? int64_t(level[p]) : INT64_MAX;
+    if (selmax_parents) par[o] = reached ? int64_t(perm[parent[p]]) : -1;
+  }
+}
+
+// dp_transform (semiring.cpp:159-187) on the layout: the smallest ORIGINAL id
+// among the row's neighbours one level closer; root self-parented.
+__global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t* __restrict__ cs,
+                                 const int32_t* __restrict__ cl, int64_t C,
+                                 const uint32_t* __restrict__ visited,
+                                 const int32_t* __restrict__ level,
+                                 const int32_t* __restrict__ perm, int64_t n,
+                                 int64_t* __restrict__ par, int* __restrict__ bad) {
+  GRID_STRIDE(p, n) {
+    const int32_t o = perm[p];
+    if (!((visited[p >> 5] >> (p & 31)) & 1u)) {
+      par[o] = -1;
+      continue;
+    }
+    const int32_t lv = level[p];
+    if (lv == 0) {
+      par[o] = o;
+      continue;
+    }
+    const int64_t ch = p / C, lane = p % C;
+    const int32_t* cells = col + cs[ch] + lane;
+    int32_t bestp = INT_MAX;
+    for (int32_t j = 0; j < cl[ch]; ++j) {
+      const int32_t c = cells[int64_t(j) * C];
+      if (c < 0) break;
+      if (((visited[c >> 5] >> (c & 31)) & 1u) && level[c] == lv - 1) bestp = min(bestp, perm[c]);
+    }
+    if (bestp == INT_MAX) atomicOr(bad, 1);
+    par[o] = bestp == INT_MAX ? -1 : bestp;
+  }
+}
+
+__global__ void reached_degree_kernel(const uint32_t* __restrict__ visited,
+                                      const int32_t* __restrict__ deg, int64_t n,
+                                      unsigned long long* __restrict__ out) {
+  unsigned long long s = 0;
+  GRID_STRIDE(p, n) {
+    if ((visited[p >> 5] >> (p & 31)) & 1u) s += uint32_t(deg[p]);
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+// ---- host side ---------------------------------------------------------------
+
+struct Geometry {
+  int64_t NW = 0;  // bitmap words
+  int32_t PW = 0, SW = 0, gshift = 0;
+  size_t smem = 0;
+};
+
+Geometry geometry32(const ssb_graph& g) {
+  Geometry G;
+  G.NW = (g.n_padded + 31) / 32;
+  const int64_t budget_words = int64_t(env_int("SSB_SMEM_KB", 200)) * 1024 / 4;
+  const int64_t nw4 = (G.NW + 3) & ~int64_t(3);
+  if (nw4 <= budget_words) {
+    G.PW = int32_t(nw4);
+    G.SW = 0;
+    G.gshift = 0;
+  } else {
+    const int64_t sum_budget = budget_words * env_int("SSB_SUMMARY_PCT", 25) / 100;
+    int gs = env_int("SSB_GSHIFT", -1);
+    if (gs < 0) {
+      gs = 0;
+      while ((((G.NW >> gs) + 31) / 32 + 3) / 4 * 4 > sum_budget) ++gs;
+    }
+    G.gshift = gs;
+    G.SW = int32_t(((((G.NW + (int64_t{1} << gs) - 1) >> gs) + 31) / 32 + 3) / 4 * 4);
+    G.PW = int32_t(std::max<int64_t>(0, (budget_words - G.SW)) & ~int64_t(3));
+  }
+  G.smem = size_t(G.PW + G.SW) * 4;
+  return G;
+}
+
+// Work units + tasks for the C=32 engine. A unit is a SlimChunk segment of at
+// most L columns (the whole chunk when L <= 0, as the reference's task list,
+// bfs.cpp:122-138); a task groups up to 32 consecutive units whose cost stays
+// under a budget, the grain of the dynamic scheduler.
+void build_plan32(ssb_graph& g, int64_t L) {
+  ssb_bfs_plan& P = g.plan;
+  if (P.L == L && P.n_units > 0) return;
+  std::vector<ssb_unit> units;
+  std::vector<int32_t> split_units;
+  units.reserve(g.n_chunks + 16);
+  for (int64_t i = 0; i < g.n_chunks; ++i) {
+    const int64_t cl = g.cl_host[i];
+    if (L <= 0 || cl <= L) {
+      units.push_back({int32_t(i), 0, int32_t(cl), -1});
+    } else {
+      const int32_t sp = int32_t(split_units.size());
+      const int64_t nseg = (cl + L - 1) / L;
+      split_units.push_back(int32_t(nseg));
+      for (int64_t s = 0; s < nseg; ++s)
+        units.push_back({int32_t(i), int32_t(s * L), int32_t(std::min(L, cl - s * L)), sp});
+    }
+  }
+  const int64_t budget = env_int("SSB_TASK_BUDGET", 512);
+  const int64_t overhead = env_int("SSB_UNIT_OVERHEAD", 4);
+  std::vector<int32_t> tb;
+  tb.push_back(0);
+  int64_t cost = 0, cnt = 0;
+  for (size_t u = 0; u < units.size(); ++u) {
+    cost += units[u].col_len + overhead;
+    ++cnt;
+    if (cnt == kUnitsPerTask || cost >= budget) {
+      tb.push_back(int32_t(u + 1));
+      cost = 0;
+      cnt = 0;
+    }
+  }
+  if (cnt) tb.push_back(int32_t(units.size()));
+  if (units.size() >= size_t(INT32_MAX)) fail(SSB_EINVAL, "too many work units");
+  cudaStream_t s = g.sc.s;
+  P.L = L;
+  P.n_units = int64_t(units.size());
+  P.n_tasks = int64_t(tb.size()) - 1;
+  P.n_split = int64_t(split_units.size());
+  P.units.alloc(units.size());
+  P.task_begin.alloc(tb.size());
+  P.split_units.alloc(std::max<size_t>(split_units.size(), 1));
+  P.split_hit.alloc(std::max<size_t>(split_units.size(), 1));
+  P.split_best.alloc(std::max<size_t>(split_units.size(), 1) * 32);
+  P.split_count.alloc(std::max<size_t>(split_units.size(), 1));
+  SSB_CUDA(cudaMemcpyAsync(P.units.p, units.data(), sizeof(ssb_unit) * units.size(),
+                           cudaMemcpyHostToDevice, s));
+  SSB_CUDA(cudaMemcpyAsync(P.task_begin.p, tb.data(), 4 * tb.size(), cudaMemcpyHostToDevice, s));
+  if (!split_units.empty())
+    SSB_CUDA(cudaMemcpyAsync(P.split_units.p, split_units.data(), 4 * split_units.size(),
+                             cudaMemcpyHostToDevice, s));
+  SSB_CUDA(cudaMemsetAsync(P.split_hit.p, 0, P.split_hit.bytes(), s));
+  SSB_CUDA(cudaMemsetAsync(P.split_best.p, 0xff, P.split_best.bytes(), s));
+  SSB_CUDA(cudaMemsetAsync(P.split_count.p, 0, P.split_count.bytes(), s));
+  g.sc.sync();
+}
+
+// bits layout: visited | F0 | F1 | S0 | S1 | S2 (each region 16-byte aligned)
+struct BitRegions {
+  int64_t NW4, SW4;
+  uint32_t *visited, *F0, *F1, *S0, *S1, *S2;
+};
+
+BitRegions bit_regions(ssb_graph& g, int64_t SW) {
+  BitRegions R;
+  R.NW4 = ((g.n_padded + 31) / 32 + 3) & ~int64_t(3);
+  R.SW4 = std::max<int64_t>((SW + 3) & ~int64_t(3), 4);
+  g.bits.ensure(size_t(3 * R.NW4 + 3 * R.SW4));
+  R.visited = g.bits.p;
+  R.F0 = R.visited + R.NW4;
+  R.F1 = R.F0 + R.NW4;
+  R.S0 = R.F1 + R.NW4;
+  R.S1 = R.S0 + R.SW4;
+  R.S2 = R.S1 + R.SW4;
+  return R;
+}
+
+void collect_stats(const std::vector<int64_t>& rec, int64_t k0, int64_t count,
+                   std::vector<ssb_iter_stats>& out) {
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t* r = rec.data() + i * kStatW;
+    ssb_iter_stats s;
+    s.iteration = k0 + i;
+    s.elapsed_ns = r[5];
+    s.chunks_processed = r[1];
+    s.chunks_skipped = r[2];
+    s.subchunks_processed = r[3];
+    s.columns_processed = r[4];
+    s.frontier_size = r[0];
+    out.push_back(s);
+  }
+}
+
+template <bool kSel>
+void configure32() {
+  static bool done = false;
+  if (!done) {
+    SSB_CUDA(cudaFuncSetAttribute(bfs32_kernel<kSel>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    done = true;
+  }
+}
+
+// Returns true when converged; appends per-iteration stats.
+bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
+           int64_t cap, std::vector<ssb_iter_stats>& stats) {
+  cudaStream_t s = g.sc.s;
+  const bool sel = o.variant == SSB_SELMAX;
+  build_plan32(g, o.slimchunk_len);
+  const Geometry G = geometry32(g);
+  BitRegions R = bit_regions(g, G.SW);
+  g.level.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
+  g.parent.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
+  g.dstats.ensure(size_t(kItersPerLaunch) * kStatW);
+  g.dctrl.ensure(size_t(kItersPerLaunch));
+
+  // init_state (semiring.cpp:56-88) in 1-bit form
+  SSB_CUDA(cudaMemsetAsync(R.visited, 0, size_t(R.NW4) * 4 * 2, s));  // visited + F0
+  SSB_CUDA(cudaMemsetAsync(R.S0, 0, size_t(R.SW4) * 4 * 3, s));
+  set_root_kernel<<<1, 1, 0, s>>>(R.visited, R.F0, G.SW ? R.S0 : nullptr, g.level.p, g.parent.p,
+                                  root_pos, root_code, G.PW, G.gshift);
+  SSB_CUDA(cudaGetLastError());
+
+  if (sel) configure32<true>(); else configure32<false>();
+  int per_sm = 0;
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, kThreads,
+      G.smem));
+  if (per_sm < 1) fail(SSB_ECUDA, "bfs32 kernel does not fit on an SM");
+  const int grid = num_sms();
+
+  Args32 a;
+  a.col = g.col.p;
+  a.cs = g.cs.p;
+  a.cl = g.cl.p;
+  a.units = g.plan.units.p;
+  a.task_begin = g.plan.task_begin.p;
+  a.split_units = g.plan.split_units.p;
+  a.split_hit = g.plan.split_hit.p;
+  a.split_best = g.plan.split_best.p;
+  a.split_count = g.plan.split_count.p;
+  a.visited = R.visited;
+  a.F0 = R.F0;
+  a.F1 = R.F1;
+  a.S0 = R.S0;
+  a.S1 = R.S1;
+  a.S2 = R.S2;
+  a.level = g.level.p;
+  a.parent = g.parent.p;
+  a.stats = g.dstats.p;
+  a.task_ctr = g.dctrl.p;
+  a.n_tasks = int32_t(g.plan.n_tasks);
+  a.n_chunks = int32_t(g.n_chunks);
+  a.PW = G.PW;
+  a.SW = G.SW;
+  a.gshift = G.gshift;
+  a.L = int32_t(std::max<int64_t>(0, std::min<int64_t>(o.slimchunk_len, INT32_MAX)));
+  a.slimwork = o.slimwork ? 1 : 0;
+  a.root_code = root_code;
+  {
+    const int64_t real_last = g.n - (g.n_chunks - 1) * 32;  // 1..32
+    a.last_real = real_last >= 32 ? 0xffffffffu : ((1u << real_last) - 1u);
+  }
+  std::vector<int64_t> rec(size_t(kItersPerLaunch) * kStatW);
+  int64_t k = 1;
+  while (k <= cap) {
+    const int64_t kend = std::min<int64_t>(cap + 1, k + kItersPerLaunch);
+    a.k_begin = int32_t(k);
+    a.k_end = int32_t(kend);
+    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, g.dstats.bytes(), s));
+    SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
+    void* params[] = {&a};
+    SSB_CUDA(cudaLaunchCooperativeKernel(
+        sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, dim3(grid),
+        dim3(kThreads), params, G.smem, s));
+    SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, rec.size() * 8, cudaMemcpyDeviceToHost, s));
+    g.sc.sync();
+    // the launch ran iterations k .. until a record with frontier 0 or kend
+    int64_t ran = 0;
+    bool conv = false;
+    for (int64_t i = 0; i < kend - k; ++i) {
+      ++ran;
+      if (rec[size_t(i) * kStatW] == 0) {
+        conv = true;
+        break;
+      }
+    }
+    collect_stats(rec, k, ran, stats);
+    if (conv) return true;
+    k += ran;
+  }
+  return false;
+}
+
+bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
+                 int64_t cap, std::vector<ssb_iter_stats>& stats) {
+  cudaStream_t s = g.sc.s;
+  const int64_t np = g.n_padded;
+  g.level.ensure(size_t(std::max<int64_t>(np, 1)));
+  g.parent.ensure(size_t(std::max<int64_t>(np, 1)));
+  g.gbytes.ensure(size_t(3 * np + g.n_chunks + 16));
+  g.dstats.ensure(kStatW);
+  uint8_t* vis = g.gbytes.p;
+  uint8_t* f0 = vis + np;
+  uint8_t* f1 = f0 + np;
+  uint8_t* skip = f1 + np;
+  SSB_CUDA(cudaMemsetAsync(vis, 0, size_t(2 * np), s));
+  const uint8_t one = 1;
+  SSB_CUDA(cudaMemcpyAsync(vis + root_pos, &one, 1, cudaMemcpyHostToDevice, s));
+  SSB_CUDA(cudaMemcpyAsync(f0 + root_pos, &one, 1, cudaMemcpyHostToDevice, s));
+  const int32_t zero = 0;
+  SSB_CUDA(cudaMemcpyAsync(g.level.p + root_pos, &zero, 4, cudaMemcpyHostToDevice, s));
+  SSB_CUDA(cudaMemcpyAsync(g.parent.p + root_pos, &root_code, 4, cudaMemcpyHostToDevice, s));
+  ArgsG a;
+  a.col = g.col.p;
+  a.cs = g.cs.p;
+  a.cl = g.cl.p;
+  a.C = g.C;
+  a.n = g.n;
+  a.n_chunks = g.n_chunks;
+  a.vis = vis;
+  a.skip = skip;
+  a.level = g.level.p;
+  a.parent = g.parent.p;
+  a.stats = reinterpret_cast<unsigned long long*>(g.dstats.p);
+  a.L = int32_t(std::max<int64_t>(0, std::min<int64_t>(o.slimchunk_len, INT32_MAX)));
+  a.slimwork = o.slimwork ? 1 : 0;
+  a.root_code = root_code;
+  a.selmax = o.variant == SSB_SELMAX;
+  bool conv = false;
+  std::vector<int64_t> rec(kStatW);
+  for (int64_t k = 1; k <= cap && !conv; ++k) {
+    a.k = int32_t(k);
+    a.fcur = (k & 1) ? f0 : f1;
+    a.fnext = (k & 1) ? f1 : f0;
+    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, kStatW * 8, s));
+    SSB_CUDA(cudaEventRecord(g.sc.e0, s));
+    if (g.n_chunks) {
+      gen_chunk_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(a);
+      gen_sweep_kernel<<<grid_for(np), 256, 0, s>>>(a);
+    }
+    SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaEventRecord(g.sc.e1, s));
+    SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, kStatW * 8, cudaMemcpyDeviceToHost, s));
+    g.sc.sync();
+    float ms = 0;
+    SSB_CUDA(cudaEventElapsedTime(&ms, g.sc.e0, g.sc.e1));
+    rec[5] = int64_t(double(ms) * 1e6);
+    collect_stats(rec, k, 1, stats);
+    conv = rec[0] == 0;
+  }
+  // the shared epilogue reads the visited bitmap
+  BitRegions R = bit_regions(g, 0);
+  bytes_to_bits_kernel<<<grid_for((np + 31) / 32), 256, 0, s>>>(vis, np, R.visited);
+  SSB_CUDA(cudaGetLastError());
+  g.sc.sync();
+  return conv;
+}
+
+}  // namespace
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return v;
+  }();
+  return sms;
+}
+
+int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats,
+            int64_t stats_cap, int64_t* iterations, double* device_ms) {
+  if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
+  // semiring.cpp:57-60
+  if (root < 0 || root >= g.n)
+    fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g.n) + ")");
+  g.last_valid = false;
+  const int32_t root_pos = [&] {
+    int32_t p = 0;
+    SSB_CUDA(cudaMemcpy(&p, g.inv_perm.p + root, 4, cudaMemcpyDeviceToHost));
+    return p;
+  }();
+  // sel-max: the reference seeds x[root] = root+1 in ORIGINAL numbering and
+  // decodes it as a position; compat keeps that encoding.
+  const int32_t root_code = (o.variant == SSB_SELMAX && o.selmax_compat) ? int32_t(root) : root_pos;
+  const int64_t cap = o.max_iterations > 0 ? o.max_iterations : g.n + 1;
+  std::vector<ssb_iter_stats> st;
+  SSB_CUDA(cudaEventRecord(g.sc.e0, g.sc.s));
+  cudaEvent_t t0, t1;
+  SSB_CUDA(cudaEventCreate(&t0));
+  SSB_CUDA(cudaEventCreate(&t1));
+  SSB_CUDA(cudaEventRecord(t0, g.sc.s));
+  bool conv;
+  try {
+    conv = g.C == 32 ? run32(g, root_pos, root_code, o, cap, st)
+                     : run_generic(g, root_pos, root_code, o, cap, st);
+  } catch (...) {
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    throw;
+  }
+  SSB_CUDA(cudaEventRecord(t1, g.sc.s));
+  SSB_CUDA(cudaEventSynchronize(t1));
+  float ms = 0;
+  SSB_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (device_ms) *device_ms = ms;
+  if (iterations) *iterations = int64_t(st.size());
+  if (stats)
+    for (int64_t i = 0; i < std::min<int64_t>(stats_cap, int64_t(st.size())); ++i) stats[i] = st[i];
+  g.last_root = root;
+  g.last_variant = o.variant;
+  g.last_compat = o.selmax_compat;
+  g.last_iterations = int64_t(st.size());
+  g.last_valid = true;
+  return conv ? SSB_OK : SSB_ECAP;
+}
+
+void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
+               int64_t* parent_len) {
+  if (!g.last_valid) fail(SSB_EINVAL, "no BFS result on this graph");
+  cudaStream_t s = g.sc.s;
+  const int64_t n = g.n;
+  BitRegions R = bit_regions(g, 0);  // visited is the first region for both engines
+  DevBuf<int64_t> dd(std::max<int64_t>(n, 1)), dp(std::max<int64_t>(n, 1));
+  const bool sel = g.last_variant == SSB_SELMAX;
+  unpermute_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p, n,
+                                               sel && want_parents, dd.p, dp.p);
+  SSB_CUDA(cudaGetLastError());
+  int64_t plen = 0;
+  if (want_parents && !sel) {
+    DevBuf<int> bad(1);
+    SSB_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+    dp_parent_kernel<<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
+                                                 g.level.p, g.perm.p, n, dp.p, bad.p);
+    SSB_CUDA(cudaGetLastError());
+    int hbad = 0;
+    SSB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    g.sc.sync();
+    if (hbad) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
+  }
+  if (want_parents) plen = n;
+  if (dist) SSB_CUDA(cudaMemcpyAsync(dist, dd.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (parent && plen) SSB_CUDA(cudaMemcpyAsync(parent, dp.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  g.sc.sync();
+  if (parent_len) *parent_len = plen;
+}
+
+int64_t bfs_edges_traversed(ssb_graph& g) {
+  if (!g.last_valid) fail(SSB_EINVAL, "no BFS result on this graph");
+  cudaStream_t s = g.sc.s;
+  BitRegions R = bit_regions(g, 0);
+  DevBuf<unsigned long long> acc(1);
+  SSB_CUDA(cudaMemsetAsync(acc.p, 0, 8, s));
+  reached_degree_kernel<<<grid_for(g.n), 256, 0, s>>>(R.visited, g.deg.p, g.n, acc.p);
+  SSB_CUDA(cudaGetLastError());
+  unsigned long long v = 0;
+  SSB_CUDA(cudaMemcpyAsync(&v, acc.p, 8, cudaMemcpyDeviceToHost, s));
+  g.sc.sync();
+  return int64_t(v / 2);
+}
+
+}  // namespace ssb

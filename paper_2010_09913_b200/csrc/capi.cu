@@ -1,0 +1,234 @@
+// extern "C" entry points of libslimsell_b200.so (include/slimsell_b200.h).
+// Each maps C++ exceptions to SSB_* status codes and a thread-local message,
+// mirroring the reference's exception contract.
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "ssb_internal.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SSB_OK;
+  } catch (const ssb::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = std::string("host allocation failed: ") + e.what();
+    return SSB_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SSB_ECUDA;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (p == nullptr) ssb::fail(SSB_EINVAL, std::string(what) + " is NULL");
+}
+}  // namespace
+
+extern "C" {
+
+const char* ssb_last_error(void) { return g_last_error.c_str(); }
+
+int ssb_abi_version(void) { return SSB_ABI_VERSION; }
+
+int ssb_set_device(int device) {
+  return guarded([&] { SSB_CUDA(cudaSetDevice(device)); });
+}
+
+int ssb_edges_from_pairs(const int64_t* uv, int64_t count, int64_t n, ssb_edges** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (count > 0) need(uv, "uv");
+    *out = ssb::edges_from_pairs(uv, count, n);
+  });
+}
+
+int ssb_gen_kronecker(int64_t scale, int64_t edgefactor, uint64_t seed,
+                      const double initiator[4], ssb_edges** out) {
+  return guarded([&] {
+    need(out, "out");
+    const double def[4] = {0.57, 0.19, 0.19, 0.05};
+    *out = ssb::gen_kronecker(scale, edgefactor, seed, initiator ? initiator : def);
+  });
+}
+
+int ssb_edges_info(const ssb_edges* e, int64_t* n, int64_t* m) {
+  return guarded([&] {
+    need(e, "edges");
+    if (n) *n = e->n;
+    if (m) *m = e->m;
+  });
+}
+
+int ssb_edges_export(const ssb_edges* e, int64_t* uv) {
+  return guarded([&] {
+    need(e, "edges");
+    need(uv, "uv");
+    if (e->m == 0) return;
+    ssb_edges& me = const_cast<ssb_edges&>(*e);
+    std::vector<uint64_t> keys(e->m);
+    SSB_CUDA(cudaMemcpyAsync(keys.data(), e->keys.p, 8 * e->m, cudaMemcpyDeviceToHost, me.sc.s));
+    me.sc.sync();
+    const uint64_t mask = (uint64_t{1} << e->bits) - 1;
+    for (int64_t i = 0; i < e->m; ++i) {
+      uv[2 * i] = int64_t(keys[i] >> e->bits);
+      uv[2 * i + 1] = int64_t(keys[i] & mask);
+    }
+  });
+}
+
+int ssb_to_csr(const ssb_edges* e, int64_t* row, int64_t* col) {
+  return guarded([&] {
+    need(e, "edges");
+    need(row, "row");
+    if (e->m) need(col, "col");
+    ssb::edges_to_csr(*e, row, col);
+  });
+}
+
+void ssb_edges_destroy(ssb_edges* e) { delete e; }
+
+int ssb_build_slimsell(const ssb_edges* e, int64_t C, int64_t sigma, ssb_graph** out) {
+  return guarded([&] {
+    need(e, "edges");
+    need(out, "out");
+    *out = ssb::build_from_edges(*e, C, sigma);
+  });
+}
+
+int ssb_graph_from_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
+                          const int64_t* col, int64_t n_cells, const int64_t* cs,
+                          const int64_t* cl, int64_t n_chunks, const int64_t* perm,
+                          ssb_graph** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (n_cells) need(col, "col");
+    if (n_chunks) { need(cs, "cs"); need(cl, "cl"); }
+    if (n) need(perm, "perm");
+    *out = ssb::graph_from_host_layout(n, C, sigma, nonzeros, col, n_cells, cs, cl, n_chunks, perm);
+  });
+}
+
+int ssb_graph_info(const ssb_graph* g, ssb_layout_info* info) {
+  return guarded([&] {
+    need(g, "graph");
+    need(info, "info");
+    info->C = g->C;
+    info->sigma = g->sigma;
+    info->n = g->n;
+    info->n_padded = g->n_padded;
+    info->n_chunks = g->n_chunks;
+    info->nonzeros = g->nonzeros;
+    info->n_cells = g->n_cells;
+    info->padding = g->padding;
+    info->max_chunk_len = g->max_cl;
+  });
+}
+
+int ssb_graph_export(const ssb_graph* cg, int64_t* col, int64_t* cs, int64_t* cl, int64_t* perm,
+                     int64_t* inv_perm) {
+  return guarded([&] {
+    need(cg, "graph");
+    ssb_graph& g = const_cast<ssb_graph&>(*cg);
+    cudaStream_t s = g.sc.s;
+    auto widen32 = [&](const int32_t* src, int64_t count, int64_t* dst) {
+      if (!dst || count == 0) return;
+      const int64_t slab = int64_t{1} << 26;
+      std::vector<int32_t> tmp(std::min(slab, count));
+      for (int64_t off = 0; off < count; off += slab) {
+        const int64_t c = std::min(slab, count - off);
+        SSB_CUDA(cudaMemcpyAsync(tmp.data(), src + off, 4 * c, cudaMemcpyDeviceToHost, s));
+        g.sc.sync();
+        for (int64_t i = 0; i < c; ++i) dst[off + i] = tmp[i];
+      }
+    };
+    widen32(g.col.p, g.n_cells, col);
+    if (cs && g.n_chunks) {
+      SSB_CUDA(cudaMemcpyAsync(cs, g.cs.p, 8 * g.n_chunks, cudaMemcpyDeviceToHost, s));
+      g.sc.sync();
+    }
+    widen32(g.cl.p, g.n_chunks, cl);
+    widen32(g.perm.p, g.n, perm);
+    widen32(g.inv_perm.p, g.n, inv_perm);
+  });
+}
+
+int ssb_graph_export_col32(const ssb_graph* cg, int32_t* col) {
+  return guarded([&] {
+    need(cg, "graph");
+    need(col, "col");
+    ssb_graph& g = const_cast<ssb_graph&>(*cg);
+    if (g.n_cells) {
+      SSB_CUDA(cudaMemcpyAsync(col, g.col.p, 4 * g.n_cells, cudaMemcpyDeviceToHost, g.sc.s));
+      g.sc.sync();
+    }
+  });
+}
+
+void ssb_graph_destroy(ssb_graph* g) { delete g; }
+
+int ssb_spmv_step(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* out,
+                  int64_t chunk_begin, int64_t chunk_end) {
+  return guarded([&] {
+    need(g, "graph");
+    need(x_prev, "x_prev");
+    need(out, "out");
+    ssb::spmv_step(*g, variant, x_prev, out, chunk_begin, chunk_end);
+  });
+}
+
+int ssb_bfs_run(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, ssb_iter_stats* stats,
+                int64_t stats_cap, int64_t* iterations, double* device_ms) {
+  int rc = SSB_OK;
+  const int st = guarded([&] {
+    need(g, "graph");
+    need(opts, "opts");
+    rc = ssb::bfs_run(*g, root, *opts, stats, stats_cap, iterations, device_ms);
+  });
+  if (st != SSB_OK) return st;
+  if (rc == SSB_ECAP) g_last_error = "iteration cap reached before fixed point";
+  return rc;
+}
+
+int ssb_bfs_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent,
+                  int64_t* parent_len) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::bfs_fetch(*g, want_parents, dist, parent, parent_len);
+  });
+}
+
+int ssb_bfs_spmv(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, int64_t* dist,
+                 int64_t* parent, int64_t* parent_len, ssb_iter_stats* stats,
+                 int64_t stats_cap, int64_t* iterations) {
+  int rc = ssb_bfs_run(g, root, opts, stats, stats_cap, iterations, nullptr);
+  if (rc != SSB_OK && rc != SSB_ECAP) return rc;
+  const std::string cap_msg = g_last_error;
+  // bfs.cpp:86-90: on the cap the partial result carries dist, no parents.
+  const int want = rc == SSB_OK && opts->want_parents && parent != nullptr;
+  const int f = guarded([&] {
+    need(dist, "dist");
+    ssb::bfs_fetch(*g, want, dist, want ? parent : nullptr, parent_len);
+  });
+  if (f != SSB_OK) return f;
+  if (rc == SSB_ECAP) g_last_error = cap_msg;
+  return rc;
+}
+
+int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc) {
+  return guarded([&] {
+    need(g, "graph");
+    need(m_cc, "m_cc");
+    *m_cc = ssb::bfs_edges_traversed(*g);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// Internal declarations shared by the sm_100a translation units of
+// libslimsell_b200.so. Not installed; the public surface is
+// include/slimsell_b200.h (C-ABI) and include/slimsell_b200/*.hpp (C++ façade).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "slimsell_b200.h"
+
+namespace ssb {
+
+// Status-carrying exception; the C-ABI layer maps it to SSB_* codes and the
+// thread-local last-error string.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    fail(e == cudaErrorMemoryAllocation ? SSB_ENOMEM : SSB_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+             std::to_string(line) + ")");
+  }
+}
+#define SSB_CUDA(x) ::ssb::cuda_check((x), #x, __FILE__, __LINE__)
+
+// RAII device buffer (cudaMalloc; stream-ordered frees are not needed here:
+// every C-ABI call is synchronous on return).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) SSB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void ensure(size_t count) { if (count > n) alloc(count); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// One stream + timing events per handle.
+struct StreamCtx {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  StreamCtx() {
+    SSB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SSB_CUDA(cudaEventCreate(&e0));
+    SSB_CUDA(cudaEventCreate(&e1));
+  }
+  ~StreamCtx() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+  }
+  void sync() { SSB_CUDA(cudaStreamSynchronize(s)); }
+};
+
+int num_sms();
+
+}  // namespace ssb
+
+// ---- opaque handle bodies --------------------------------------------------
+
+// Device-resident normalised edge set (the reference Graph, graph.hpp:31-51):
+// m keys (u << bits) | v with u < v, sorted ascending, unique.
+struct ssb_edges {
+  int64_t n = 0;
+  int64_t m = 0;
+  int bits = 1;  // bits per endpoint in a key
+  ssb::DevBuf<uint64_t> keys;
+  ssb::StreamCtx sc;
+};
+
+// Work unit of the C=32 engine: one SlimChunk segment (bfs.hpp:58-66).
+struct ssb_unit {
+  int32_t chunk;
+  int32_t col_begin;
+  int32_t col_len;
+  int32_t split;  // index of the split-chunk scratch slot, -1 = whole chunk
+};
+
+struct ssb_bfs_plan {  // cached per slimchunk_len
+  int64_t L = -1;
+  int64_t n_units = 0;
+  int64_t n_tasks = 0;
+  int64_t n_split = 0;
+  ssb::DevBuf<ssb_unit> units;
+  ssb::DevBuf<int32_t> task_begin;    // n_tasks + 1
+  ssb::DevBuf<int32_t> split_units;   // units per split chunk
+  ssb::DevBuf<uint32_t> split_hit;    // n_split
+  ssb::DevBuf<int32_t> split_best;    // n_split * 32
+  ssb::DevBuf<uint32_t> split_count;  // n_split
+};
+
+// Device-resident SlimSellRepr (repr.hpp:33-55) plus the BFS workspace.
+struct ssb_graph {
+  int64_t C = 1, sigma = 1, n = 0, n_padded = 0, n_chunks = 0, nonzeros = 0;
+  int64_t n_cells = 0, padding = 0, max_cl = 0;
+  ssb::DevBuf<int32_t> col;       // n_cells, -1 = padding cell
+  ssb::DevBuf<int64_t> cs;        // n_chunks + 1 (cs[n_chunks] = n_cells)
+  ssb::DevBuf<int32_t> cl;        // n_chunks
+  ssb::DevBuf<int32_t> perm;      // n: position -> original id
+  ssb::DevBuf<int32_t> inv_perm;  // n: original id -> position
+  ssb::DevBuf<int32_t> deg;       // n_padded: row length per position
+  std::vector<int32_t> cl_host;   // for host-side work planning
+
+  // BFS workspace (allocated on first use).
+  ssb::DevBuf<uint32_t> bits;     // visited | F0 | F1 | S0 | S1 | S2
+  ssb::DevBuf<int32_t> level;     // n_padded, valid where visited
+  ssb::DevBuf<int32_t> parent;    // n_padded, sel-max parent position
+  ssb::DevBuf<int64_t> dstats;    // per-iteration counters
+  ssb::DevBuf<uint32_t> dctrl;    // task counters + control words
+  ssb::DevBuf<uint8_t> gbytes;    // generic engine: skip flags / frontier bytes
+  ssb_bfs_plan plan;
+
+  // Last BFS (device-resident result).
+  int64_t last_root = -1;
+  int32_t last_variant = -1;
+  int32_t last_compat = 1;
+  int64_t last_iterations = 0;
+  bool last_valid = false;
+  int last_frontier_buf = 0;
+
+  ssb::StreamCtx sc;
+};
+
+namespace ssb {
+// builder.cu
+ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma);
+ssb_graph* graph_from_host_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
+                                  const int64_t* col, int64_t n_cells, const int64_t* cs,
+                                  const int64_t* cl, int64_t n_chunks, const int64_t* perm);
+// generator.cu
+ssb_edges* edges_from_pairs(const int64_t* uv, int64_t count, int64_t n);
+ssb_edges* gen_kronecker(int64_t scale, int64_t ef, uint64_t seed, const double init[4]);
+void edges_to_csr(const ssb_edges& e, int64_t* row, int64_t* col);
+// spmv.cu
+void spmv_step(const ssb_graph& g, int variant, const int64_t* x_prev, int64_t* out,
+               int64_t chunk_begin, int64_t chunk_end);
+// bfs.cu
+int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats,
+            int64_t stats_cap, int64_t* iterations, double* device_ms);
+void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
+               int64_t* parent_len);
+int64_t bfs_edges_traversed(ssb_graph& g);
+}  // namespace ssb

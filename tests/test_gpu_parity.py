@@ -1,0 +1,285 @@
+"""GPU suite: the sm_100a path through the C-ABI against the oracle and the
+reference's golden vectors. Bit-exact everywhere (integer path)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KINF = np.iinfo(np.int64).max
+STAT_KEYS = ("iteration", "chunks_processed", "chunks_skipped", "subchunks_processed",
+             "columns_processed", "frontier_size")
+
+
+def dev_rows(res):
+    return [[getattr(s, k) for k in STAT_KEYS] for s in res.per_iter]
+
+
+def port_rows(stats):
+    return [[int(r[c]) for c in (0, 2, 3, 4, 5, 6)] for r in stats]
+
+
+def opts(ssb, v, slimwork=False, L=0, compat=True, max_it=0):
+    return ssb.BfsOptions(variant=ssb.Variant(v), slimwork=slimwork, slimchunk_len=L,
+                          selmax_compat=compat, max_iterations=max_it)
+
+
+# ---- graph input + builder --------------------------------------------------
+
+@pytest.mark.parametrize("scale", [10, 16, 20, 22])
+def test_device_kronecker_and_builder_match_reference(ssb, port, golden, scale):
+    e = next(g for g in golden["graphs"] if g["scale"] == scale)
+    g = ssb.gen_kronecker(scale, 16, 1)
+    assert (g.num_vertices(), g.num_edges()) == (e["n"], e["m"])
+    assert port.fnv(g.edges()) == e["edges_fnv"]
+    for lay in e["layouts"]:
+        r = ssb.build_slimsell(g, lay["C"], lay["sigma_in"])
+        assert (r.sigma, r.n_cells, r.padding) == (lay["sigma"], lay["n_cells"], lay["padding"])
+        assert port.fnv(r.col) == lay["col_fnv"]
+        assert port.fnv(r.cs) == lay["cs_fnv"]
+        assert port.fnv(r.cl) == lay["cl_fnv"]
+        assert port.fnv(r.perm) == lay["perm_fnv"]
+        assert np.array_equal(r.inv_perm[r.perm], np.arange(r.n))
+
+
+def test_from_pairs_and_csr_match_oracle(ssb, port):
+    rng = np.random.default_rng(1)
+    for n in (1, 2, 7, 300):
+        pairs = rng.integers(0, n, size=(5 * n + 3, 2))
+        pairs = np.concatenate([pairs, pairs[:5], np.stack([np.arange(n)] * 2, 1)])  # dups + loops
+        g = ssb.Graph.from_pairs(pairs, n)
+        nn, uv = port.from_pairs(pairs, n)
+        assert g.num_vertices() == nn and np.array_equal(g.edges(), uv)
+        csr = ssb.to_csr(g)
+        row, col = port.to_csr(nn, uv)
+        assert np.array_equal(csr.row, row) and np.array_equal(csr.col, col)
+    g = ssb.Graph.from_pairs(np.array([[0, 5], [2, 3]]))  # inferred n
+    assert g.num_vertices() == 6 and g.edges().tolist() == [[0, 5], [2, 3]]
+    assert ssb.Graph.from_pairs(np.zeros((0, 2), np.int64), 0).num_vertices() == 0
+    with pytest.raises(ssb.OutOfRange):
+        ssb.Graph.from_pairs(np.array([[0, 9]]), 5)
+    with pytest.raises(ssb.OutOfRange):
+        ssb.Graph.from_pairs(np.array([[-1, 2]]))
+
+
+def small_graphs(port):
+    """The reference selftest's graph list (cli.cpp:360-382), seed 7."""
+    out = [("path7", *port.gen_path(7)), ("clique5", *port.gen_clique(5)), ("star9", *port.gen_star(9))]
+    idx, seed = 0, 7
+    for n in (16, 33, 64):
+        for p in (0.05, 0.15, 0.4):
+            out.append((f"er{n}_{p}", *port.gen_erdos_renyi(n, p, seed + idx)))
+            idx += 1
+    for scale in (4, 6):
+        for ef in (4, 8):
+            nn, uv = port.gen_kronecker(scale, ef, seed + idx)
+            out.append((f"kron{scale}_{ef}", nn, uv))
+            idx += 1
+    return out
+
+
+def test_builder_matches_oracle_small(ssb, port):
+    for name, n, uv in small_graphs(port):
+        g = ssb.Graph.from_pairs(uv, n)
+        row, col = port.to_csr(n, uv)
+        for C_ in (1, 2, 3, 8, 32):
+            for sig in (1, 2, 5, n):
+                r = ssb.build_slimsell(g, C_, sig)
+                L = port.build_slimsell(n, row, col, C_, sig)
+                assert np.array_equal(r.col, L.col), (name, C_, sig)
+                assert np.array_equal(r.cs, L.cs) and np.array_equal(r.cl, L.cl)
+                assert np.array_equal(r.perm, L.perm) and r.padding == L.padding
+
+
+# ---- kernel-level spmv_step -----------------------------------------------------
+
+def test_spmv_step_golden(ssb, port, golden):
+    r = ssb.build_slimsell(ssb.gen_kronecker(10, 16, 1), 8, 8)
+    for c in golden["kron10_spmv_C8_s8"]:
+        out = ssb.spmv_step(r, ssb.Variant(c["variant"]), np.array(c["x"], dtype=np.int64))
+        assert port.fnv(out) == c["out_fnv"]
+
+
+def test_spmv_step_random_vs_oracle(ssb, port):
+    n, uv = port.gen_kronecker(9, 8, 3)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    rng = np.random.default_rng(0)
+    for C_ in (1, 3, 8, 32):
+        r = ssb.build_slimsell(g, C_, n)
+        L = port.build_slimsell(n, row, col, C_, n)
+        for v in range(4):
+            x = rng.integers(-(1 << 40), 1 << 40, r.n_padded)
+            if v == 0:
+                x[rng.random(r.n_padded) < 0.5] = KINF
+            cb, ce = 1, max(1, r.n_chunks - 1)
+            base = rng.integers(0, 9, r.n_padded)
+            a = ssb.spmv_step(r, ssb.Variant(v), x, base.copy(), cb, ce)
+            b = port.spmv_step(L, v, x, base.copy(), cb, ce)
+            assert np.array_equal(a, b), (C_, v)
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.spmv_step(r, ssb.Variant.real, np.zeros(r.n_padded, np.int64), None, 0, r.n_chunks + 1)
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.spmv_step(r, ssb.Variant.real, np.zeros(3, np.int64))
+
+
+# ---- BFS ------------------------------------------------------------------------
+
+def test_selftest_grid_vs_oracle(ssb, port):
+    """The reference selftest's oracle grid (cli.cpp:427-466) plus C=32 (the
+    persistent engine): dist, parents and every counter equal the oracle."""
+    count = 0
+    for name, n, uv in small_graphs(port):
+        g = ssb.Graph.from_pairs(uv, n)
+        row, col = port.to_csr(n, uv)
+        csr = ssb.to_csr(g)
+        for C_ in (2, 8, 32):
+            for sig in (1, n):
+                r = ssb.build_slimsell(g, C_, sig)
+                L = port.build_slimsell(n, row, col, C_, sig)
+                for root in (0, n // 2):
+                    for v in range(4):
+                        for sw in (False, True):
+                            for Lc in (0, 4):
+                                a = ssb.bfs_spmv(r, root, opts(ssb, v, sw, Lc), csr)
+                                b = port.bfs_spmv(L, root, v, sw, Lc, csr=(row, col))
+                                key = (name, C_, sig, root, v, sw, Lc)
+                                assert a.iterations == b.iterations, key
+                                assert np.array_equal(a.dist, b.dist), key
+                                assert np.array_equal(a.parent, b.parent), key
+                                assert dev_rows(a) == port_rows(b.stats), key
+                                count += 1
+    assert count == 16 * 3 * 2 * 2 * 4 * 4
+
+
+def test_cfg1_golden(ssb, port, golden):
+    """Config 1: S16, C=8, σ=C, sel-max, the 16 pick_roots roots (4 isolated,
+    10 not perm fixed points — the reference's parent encoding is active)."""
+    r = ssb.build_slimsell(ssb.gen_kronecker(16, 16, 1), 8, 8)
+    cases = [c for c in golden["cases"] if c["graph"] == "kron16" and c["C"] == 8]
+    assert len(cases) == 48
+    for c in cases:
+        res = ssb.bfs_spmv(r, c["root"], opts(ssb, 3, c["slimwork"], c["L"]))
+        assert res.iterations == c["iterations"]
+        assert port.fnv(res.dist) == c["dist_fnv"], c
+        assert port.fnv(res.parent) == c["parent_fnv"], c
+        assert dev_rows(res) == c["stats"], c
+
+
+@pytest.mark.parametrize("graph", ["kron16", "kron20", "kron22"])
+def test_c32_golden_all_semirings(ssb, port, golden, graph):
+    scale = int(graph[4:])
+    g = ssb.gen_kronecker(scale, 16, 1)
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    csr = ssb.to_csr(g)
+    cases = [c for c in golden["cases"] if c["graph"] == graph and c["C"] == 32]
+    assert cases
+    for c in cases:
+        res = ssb.bfs_spmv(r, c["root"], opts(ssb, c["variant"], c["slimwork"], c["L"]), csr)
+        assert res.iterations == c["iterations"], c
+        assert port.fnv(res.dist) == c["dist_fnv"], c
+        assert port.fnv(res.parent) == c["parent_fnv"], c
+        assert dev_rows(res) == c["stats"], c
+
+
+def test_kron10_full_vectors(ssb, golden):
+    g = ssb.gen_kronecker(10, 16, 1)
+    csr = ssb.to_csr(g)
+    reprs = {}
+    for c in golden["kron10_full"]:
+        key = (c["C"], c["sigma"])
+        if key not in reprs:
+            reprs[key] = ssb.build_slimsell(g, *key)
+        res = ssb.bfs_spmv(reprs[key], c["root"], opts(ssb, c["variant"], True, 4), csr)
+        assert res.dist.tolist() == c["dist"]
+        assert res.parent.tolist() == c["parent"]
+        assert dev_rows(res) == c["stats"]
+
+
+def test_selmax_corrected_parents_closed_form(ssb, port):
+    """selmax_compat=False: parent = perm[max inv_perm[u] over neighbours one
+    level up], root self-parented."""
+    n, uv = port.gen_kronecker(12, 16, 5)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    for C_, sig in ((32, n), (8, 8)):
+        r = ssb.build_slimsell(g, C_, sig)
+        inv = r.inv_perm
+        for root in (0, 17, 1000):
+            res = ssb.bfs_spmv(r, root, opts(ssb, 3, True, 16, compat=False))
+            d = res.dist
+            for v in range(n):
+                if d[v] == KINF:
+                    assert res.parent[v] == -1
+                elif d[v] == 0:
+                    assert res.parent[v] == v
+                else:
+                    nb = col[row[v]:row[v + 1]]
+                    up = nb[d[nb] == d[v] - 1]
+                    assert res.parent[v] == up[np.argmax(inv[up])]
+
+
+def test_bfs_properties_large(ssb):
+    """Size-independent BFS invariants at S22 (C=32): every edge spans at most
+    one level, every reached non-root vertex has a parent one level up, the
+    four semirings agree on dist, and counters add up."""
+    g = ssb.gen_kronecker(22, 16, 2)
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    uv = g.edges()
+    dists = []
+    for v in range(4):
+        res = ssb.bfs_spmv(r, 123, opts(ssb, v, True, 128))
+        d = res.dist
+        du, dv = d[uv[:, 0]], d[uv[:, 1]]
+        both = (du != KINF) & (dv != KINF)
+        assert np.all(np.abs(du[both] - dv[both]) <= 1)
+        assert np.all((du == KINF) == (dv == KINF))
+        for s in res.per_iter:
+            assert s.chunks_processed + s.chunks_skipped == r.n_chunks
+        assert sum(s.frontier_size for s in res.per_iter) == int(np.sum(d != KINF)) - 1
+        if v == 3:
+            p = res.parent
+            reached = np.nonzero((d != KINF) & (d > 0))[0]
+            assert np.all(d[p[reached]] == d[reached] - 1)
+        dists.append(d)
+    for d in dists[1:]:
+        assert np.array_equal(d, dists[0])
+
+
+def test_device_bfs_handle_and_traversed_edges(ssb, port):
+    n, uv = port.gen_kronecker(14, 16, 1)
+    g = ssb.Graph.from_pairs(uv, n)
+    r = ssb.build_slimsell(g, 32, n)
+    row, col = port.to_csr(n, uv)
+    db = ssb.DeviceBfs(r)
+    k, ms, stats, rc = db.run(5, opts(ssb, 3, True, 64))
+    assert rc == 0 and ms > 0 and len(stats) == k
+    dist, parent = db.fetch(True)
+    b = port.bfs_spmv(port.build_slimsell(n, row, col, 32, n), 5, 3, True, 64)
+    assert np.array_equal(dist, b.dist) and np.array_equal(parent, b.parent)
+    deg = np.diff(row)
+    assert db.edges_traversed() == int(deg[dist != KINF].sum() // 2)
+
+
+def test_errors(ssb):
+    g = ssb.gen_path(4)
+    r = ssb.build_slimsell(g, 2, 1)
+    with pytest.raises(ssb.OutOfRange):
+        ssb.bfs_spmv(r, 4)
+    with pytest.raises(ssb.OutOfRange):
+        ssb.bfs_spmv(r, -1)
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.build_slimsell(g, 0, 1)
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.build_slimsell(g, 2, 0)
+    for C_ in (2, 32):
+        r = ssb.build_slimsell(g, C_, 1)
+        with pytest.raises(ssb.BfsCapError) as ei:
+            ssb.bfs_spmv(r, 0, opts(ssb, 0, max_it=2))
+        assert ei.value.partial.dist.tolist() == [0, 1, 2, KINF]
+        assert ei.value.partial.parent.size == 0 and ei.value.partial.iterations == 2
+    # isolated root: one iteration, nothing reached
+    g = ssb.Graph.from_pairs(np.array([[0, 1]]), 3)
+    for C_ in (1, 32):
+        res = ssb.bfs_spmv(ssb.build_slimsell(g, C_, 3), 2, opts(ssb, 3))
+        assert res.iterations == 1 and res.dist.tolist() == [KINF, KINF, 0]
+        assert res.parent.tolist() == [-1, -1, 2]
