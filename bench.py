@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""bench.py — SlimSell BFS-SpMV on B200: GTEPS on a Graph500 Kronecker graph.
+
+Workload (BASELINE.json config 3): gen_kronecker(26, 16, seed 1) built into
+SlimSell with C = 32, σ = n; sel-max semiring, SlimWork on, SlimChunk
+L = --slimchunk; the Graph500 root set (the reference's pick_roots stream,
+cli.cpp:114-134, rejecting degree-0 vertices). One "step" = one BFS from every
+root of the batch (--roots, default 64).
+
+  value  = Σ_roots m_cc / Σ_roots t  (GTEPS; t = device time of the BFS, CUDA
+           events on the launching stream; m_cc = edges in the root's
+           component; graph resident in HBM)
+  e2e    = the same through the public C-ABI call with HOST outputs
+           (dist + parent, int64[n] each, into pinned buffers) — copies inside
+  roofline: bfs32_kernel, algorithmic bytes B_alg = 4·C·Σ_k cols_k
+           + 3·iters·n_padded/8 + 8·n_padded per launch
+  cpu_baseline: the reference library itself (oracle/_ref, built from
+           /root/reference sources) on this host, all cores, one root.
+
+--impl reference runs the reference's own bfs_spmv (oracle/_ref) instead.
+Multi-GPU (torchrun): each rank holds the whole graph and runs its share of
+the root batch (independent BFS per root, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS (Graph500 BFS) Kronecker scale 26 at 1/2/4/8 B200; % HBM roofline"
+FALLBACK_HBM = 6650.0
+
+
+# ---------------------------------------------------------------------------
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scale", type=int, default=26)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--roots", type=int, default=64)
+    ap.add_argument("--slimchunk", type=int, default=128)
+    ap.add_argument("--variant", default="selmax", choices=["tropical", "real", "boolean", "selmax"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-slimwork", action="store_true")
+    return ap.parse_args()
+
+
+def mix64(x: int) -> int:
+    M = (1 << 64) - 1
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+def graph500_roots(deg: np.ndarray, want: int, seed: int) -> list[int]:
+    """pick_roots' stream (cli.cpp:114-134: SplitMix64(seed).split(0x526f),
+    next() % n, distinct) additionally rejecting degree-0 vertices."""
+    M = (1 << 64) - 1
+    n = deg.shape[0]
+    s = mix64(seed ^ mix64((0x526F + 0x6A09E667F3BCC909) & M))
+    out, seen = [], set()
+    while len(out) < min(want, int(np.count_nonzero(deg))):
+        s = (s + 0x9E3779B97F4A7C15) & M
+        r = mix64(s) % n
+        if r not in seen:
+            seen.add(r)
+            if deg[r] > 0:
+                out.append(int(r))
+    return out
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic():
+    """dram bytes per bfs32 launch from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_bfs32_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("workload")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def b_alg(stats, C: int, n_padded: int) -> float:
+    """Algorithmic HBM bytes of one BFS."""
+    cols = sum(s.columns_processed for s in stats)
+    return 4.0 * C * cols + 3.0 * len(stats) * n_padded / 8.0 + 8.0 * n_padded
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+def build_graph(ssb, a, log):
+    t0 = time.time()
+    g = ssb.gen_kronecker(a.scale, a.edgefactor, a.seed)
+    t1 = time.time()
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    t2 = time.time()
+    m = g.num_edges()
+    del g
+    log(f"graph S{a.scale}: n={r.n} m={m} cells={r.n_cells} gen {t1 - t0:.2f}s build {t2 - t1:.2f}s")
+    return r, m, t1 - t0, t2 - t1
+
+
+def reference_repr(ssb, r, log):
+    """Materialise the device-built layout as the reference's SlimSellRepr
+    (bit-identical to build_slimsell — tests/test_gpu_parity.py pins the
+    fingerprints up to S22), so the reference's stock bfs_spmv can run on it
+    without 8 + 5 minutes of single-threaded generation and build."""
+    import ctypes as C
+
+    from oracle import Reference
+    from paper_2010_09913_b200 import _lib as L
+
+    t0 = time.time()
+    col32 = r.col32()
+    cs = np.empty(r.n_chunks, np.int64)
+    cl = np.empty(r.n_chunks, np.int64)
+    perm = np.empty(r.n, np.int64)
+    inv = np.empty(r.n, np.int64)
+    p = lambda x: x.ctypes.data_as(L.i64p)  # noqa: E731
+    rc = L.lib().ssb_graph_export(r._h, None, p(cs), p(cl), p(perm), p(inv))
+    assert rc == 0
+    ref = Reference()
+    rr = ref.repr_from_arrays(r.n, r.C, r.sigma, r.nonzeros, col32, cs, cl, perm, inv)
+    del col32
+    log(f"reference repr materialised in {time.time() - t0:.1f}s")
+    return ref, rr
+
+
+def cpu_reference_run(ref, rr, root, variant, slimwork, L, cores):
+    t0 = time.time()
+    out = ref.bfs_spmv(rr, root, variant, slimwork=slimwork, slimchunk_len=L, schedule=1, workers=cores,
+                       want_parents=True)
+    wall = time.time() - t0
+    t = float(out.stats[:, 1].sum()) * 1e-9  # Σ IterStats.elapsed_ns (cli.cpp:46-50)
+    return out, t, wall
+
+
+def m_cc_of(dist: np.ndarray, deg: np.ndarray) -> int:
+    return int(deg[dist != np.iinfo(np.int64).max].sum() // 2)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    a = args_()
+    world, rank, local = dist_env()
+    log = (lambda *x: print("[bench]", *x, file=sys.stderr, flush=True)) if rank == 0 else (lambda *x: None)
+    variant_id = {"tropical": 0, "real": 1, "boolean": 2, "selmax": 3}[a.variant]
+    slimwork = not a.no_slimwork
+    cores = os.cpu_count() or 1
+    workload = (f"kronecker scale {a.scale} ef {a.edgefactor} seed {a.seed}, SlimSell C=32 sigma=n, "
+                f"{a.variant}, slimwork={'on' if slimwork else 'off'}, slimchunk L={a.slimchunk}, "
+                f"{a.roots} Graph500 roots/step")
+
+    if a.impl == "reference":
+        return main_reference(a, world, rank, local, log, variant_id, slimwork, cores, workload)
+
+    import torch
+
+    import paper_2010_09913_b200 as ssb
+
+    torch.cuda.set_device(local)
+    ssb.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    r, m, t_gen, t_build = build_graph(ssb, a, log)
+    deg = r.degrees()
+    roots = graph500_roots(deg, a.roots, a.seed)
+    mine = roots[rank::world]
+    opts = ssb.BfsOptions(variant=ssb.Variant(variant_id), slimwork=slimwork, slimchunk_len=a.slimchunk)
+    db = ssb.DeviceBfs(r)
+
+    # warm-up (also computes m_cc per root once; the graph is static)
+    mcc = {}
+    for w in range(a.warmup):
+        for root in mine:
+            db.run(root, opts)
+            if root not in mcc:
+                mcc[root] = db.edges_traversed()
+    for root in mine:
+        if root not in mcc:
+            db.run(root, opts)
+            mcc[root] = db.edges_traversed()
+
+    # ---- timed region: device time of K steps -------------------------------
+    sampler = ClockSampler(local)
+    barrier()
+    sampler.start()
+    step_ms, kern = [], []
+    launches = 0
+    per_root_ms = {}
+    balg_total, kernel_ms_total, n_bfs = 0.0, 0.0, 0
+    t_wall0 = time.time()
+    for s in range(a.steps):
+        tot = 0.0
+        for root in mine:
+            k, ms, stats, rc = db.run(root, opts)
+            assert rc == 0, "BFS hit the iteration cap"
+            kms, nl = db.last_timing()
+            tot += ms
+            launches += nl
+            balg_total += b_alg(stats, r.C, r.n_padded)
+            kernel_ms_total += kms
+            n_bfs += 1
+            per_root_ms.setdefault(root, []).append(ms)
+            if s == 0:
+                last_stats = stats
+        step_ms.append(tot)
+    barrier()
+    wall_s = time.time() - t_wall0
+    clocks = sampler.stop()
+
+    my_edges = sum(mcc[x] for x in mine)
+    my_ms = float(np.mean(step_ms))
+    tot_edges, max_ms = my_edges, my_ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(my_edges), my_ms], dtype=torch.float64, device="cuda")
+        e = t[:1].clone()
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        mx = t[1:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot_edges, max_ms = float(e.item()), float(mx.item())
+    value = tot_edges / (max_ms * 1e-3) / 1e9
+
+    # Graph500-style aggregates over roots (this rank)
+    teps = [mcc[x] / (np.median(per_root_ms[x]) * 1e-3) / 1e9 for x in mine]
+    hmean = len(teps) / sum(1.0 / t for t in teps)
+
+    # ---- roofline of the dominant kernel ------------------------------------
+    peak, peak_src = hbm_peak()
+    achieved = balg_total / (kernel_ms_total * 1e-3) / 1e9
+    traffic, traffic_src = profiled_traffic()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "bfs32_kernel", "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": round(balg_total / n_bfs),
+                "kernel_ms_per_launch": round(kernel_ms_total / n_bfs, 4),
+                "kernel_share_of_step": round(kernel_ms_total / max(sum(step_ms), 1e-9), 4)}
+    if traffic_src:
+        roofline["traffic_workload"] = traffic_src
+
+    # ---- e2e: public C-ABI call with host (pinned) outputs -------------------
+    n = r.n
+    pin_d = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    pin_p = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    barrier()
+    t0 = time.time()
+    e2e_edges = 0
+    for s in range(a.e2e_steps):
+        for root in mine:
+            res = ssb.bfs_spmv(r, root, opts, None, pin_d, pin_p)
+            e2e_edges += mcc[root]
+    barrier()
+    e2e_s = time.time() - t0
+    if a.e2e_steps:  # the e2e result must be a real BFS from the root
+        assert int(res.dist[root]) == 0 and len(res.parent) == n
+    e2e_tot, e2e_max = float(e2e_edges), e2e_s
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        mx = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        e2e_tot, e2e_max = float(t.item()), float(mx.item())
+    e2e = {"value": round(e2e_tot / e2e_max / 1e9, 3) if e2e_tot else None, "unit": "GTEPS",
+           "h2d_bytes_per_step": 8 * len(roots), "d2h_bytes_per_step": 16 * n * len(roots),
+           "note": "ssb_bfs_spmv per root: root in, dist+parent int64[n] out to pinned host memory"}
+
+    # ---- CPU baseline: the reference library on this host, one root ---------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            ref, rr = reference_repr(ssb, r, log)
+            root0 = mine[0]
+            out, t, wall = cpu_reference_run(ref, rr, root0, variant_id, slimwork, a.slimchunk, cores)
+            # parity of the sampled root while we have it
+            db.run(root0, opts)
+            dd, pp = db.fetch(True)
+            same = bool(np.array_equal(dd, out.dist) and np.array_equal(pp, out.parent))
+            cpu = {"value": round(mcc[root0] / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
+                   "kind": "reference",
+                   "sample": f"1 of {len(roots)} roots (root {root0}), full S{a.scale} graph; "
+                             f"reference bfs_spmv, workers={cores}, dynamic_queue; t = Σ elapsed_ns "
+                             f"{t:.2f}s (wall {wall:.2f}s)",
+                   "bit_exact_vs_gpu": same}
+            del rr
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GTEPS", "cores": cores, "kind": "reference",
+                   "sample": f"unavailable: {type(ex).__name__}: {ex}"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(max_ms, 3),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic (device Kronecker generator, "
+        "bit-identical to the reference gen_kronecker)",
+        "config": {"workload": workload, "scale": a.scale, "edgefactor": a.edgefactor,
+                   "C": 32, "sigma": "n", "semiring": a.variant, "slimwork": slimwork,
+                   "slimchunk_len": a.slimchunk, "roots_per_step": len(roots),
+                   "root_rule": "pick_roots stream (cli.cpp:114-134) rejecting degree 0",
+                   "parallelism": f"root-parallel x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (col = %.2f GB int32 >> 126 MB)" % (4 * r.n_cells / 1e9),
+                   "n": r.n, "m": m, "n_cells": r.n_cells, "iterations": len(last_stats)},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "gpu_launches": int(launches),
+        "graph500": {"harmonic_mean_gteps": round(hmean, 3), "median_gteps": round(float(np.median(teps)), 3),
+                     "m_cc_first_root": mcc[mine[0]]},
+        "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "host_wall_s": round(wall_s, 3),
+                   "gen_s": round(t_gen, 3), "build_s": round(t_build, 3)},
+        "per_iteration_first_root": [{"k": s.iteration, "ms": round(s.elapsed_ns / 1e6, 4),
+                                      "cols": s.columns_processed, "frontier": s.frontier_size,
+                                      "skipped": s.chunks_skipped} for s in last_stats],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main_reference(a, world, rank, local, log, variant_id, slimwork, cores, workload):
+    """The reference's own CPU bfs_spmv (oracle/_ref) on this host."""
+    if rank != 0:
+        return
+    import paper_2010_09913_b200 as ssb
+
+    ssb.set_device(local)
+    r, m, t_gen, t_build = build_graph(ssb, a, log)
+    deg = r.degrees()
+    roots = graph500_roots(deg, a.roots, a.seed)
+    ref, rr = reference_repr(ssb, r, log)
+    del r
+    times, edges = [], []
+    for i in range(a.warmup + a.steps):
+        root = roots[i % len(roots)]
+        out, t, wall = cpu_reference_run(ref, rr, root, variant_id, slimwork, a.slimchunk, cores)
+        log(f"reference root {root}: {t:.2f}s ({wall:.2f}s wall) iterations {out.iterations}")
+        if i >= a.warmup:
+            times.append(t)
+            edges.append(m_cc_of(out.dist, deg))
+    value = sum(edges) / sum(times) / 1e9
+    sample = (f"each step = 1 root of the {len(roots)}-root batch (roots cycled), full S{a.scale} graph; "
+              f"reference bfs_spmv workers={cores} dynamic_queue; layout materialised from the "
+              f"device-built (bit-identical) SlimSell arrays")
+    line = {
+        "metric": METRIC, "value": round(value, 5), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(1e3 * float(np.mean(times)), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": workload, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
+                   "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk},
+        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -107,6 +107,9 @@ int ssb_graph_info(const ssb_graph* g, ssb_layout_info* info);
  * col n_cells, cs n_chunks, cl n_chunks, perm n, inv_perm n. */
 int ssb_graph_export(const ssb_graph* g, int64_t* col, int64_t* cs, int64_t* cl,
                      int64_t* perm, int64_t* inv_perm);
+/* Row length (degree) of every ORIGINAL vertex id: n int64 (the
+ * row[v+1]-row[v] of to_csr, graph.hpp:63-71). */
+int ssb_graph_degrees(const ssb_graph* g, int64_t* deg);
 /* Compact export of col as int32 (the device storage type). */
 int ssb_graph_export_col32(const ssb_graph* g, int32_t* col);
 void ssb_graph_destroy(ssb_graph* g);
@@ -140,6 +143,9 @@ int ssb_bfs_run(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
 /* Copies the last ssb_bfs_run result out (original ids), as ssb_bfs_spmv. */
 int ssb_bfs_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent,
                   int64_t* parent_len);
+/* Timing of the last ssb_bfs_run: CUDA-event time of the main BFS kernel
+ * launches alone (kernel_ms) and how many kernels the BFS launched. */
+int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches);
 /* m_cc of the last run: Σ_{reached v} deg(v) / 2 (the GTEPS numerator). */
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc);
 

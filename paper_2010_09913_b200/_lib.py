@@ -74,6 +74,8 @@ def lib() -> C.CDLL:
         "ssb_graph_info": (C.c_int, [vp, C.POINTER(LayoutInfo)]),
         "ssb_graph_export": (C.c_int, [vp, i64p, i64p, i64p, i64p, i64p]),
         "ssb_graph_export_col32": (C.c_int, [vp, i32p]),
+        "ssb_graph_degrees": (C.c_int, [vp, i64p]),
+        "ssb_bfs_last_timing": (C.c_int, [vp, C.POINTER(C.c_double), i64p]),
         "ssb_graph_destroy": (None, [vp]),
         "ssb_spmv_step": (C.c_int, [vp, C.c_int, i64p, i64p, C.c_int64, C.c_int64]),
         "ssb_bfs_spmv": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), i64p, i64p, i64p,

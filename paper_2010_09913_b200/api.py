@@ -239,6 +239,12 @@ class SlimSellRepr:
         _check(_L.lib().ssb_graph_export_col32(self._h, _p(out, _L.i32p)))
         return out[: self.n_cells]
 
+    def degrees(self) -> np.ndarray:
+        """Degree of every original vertex id (row lengths of to_csr)."""
+        out = np.empty(max(self.n, 1), np.int64)
+        _check(_L.lib().ssb_graph_degrees(self._h, _p(out)))
+        return out[: self.n]
+
     def chunk_row_begin(self, chunk: int) -> int:  # repr.hpp:47
         return chunk * self.C
 
@@ -291,31 +297,39 @@ def _stats_list(buf, k):
 
 
 def bfs_spmv(r: SlimSellRepr, root: int, opts: BfsOptions | None = None,
-             csr_for_parents: CsrView | None = None) -> BfsResult:  # bfs.hpp:80-81
+             csr_for_parents: CsrView | None = None, out_dist: np.ndarray | None = None,
+             out_parent: np.ndarray | None = None) -> BfsResult:  # bfs.hpp:80-81
     """Algebraic BFS on the device. As the reference: sel-max always produces
     parents when opts.want_parents; the other variants only when a CSR is
-    passed (they are derived from the distances, dp_transform semantics)."""
+    passed (they are derived from the distances, dp_transform semantics).
+    out_dist / out_parent may be caller-owned (e.g. pinned) int64[n] buffers;
+    the result then aliases them instead of copying."""
     opts = opts or BfsOptions()
     want = bool(opts.want_parents) and (opts.variant == Variant.selmax or csr_for_parents is not None)
     o = opts._c()
     o.want_parents = int(want)
     n = r.n
-    dist = np.empty(max(n, 1), np.int64)
-    parent = np.empty(max(n, 1), np.int64)
+    for buf in (out_dist, out_parent):
+        if buf is not None and (buf.dtype != np.int64 or buf.shape[0] < n or not buf.flags.c_contiguous):
+            raise InvalidArgument("output buffers must be contiguous int64[n]")
+    dist = np.empty(max(n, 1), np.int64) if out_dist is None else out_dist
+    parent = np.empty(max(n, 1), np.int64) if out_parent is None else out_parent
     plen = np.zeros(1, np.int64)
     iters = np.zeros(1, np.int64)
-    cap = 4096
-    stats = (_L.IterStatsC * cap)()
-    rc = _L.lib().ssb_bfs_spmv(r._h, int(root), C.byref(o), _p(dist), _p(parent), _p(plen),
-                               stats, cap, _p(iters))
-    if rc not in (_L.SSB_OK, _L.SSB_ECAP):
-        _raise(rc)
-    k = int(iters[0])
-    if k > cap:  # very deep BFS: fetch all records
-        stats = (_L.IterStatsC * k)()
-        # rerun is not needed: stats beyond cap are dropped by the C-ABI; report what we have
-        k = cap
-    res = BfsResult(dist[:n].copy(), parent[: int(plen[0])].copy(), int(iters[0]), _stats_list(stats, k))
+    cap = min(max(n + 2, 2), 1 << 16)
+    while True:
+        stats = (_L.IterStatsC * cap)()
+        rc = _L.lib().ssb_bfs_spmv(r._h, int(root), C.byref(o), _p(dist), _p(parent), _p(plen),
+                                   stats, cap, _p(iters))
+        if rc not in (_L.SSB_OK, _L.SSB_ECAP):
+            _raise(rc)
+        k = int(iters[0])
+        if k <= cap:
+            break
+        cap = k  # deeper than the first buffer: rerun once with room for every record
+    keep = (lambda a: a[:n]) if out_dist is not None else (lambda a: a[:n].copy())
+    res = BfsResult(keep(dist), parent[: int(plen[0])] if out_parent is not None else
+                    parent[: int(plen[0])].copy(), k, _stats_list(stats, k))
     if rc == _L.SSB_ECAP:
         raise BfsCapError(_L.lib().ssb_last_error().decode(), res)
     return res
@@ -345,6 +359,13 @@ class DeviceBfs:
         plen = np.zeros(1, np.int64)
         _check(_L.lib().ssb_bfs_fetch(self.r._h, int(want_parents), _p(dist), _p(parent), _p(plen)))
         return dist, parent[: int(plen[0])]
+
+    def last_timing(self):
+        """(kernel_ms, launches) of the last run."""
+        ms = C.c_double()
+        n = np.zeros(1, np.int64)
+        _check(_L.lib().ssb_bfs_last_timing(self.r._h, C.byref(ms), _p(n)))
+        return float(ms.value), int(n[0])
 
     def edges_traversed(self) -> int:
         m = np.zeros(1, np.int64)

@@ -38,6 +38,9 @@
 #include <climits>
 #include <cstdlib>
 #include <memory>
+#include <cstdio>
+#include <cstring>
+#include <unistd.h>
 
 #include "ssb_internal.cuh"
 
@@ -122,7 +125,13 @@ struct Args32 {
   uint32_t last_real;  // real-row mask of the last chunk
   int32_t k_begin;
   int32_t k_end;
+  int* trace;  // debug progress words in mapped host memory (SSB_TRACE), or null
 };
+
+#define TRACE(slot, v)                                           \
+  do {                                                           \
+    if (a.trace) *reinterpret_cast<volatile int*>(&a.trace[slot]) = (v); \
+  } while (0)
 
 // Frontier bit of permuted vertex c (c >= 0): prefix from shared memory,
 // the rest only when the shared summary says its word group is non-empty.
@@ -197,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       if (threadIdx.x < 5) blk[threadIdx.x] = 0ull;
     }
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
 
     unsigned long long c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
 
@@ -244,7 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         const int32_t sl = src < 0 ? 0 : src;
         const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
         const int32_t cb = __shfl_sync(0xffffffffu, U.col_begin, sl);
-        const int32_t len = src < 0 ? 0 : __shfl_sync(0xffffffffu, U.col_len, sl);
+        const int32_t ulen = __shfl_sync(0xffffffffu, U.col_len, sl);  // all lanes shuffle
+        const int32_t len = src < 0 ? 0 : ulen;
         const int32_t split = __shfl_sync(0xffffffffu, U.split, sl);
         const uint32_t uvis = __shfl_sync(0xffffffffu, vis, sl);
         const uint32_t ureal = __shfl_sync(0xffffffffu, realm, sl);
@@ -361,7 +372,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     if (threadIdx.x < 5)
       atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[rec * kStatW + threadIdx.x]),
                 blk[threadIdx.x]);
+    if (threadIdx.x == 0 && a.trace) atomicAdd(&a.trace[2], 1);
     grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(1, 4);
     const int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const uint64_t t = globaltimer();
@@ -654,13 +667,16 @@ void collect_stats(const std::vector<int64_t>& rec, int64_t k0, int64_t count,
 }
 
 template <bool kSel>
-void configure32() {
-  static bool done = false;
-  if (!done) {
-    SSB_CUDA(cudaFuncSetAttribute(bfs32_kernel<kSel>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    done = true;
-  }
+void configure32(size_t dyn_smem) {
+  int dev = 0, optin = 0;
+  SSB_CUDA(cudaGetDevice(&dev));
+  SSB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  SSB_CUDA(cudaFuncGetAttributes(&fa, bfs32_kernel<kSel>));
+  if (dyn_smem + fa.sharedSizeBytes > size_t(optin))
+    fail(SSB_EINVAL, "frontier staging exceeds shared memory (SSB_SMEM_KB too large)");
+  SSB_CUDA(cudaFuncSetAttribute(bfs32_kernel<kSel>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(dyn_smem)));
 }
 
 // Returns true when converged; appends per-iteration stats.
@@ -682,8 +698,9 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   set_root_kernel<<<1, 1, 0, s>>>(R.visited, R.F0, G.SW ? R.S0 : nullptr, g.level.p, g.parent.p,
                                   root_pos, root_code, G.PW, G.gshift);
   SSB_CUDA(cudaGetLastError());
+  g.last_launches += 1;  // set_root_kernel
 
-  if (sel) configure32<true>(); else configure32<false>();
+  if (sel) configure32<true>(G.smem); else configure32<false>(G.smem);
   int per_sm = 0;
   SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &per_sm, sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, kThreads,
@@ -719,6 +736,13 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   a.L = int32_t(std::max<int64_t>(0, std::min<int64_t>(o.slimchunk_len, INT32_MAX)));
   a.slimwork = o.slimwork ? 1 : 0;
   a.root_code = root_code;
+  a.trace = nullptr;
+  static int* trace_buf = nullptr;
+  if (std::getenv("SSB_TRACE")) {
+    if (!trace_buf) SSB_CUDA(cudaHostAlloc(&trace_buf, 64, cudaHostAllocMapped));
+    std::memset(trace_buf, 0, 64);
+    SSB_CUDA(cudaHostGetDevicePointer(&a.trace, trace_buf, 0));
+  }
   {
     const int64_t real_last = g.n - (g.n_chunks - 1) * 32;  // 1..32
     a.last_real = real_last >= 32 ? 0xffffffffu : ((1u << real_last) - 1u);
@@ -732,12 +756,32 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
     SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, g.dstats.bytes(), s));
     SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
     void* params[] = {&a};
+    SSB_CUDA(cudaEventRecord(g.sc.e0, s));
     SSB_CUDA(cudaLaunchCooperativeKernel(
         sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, dim3(grid),
         dim3(kThreads), params, G.smem, s));
     SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaEventRecord(g.sc.e1, s));
+    if (a.trace) {  // debug: poll progress instead of blocking forever
+      cudaEvent_t done;
+      SSB_CUDA(cudaEventCreate(&done));
+      SSB_CUDA(cudaEventRecord(done, s));
+      for (int spin = 0; cudaEventQuery(done) == cudaErrorNotReady; ++spin) {
+        if (spin % 1000 == 999)
+          fprintf(stderr, "[ssb trace] k=%d phase=%d arrived=%d\n", a.trace[0], a.trace[1], a.trace[2]);
+        if (spin > 10000) { fprintf(stderr, "[ssb trace] giving up\n"); std::abort(); }
+        usleep(1000);
+      }
+      cudaEventDestroy(done);
+    }
     SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, rec.size() * 8, cudaMemcpyDeviceToHost, s));
     g.sc.sync();
+    {
+      float kms = 0;
+      SSB_CUDA(cudaEventElapsedTime(&kms, g.sc.e0, g.sc.e1));
+      g.last_kernel_ms += kms;
+      g.last_launches += 1;  // bfs32_kernel
+    }
     // the launch ran iterations k .. until a record with frontier 0 or kend
     int64_t ran = 0;
     bool conv = false;
@@ -809,6 +853,8 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
     float ms = 0;
     SSB_CUDA(cudaEventElapsedTime(&ms, g.sc.e0, g.sc.e1));
     rec[5] = int64_t(double(ms) * 1e6);
+    g.last_kernel_ms += ms;
+    g.last_launches += g.n_chunks ? 2 : 0;
     collect_stats(rec, k, 1, stats);
     conv = rec[0] == 0;
   }
@@ -816,6 +862,7 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
   BitRegions R = bit_regions(g, 0);
   bytes_to_bits_kernel<<<grid_for((np + 31) / 32), 256, 0, s>>>(vis, np, R.visited);
   SSB_CUDA(cudaGetLastError());
+  g.last_launches += 1;
   g.sc.sync();
   return conv;
 }
@@ -849,7 +896,8 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
   const int32_t root_code = (o.variant == SSB_SELMAX && o.selmax_compat) ? int32_t(root) : root_pos;
   const int64_t cap = o.max_iterations > 0 ? o.max_iterations : g.n + 1;
   std::vector<ssb_iter_stats> st;
-  SSB_CUDA(cudaEventRecord(g.sc.e0, g.sc.s));
+  g.last_kernel_ms = 0;
+  g.last_launches = 0;
   cudaEvent_t t0, t1;
   SSB_CUDA(cudaEventCreate(&t0));
   SSB_CUDA(cudaEventCreate(&t1));

@@ -161,6 +161,20 @@ int ssb_graph_export(const ssb_graph* cg, int64_t* col, int64_t* cs, int64_t* cl
   });
 }
 
+int ssb_graph_degrees(const ssb_graph* cg, int64_t* deg) {
+  return guarded([&] {
+    need(cg, "graph");
+    need(deg, "deg");
+    ssb_graph& g = const_cast<ssb_graph&>(*cg);
+    if (g.n == 0) return;
+    std::vector<int32_t> d(g.n), p(g.n);
+    SSB_CUDA(cudaMemcpyAsync(d.data(), g.deg.p, 4 * g.n, cudaMemcpyDeviceToHost, g.sc.s));
+    SSB_CUDA(cudaMemcpyAsync(p.data(), g.perm.p, 4 * g.n, cudaMemcpyDeviceToHost, g.sc.s));
+    g.sc.sync();
+    for (int64_t i = 0; i < g.n; ++i) deg[p[i]] = d[i];
+  });
+}
+
 int ssb_graph_export_col32(const ssb_graph* cg, int32_t* col) {
   return guarded([&] {
     need(cg, "graph");
@@ -221,6 +235,15 @@ int ssb_bfs_spmv(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, int64_
   if (f != SSB_OK) return f;
   if (rc == SSB_ECAP) g_last_error = cap_msg;
   return rc;
+}
+
+int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches) {
+  return guarded([&] {
+    need(g, "graph");
+    if (!g->last_valid) ssb::fail(SSB_EINVAL, "no BFS result on this graph");
+    if (kernel_ms) *kernel_ms = g->last_kernel_ms;
+    if (launches) *launches = g->last_launches;
+  });
 }
 
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc) {

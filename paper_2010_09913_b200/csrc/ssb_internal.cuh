@@ -143,7 +143,8 @@ struct ssb_graph {
   int32_t last_compat = 1;
   int64_t last_iterations = 0;
   bool last_valid = false;
-  int last_frontier_buf = 0;
+  double last_kernel_ms = 0;  // CUDA-event time of the main BFS kernel launches
+  int64_t last_launches = 0;  // kernels launched by the last BFS
 
   ssb::StreamCtx sc;
 };

@@ -227,7 +227,7 @@ def test_bfs_properties_large(ssb):
     uv = g.edges()
     dists = []
     for v in range(4):
-        res = ssb.bfs_spmv(r, 123, opts(ssb, v, True, 128))
+        res = ssb.bfs_spmv(r, 123, opts(ssb, v, True, 128, compat=False))
         d = res.dist
         du, dv = d[uv[:, 0]], d[uv[:, 1]]
         both = (du != KINF) & (dv != KINF)
