@@ -49,7 +49,10 @@ namespace cg = cooperative_groups;
 namespace ssb {
 namespace {
 
-constexpr int kThreads = 1024;
+#ifndef SSB_BFS_THREADS
+#define SSB_BFS_THREADS 1024
+#endif
+constexpr int kThreads = SSB_BFS_THREADS;  // 32 warps: 64 registers, no spills
 constexpr int kUnitsPerTask = 32;
 constexpr int kStatW = 8;  // int64 per iteration record
 // record: 0 frontier_size, 1 chunks_processed, 2 chunks_skipped,
@@ -133,35 +136,118 @@ struct Args32 {
     if (a.trace) *reinterpret_cast<volatile int*>(&a.trace[slot]) = (v); \
   } while (0)
 
-// Frontier bit of permuted vertex c (c >= 0): prefix from shared memory,
-// the rest only when the shared summary says its word group is non-empty.
-__device__ __forceinline__ uint32_t probe(int32_t c, const uint32_t* fine, const uint32_t* summ,
-                                          const uint32_t* Fc, int32_t PW, int32_t gshift) {
-  const int32_t w = c >> 5;
-  uint32_t word;
-  if (w < PW) {
-    word = fine[w];
-  } else {
-    const int32_t gi = (w - PW) >> gshift;
-    word = ((summ[gi >> 5] >> (gi & 31)) & 1u) ? Fc[w] : 0u;
+// Shared-memory image of the frontier F_{k-1} (word indices):
+//   [0, 4)             zeros — the target of padding cells (c = -1)
+//   [4, 4 + PW)        fine bits of vertices [0, P), P = 32·PW (the hubs:
+//                      the σ = n sort puts high degrees first)
+//   [sbase, sbase+SW)  summary of the rest: bit t <-> vertices
+//                      [P + t·2^gsh, P + (t+1)·2^gsh) contain a frontier vertex
+struct Probe {
+  const uint32_t* sm;
+  const uint32_t* Fc;  // the full frontier in global memory (L2-resident)
+  int32_t P, sbase, gsh;
+
+  // Frontier bit of cell value c (c = -1 for padding). One shared load on the
+  // common path; the global word only when the summary bit is set.
+  __device__ __forceinline__ bool operator()(int32_t c) const {
+    const bool pre = c < P;
+    const int32_t d = c - P;
+    const int32_t idx = pre ? (c >> 5) + 4 : sbase + (d >> (gsh + 5));
+    const int32_t sh = pre ? c : (d >> gsh);
+    const uint32_t word = sm[idx];
+    bool b = __funnelshift_r(word, word, sh) & 1u;  // bit (sh mod 32)
+    if (!pre && b) b = (Fc[c >> 5] >> (c & 31)) & 1u;
+    return b;
   }
-  return (word >> (c & 31)) & 1u;
-}
+};
 
 template <bool kSelMax>
-__device__ __forceinline__ void take_cells(const int4 v, const uint32_t* fine, const uint32_t* summ,
-                                           const uint32_t* Fc, int32_t PW, int32_t gshift,
-                                           uint32_t& hit, int32_t (&best)[4]) {
+__device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32_t& hit,
+                                           int32_t (&best)[4]) {
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    if (c[q] >= 0) {
-      const uint32_t b = probe(c[q], fine, summ, Fc, PW, gshift);
-      if (kSelMax) {
-        // ascending columns: the last hit is the max frontier position
-        best[q] = b ? c[q] : best[q];
-      } else {
-        hit |= b << q;
+    const bool b = pr(c[q]);
+    if (kSelMax) {
+      // ascending columns: the last hit is the max frontier position
+      best[q] = b ? c[q] : best[q];
+    } else {
+      hit |= uint32_t(b) << q;
+    }
+  }
+}
+
+// One 128-byte column of padding cells: the load target of groups without a
+// unit, so the sweep needs no per-load predicates.
+__device__ __align__(16) int32_t g_pad_column[32] = {
+    -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+    -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+
+constexpr int32_t kWarpUnitCols = 16;  // units at least this long use the warp-wide sweep
+
+// Completes one work unit; called by all 32 lanes, `valid` per 8-lane group.
+// m = the unit's 32-row hit mask, best[q] = last hit of row 4·lg+q (sel-max).
+// SlimChunk combine (bfs.cpp:205-220): partial results of a split chunk meet
+// in a scratch slot and the unit that arrives last finalises the chunk —
+// post_process_rows (semiring.cpp:90-124) in 1-bit form.
+template <bool kSelMax>
+__device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t* Fn, uint32_t* Sn,
+                                            bool valid, int32_t chunk, int32_t split, uint32_t uvis,
+                                            uint32_t ureal, uint32_t m, int32_t (&best)[4], int grp,
+                                            int lg, uint32_t gmask, uint32_t& c_front) {
+  bool fin = valid && split < 0;
+  const bool sp = valid && split >= 0;
+  if (sp) {
+    if (lg == 0 && m) atomicOr(&a.split_hit[split], m);
+    if (kSelMax) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (best[q] >= 0) atomicMax(&a.split_best[split * 32 + 4 * lg + q], best[q]);
+    }
+    __threadfence();
+  }
+  __syncwarp();
+  uint32_t last = 0;
+  if (sp && lg == 0) {
+    const uint32_t arrived = atomicAdd(&a.split_count[split], 1u) + 1u;
+    last = arrived == uint32_t(a.split_units[split]);
+  }
+  last = __shfl_sync(0xffffffffu, last, grp * 8);
+  if (sp && last) {
+    __threadfence();
+    fin = true;
+    if (lg == 0) {
+      m = atomicExch(&a.split_hit[split], 0u);
+      a.split_count[split] = 0u;
+    }
+    m = __shfl_sync(gmask, m, grp * 8, 32);
+    if (kSelMax) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) best[q] = atomicExch(&a.split_best[split * 32 + 4 * lg + q], -1);
+    }
+  }
+  if (fin) {
+    const uint32_t newly = m & ~uvis & ureal;
+    if (lg == 0) {
+      Fn[chunk] = newly;
+      if (newly) {
+        a.visited[chunk] = uvis | newly;
+        if (chunk >= a.PW) {
+          const int32_t gi = (chunk - a.PW) >> a.gshift;
+          atomicOr(&Sn[gi >> 5], 1u << (gi & 31));
+        }
+        c_front += __popc(newly);
+      }
+    }
+    if (newly) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int32_t r = 4 * lg + q;
+        if ((newly >> r) & 1u) {
+          const int64_t row = int64_t(chunk) * 32 + r;
+          a.level[row] = k;
+          if (kSelMax) a.parent[row] = k == 1 ? a.root_code : best[q];
+        }
       }
     }
   }
@@ -170,8 +256,8 @@ __device__ __forceinline__ void take_cells(const int4 v, const uint32_t* fine, c
 template <bool kSelMax>
 __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   extern __shared__ uint4 smem_v4[];
-  uint32_t* fine = reinterpret_cast<uint32_t*>(smem_v4);
-  uint32_t* summ = fine + a.PW;
+  uint32_t* sm = reinterpret_cast<uint32_t*>(smem_v4);
+  uint32_t* summ = sm + 4 + a.PW;
   __shared__ unsigned long long blk[5];
 
   cg::grid_group grid = cg::this_grid();
@@ -195,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     // -- stage the frontier prefix and the summary into shared memory -------
     {
       const uint4* src = reinterpret_cast<const uint4*>(Fc);
-      uint4* dst = smem_v4;
+      uint4* dst = smem_v4 + 1;  // words [4, 4 + PW)
+      if (threadIdx.x == 0) smem_v4[0] = make_uint4(0u, 0u, 0u, 0u);
       for (int i = threadIdx.x; i < (a.PW >> 2); i += kThreads) dst[i] = src[i];
       const uint4* ssrc = reinterpret_cast<const uint4*>(Sc);
       uint4* sdst = reinterpret_cast<uint4*>(summ);
@@ -208,7 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
 
-    unsigned long long c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
+    // per-warp counters of this iteration (a warp's share fits 32 bits)
+    uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
+    const Probe pr{sm, Fc, a.PW * 32, 4 + a.PW, a.gshift + 5};
 
     for (;;) {
       int32_t t = 0;
@@ -240,7 +329,65 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
           }
         }
       }
-      uint32_t active = __ballot_sync(0xffffffffu, has && !skip);
+      // Long units (≥ kWarpUnitCols columns) are swept by the whole warp as one
+      // contiguous 128-bit stream; short ones four at a time, one per group.
+      const bool is_long = has && !skip && U.col_len >= kWarpUnitCols;
+      uint32_t longs = __ballot_sync(0xffffffffu, is_long);
+      uint32_t active = __ballot_sync(0xffffffffu, has && !skip && !is_long);
+
+      while (longs) {
+        const int32_t sl = __ffs(longs) - 1;
+        longs &= longs - 1;
+        const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
+        const int32_t cb = __shfl_sync(0xffffffffu, U.col_begin, sl);
+        const int32_t len = __shfl_sync(0xffffffffu, U.col_len, sl);
+        const int32_t split = __shfl_sync(0xffffffffu, U.split, sl);
+        const uint32_t uvis = __shfl_sync(0xffffffffu, vis, sl);
+        const uint32_t ureal = __shfl_sync(0xffffffffu, realm, sl);
+        // int4 i of the unit = column i/8, rows 4(i%8)..+3; lane l takes
+        // i = 32s + l, so lg (rows) is fixed per lane and grp picks the column
+        // within each 4-column step. Out-of-range indices re-read the lane's
+        // own rows of the last column (idempotent).
+        const int4* base = reinterpret_cast<const int4*>(a.col + a.cs[chunk] + int64_t(cb) * 32);
+        const int32_t nv = len * 8, imax = nv - 8 + lg;
+        const int32_t nsteps = (nv + 31) >> 5;
+        uint32_t hit = 0;
+        int32_t best[4] = {-1, -1, -1, -1};
+        int4 v0 = ld_stream(base + min(lane, imax), pol);
+        int4 v1 = ld_stream(base + min(32 + lane, imax), pol);
+        int4 v2 = ld_stream(base + min(64 + lane, imax), pol);
+        int4 v3 = ld_stream(base + min(96 + lane, imax), pol);
+        for (int32_t s = 0; s < nsteps; s += 4) {
+          const bool more = s + 4 < nsteps;  // warp-uniform
+          const int32_t i0 = (s + 4) * 32 + lane;
+          take_cells<kSelMax>(v0, pr, hit, best);
+          if (more) v0 = ld_stream(base + min(i0, imax), pol);
+          take_cells<kSelMax>(v1, pr, hit, best);
+          if (more) v1 = ld_stream(base + min(i0 + 32, imax), pol);
+          take_cells<kSelMax>(v2, pr, hit, best);
+          if (more) v2 = ld_stream(base + min(i0 + 64, imax), pol);
+          take_cells<kSelMax>(v3, pr, hit, best);
+          if (more) v3 = ld_stream(base + min(i0 + 96, imax), pol);
+        }
+        // combine the four column groups, then form the unit's row mask
+        if (kSelMax) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            best[q] = max(best[q], __shfl_xor_sync(0xffffffffu, best[q], 8));
+            best[q] = max(best[q], __shfl_xor_sync(0xffffffffu, best[q], 16));
+            hit |= uint32_t(best[q] >= 0) << q;
+          }
+        } else {
+          hit |= __shfl_xor_sync(0xffffffffu, hit, 8);
+          hit |= __shfl_xor_sync(0xffffffffu, hit, 16);
+        }
+        uint32_t m = hit << (4 * lg);
+        m |= __shfl_xor_sync(0xffffffffu, m, 1);
+        m |= __shfl_xor_sync(0xffffffffu, m, 2);
+        m |= __shfl_xor_sync(0xffffffffu, m, 4);
+        finish_unit<kSelMax>(a, k, Fn, Sn, grp == 0, chunk, split, uvis, ureal, m, best, grp, lg,
+                             gmask, c_front);
+      }
 
       while (active) {
         // the next (up to) four active units, one per 8-lane group
@@ -263,22 +410,31 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, 8));
         maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, 16));
 
-        const int4* p = reinterpret_cast<const int4*>(a.col + (src < 0 ? 0 : a.cs[chunk]) +
-                                                      int64_t(cb) * 32) + lg;
+        // Column j of the unit is int4 p[8j] (lane lg: rows 4lg..4lg+3). Groups
+        // shorter than maxlen re-read their last column (idempotent for both
+        // the "any" and the "last hit" reduction); groups without a unit read
+        // a padding column. Loads run 4 columns ahead of the probes.
+        const int4* p = len > 0 ? reinterpret_cast<const int4*>(a.col + a.cs[chunk] +
+                                                                 int64_t(cb) * 32) + lg
+                                : reinterpret_cast<const int4*>(g_pad_column) + (lg & 7);
+        const int32_t jlast = len > 0 ? len - 1 : 0;
+        const int64_t stride = len > 0 ? 8 : 0;
         uint32_t hit = 0;
         int32_t best[4] = {-1, -1, -1, -1};
-        int32_t j = 0;
-        for (; j + 4 <= maxlen; j += 4) {
-          int4 v[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-            v[x] = (j + x < len) ? ld_stream(p + int64_t(j + x) * 8, pol) : make_int4(-1, -1, -1, -1);
-#pragma unroll
-          for (int x = 0; x < 4; ++x) take_cells<kSelMax>(v[x], fine, summ, Fc, a.PW, a.gshift, hit, best);
-        }
-        for (; j < maxlen; ++j) {
-          const int4 v = j < len ? ld_stream(p + int64_t(j) * 8, pol) : make_int4(-1, -1, -1, -1);
-          take_cells<kSelMax>(v, fine, summ, Fc, a.PW, a.gshift, hit, best);
+        int4 v0 = ld_stream(p, pol);
+        int4 v1 = ld_stream(p + min(1, jlast) * stride, pol);
+        int4 v2 = ld_stream(p + min(2, jlast) * stride, pol);
+        int4 v3 = ld_stream(p + min(3, jlast) * stride, pol);
+        for (int32_t j = 0; j < maxlen; j += 4) {
+          const bool more = j + 4 < maxlen;  // warp-uniform
+          take_cells<kSelMax>(v0, pr, hit, best);
+          if (more) v0 = ld_stream(p + min(j + 4, jlast) * stride, pol);
+          take_cells<kSelMax>(v1, pr, hit, best);
+          if (more) v1 = ld_stream(p + min(j + 5, jlast) * stride, pol);
+          take_cells<kSelMax>(v2, pr, hit, best);
+          if (more) v2 = ld_stream(p + min(j + 6, jlast) * stride, pol);
+          take_cells<kSelMax>(v3, pr, hit, best);
+          if (more) v3 = ld_stream(p + min(j + 7, jlast) * stride, pol);
         }
         if (kSelMax) {
 #pragma unroll
@@ -290,65 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         m |= __shfl_xor_sync(0xffffffffu, m, 2);
         m |= __shfl_xor_sync(0xffffffffu, m, 4);
 
-        // SlimChunk combine (bfs.cpp:205-220): partial results of a split chunk
-        // meet in a scratch slot; the unit that arrives last finalises.
-        bool fin = src >= 0 && split < 0;
-        const bool sp = src >= 0 && split >= 0;
-        if (sp) {
-          if (lg == 0 && m) atomicOr(&a.split_hit[split], m);
-          if (kSelMax) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (best[q] >= 0) atomicMax(&a.split_best[split * 32 + 4 * lg + q], best[q]);
-          }
-          __threadfence();
-        }
-        __syncwarp();
-        uint32_t last = 0;
-        if (sp && lg == 0) {
-          const uint32_t arrived = atomicAdd(&a.split_count[split], 1u) + 1u;
-          last = arrived == uint32_t(a.split_units[split]);
-        }
-        last = __shfl_sync(0xffffffffu, last, grp * 8);
-        if (sp && last) {
-          __threadfence();
-          fin = true;
-          if (lg == 0) {
-            m = atomicExch(&a.split_hit[split], 0u);
-            a.split_count[split] = 0u;
-          }
-          m = __shfl_sync(gmask, m, grp * 8, 32);
-          if (kSelMax) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) best[q] = atomicExch(&a.split_best[split * 32 + 4 * lg + q], -1);
-          }
-        }
-        // finalise the chunk (post_process_rows, semiring.cpp:90-124)
-        if (fin) {
-          const uint32_t newly = m & ~uvis & ureal;
-          if (lg == 0) {
-            Fn[chunk] = newly;
-            if (newly) {
-              a.visited[chunk] = uvis | newly;
-              if (chunk >= a.PW) {
-                const int32_t gi = (chunk - a.PW) >> a.gshift;
-                atomicOr(&Sn[gi >> 5], 1u << (gi & 31));
-              }
-              c_front += __popc(newly);
-            }
-          }
-          if (newly) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int32_t r = 4 * lg + q;
-              if ((newly >> r) & 1u) {
-                const int64_t row = int64_t(chunk) * 32 + r;
-                a.level[row] = k;
-                if (kSelMax) a.parent[row] = k == 1 ? a.root_code : best[q];
-              }
-            }
-          }
-        }
+        finish_unit<kSelMax>(a, k, Fn, Sn, src >= 0, chunk, split, uvis, ureal, m, best, grp, lg,
+                             gmask, c_front);
       }
     }
 
@@ -362,11 +461,11 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       c_cols += __shfl_xor_sync(0xffffffffu, c_cols, o);
     }
     if (lane == 0) {
-      atomicAdd(&blk[0], c_front);
-      atomicAdd(&blk[1], c_proc);
-      atomicAdd(&blk[2], c_skip);
-      atomicAdd(&blk[3], c_sub);
-      atomicAdd(&blk[4], c_cols);
+      atomicAdd(&blk[0], (unsigned long long)c_front);
+      atomicAdd(&blk[1], (unsigned long long)c_proc);
+      atomicAdd(&blk[2], (unsigned long long)c_skip);
+      atomicAdd(&blk[3], (unsigned long long)c_sub);
+      atomicAdd(&blk[4], (unsigned long long)c_cols);
     }
     __syncthreads();
     if (threadIdx.x < 5)
@@ -565,7 +664,7 @@ Geometry geometry32(const ssb_graph& g) {
     G.SW = int32_t(((((G.NW + (int64_t{1} << gs) - 1) >> gs) + 31) / 32 + 3) / 4 * 4);
     G.PW = int32_t(std::max<int64_t>(0, (budget_words - G.SW)) & ~int64_t(3));
   }
-  G.smem = size_t(G.PW + G.SW) * 4;
+  G.smem = size_t(4 + G.PW + G.SW) * 4;  // + 4 zero words for padding cells
   return G;
 }
 
