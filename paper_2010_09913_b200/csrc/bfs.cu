@@ -136,43 +136,63 @@ struct Args32 {
     if (a.trace) *reinterpret_cast<volatile int*>(&a.trace[slot]) = (v); \
   } while (0)
 
-// Shared-memory image of the frontier F_{k-1} (word indices):
-//   [0, 4)             zeros — the target of padding cells (c = -1)
-//   [4, 4 + PW)        fine bits of vertices [0, P), P = 32·PW (the hubs:
-//                      the σ = n sort puts high degrees first)
-//   [sbase, sbase+SW)  summary of the rest: bit t <-> vertices
-//                      [P + t·2^gsh, P + (t+1)·2^gsh) contain a frontier vertex
-struct Probe {
-  const uint32_t* sm;
-  const uint32_t* Fc;  // the full frontier in global memory (L2-resident)
-  int32_t P, sbase, gsh;
+// Shared-memory image of the frontier F_{k-1} as ONE virtual bit array:
+//   bits [0, P)      fine frontier bits of vertices [0, P), P = 32·PW (the
+//                    hubs: the σ = n sort puts high degrees first)
+//   bits [P, P+G)    summary of the rest: bit P + t says vertices
+//                    [P + 256t, P + 256t + 256) hold a frontier vertex
+// preceded by 4 zero words, the target of padding cells (c = -1). Cell c maps
+// to virtual bit v = min(c, P + ((c - P) >> 8)) — c itself in the prefix, its
+// summary bit in the tail — so every probe is the same shared load; only a
+// set summary bit needs the exact word from global memory (L2-resident).
+constexpr int kSummaryShift = 8;  // 256 vertices (8 frontier words) per summary bit
+constexpr int kSummaryWordShift = kSummaryShift - 5;
 
-  // Frontier bit of cell value c (c = -1 for padding). One shared load on the
-  // common path; the global word only when the summary bit is set.
-  __device__ __forceinline__ bool operator()(int32_t c) const {
-    const bool pre = c < P;
-    const int32_t d = c - P;
-    const int32_t idx = pre ? (c >> 5) + 4 : sbase + (d >> (gsh + 5));
-    const int32_t sh = pre ? c : (d >> gsh);
-    const uint32_t word = sm[idx];
-    bool b = __funnelshift_r(word, word, sh) & 1u;  // bit (sh mod 32)
-    if (!pre && b) b = (Fc[c >> 5] >> (c & 31)) & 1u;
-    return b;
+struct Probe {
+  const uint32_t* sm;  // word 0 = first prefix word; sm[-4..-1] are zero
+  const uint32_t* Fc;  // the full frontier in global memory
+  int32_t P;
+
+  __device__ __forceinline__ uint32_t vbit(int32_t c) const {
+    const int32_t v = min(c, P + ((c - P) >> kSummaryShift));
+    const uint32_t word = sm[v >> 5];
+    return __funnelshift_r(word, word, v) & 1u;  // bit (v mod 32)
+  }
+  __device__ __forceinline__ uint32_t exact(int32_t c) const {
+    return (Fc[c >> 5] >> (c & 31)) & 1u;  // L1 is invalidated by every grid.sync fence
   }
 };
 
+// Four cells of one column (rows 4·lg .. 4·lg+3). Prefix hits are final; a
+// set summary bit is resolved against the global frontier right away, before
+// the next column, so each row still sees its cells in ascending order.
 template <bool kSelMax>
 __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32_t& hit,
                                            int32_t (&best)[4]) {
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
+  uint32_t need = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const bool b = pr(c[q]);
+    const uint32_t b = pr.vbit(c[q]);
+    const bool def = b && c[q] < pr.P;
     if (kSelMax) {
-      // ascending columns: the last hit is the max frontier position
-      best[q] = b ? c[q] : best[q];
+      best[q] = def ? c[q] : best[q];  // ascending columns: the last hit is the max
     } else {
-      hit |= uint32_t(b) << q;
+      hit |= uint32_t(def) << q;
+    }
+    need |= uint32_t(b && c[q] >= pr.P) << q;
+  }
+  if (need) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if ((need >> q) & 1u) {
+        const uint32_t e = pr.exact(c[q]);
+        if (kSelMax) {
+          best[q] = e ? c[q] : best[q];
+        } else {
+          hit |= e << q;
+        }
+      }
     }
   }
 }
@@ -297,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
-    const Probe pr{sm, Fc, a.PW * 32, 4 + a.PW, a.gshift + 5};
+    const Probe pr{sm + 4, Fc, a.PW * 32};
 
     for (;;) {
       int32_t t = 0;
@@ -647,22 +667,17 @@ struct Geometry {
 Geometry geometry32(const ssb_graph& g) {
   Geometry G;
   G.NW = (g.n_padded + 31) / 32;
-  const int64_t budget_words = int64_t(env_int("SSB_SMEM_KB", 200)) * 1024 / 4;
+  const int64_t budget_words = int64_t(env_int("SSB_SMEM_KB", 200)) * 1024 / 4 - 4;
   const int64_t nw4 = (G.NW + 3) & ~int64_t(3);
+  G.gshift = kSummaryWordShift;  // summary bit = 2^gshift frontier words
   if (nw4 <= budget_words) {
     G.PW = int32_t(nw4);
     G.SW = 0;
-    G.gshift = 0;
   } else {
-    const int64_t sum_budget = budget_words * env_int("SSB_SUMMARY_PCT", 25) / 100;
-    int gs = env_int("SSB_GSHIFT", -1);
-    if (gs < 0) {
-      gs = 0;
-      while ((((G.NW >> gs) + 31) / 32 + 3) / 4 * 4 > sum_budget) ++gs;
-    }
-    G.gshift = gs;
-    G.SW = int32_t(((((G.NW + (int64_t{1} << gs) - 1) >> gs) + 31) / 32 + 3) / 4 * 4);
-    G.PW = int32_t(std::max<int64_t>(0, (budget_words - G.SW)) & ~int64_t(3));
+    // summary over the whole id range (an upper bound for the tail), rest prefix
+    const int64_t groups = (G.NW + (int64_t{1} << G.gshift) - 1) >> G.gshift;
+    G.SW = int32_t(((groups + 31) / 32 + 3) / 4 * 4);
+    G.PW = int32_t(std::max<int64_t>(0, budget_words - G.SW) & ~int64_t(3));
   }
   G.smem = size_t(4 + G.PW + G.SW) * 4;  // + 4 zero words for padding cells
   return G;
