@@ -116,8 +116,14 @@ struct Args32 {
   int32_t* level;
   int32_t* parent;
   int64_t* stats;      // [kItersPerLaunch][kStatW]
-  uint32_t* task_ctr;  // [kItersPerLaunch]
-  int32_t n_tasks;
+  uint32_t* task_ctr;  // [kItersPerLaunch] tasks grabbed per iteration
+  uint32_t* task_out;  // [kItersPerLaunch] tasks kept for the next iteration
+  int32_t* tlist0;     // active task lists (ping-pong by iteration parity)
+  int32_t* tlist1;
+  uint8_t* tskip;      // per task: every unit skipped in its last sweep
+  unsigned long long* gone_chunks;  // chunks of retired tasks (skipped forever)
+  int32_t n_tasks;     // active tasks entering iteration k_begin
+  unsigned long long gone_base;  // chunks of tasks retired before k_begin
   int32_t n_chunks;
   int32_t PW;      // frontier prefix words staged in shared memory
   int32_t SW;      // summary words staged in shared memory
@@ -288,6 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   const uint64_t pol = evict_first_policy();
   uint64_t t_prev = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
+  int32_t n_in = a.n_tasks;                  // active tasks entering iteration k
+  unsigned long long gone = a.gone_base;     // chunks of tasks retired before k
 
   for (int32_t k = a.k_begin; k < a.k_end; ++k) {
     const int32_t rec = k - a.k_begin;
@@ -319,11 +327,19 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
     const Probe pr{sm + 4, Fc, a.PW * 32};
 
+    // Active task list: iteration 1 walks every task; later iterations only the
+    // tasks kept by the previous one. A task whose units were all skipped in
+    // two consecutive iterations (so both frontier buffers hold zeros for its
+    // chunks) is retired: SlimWork would skip it forever, and its chunks are
+    // counted as skipped through gone_chunks.
+    const int32_t* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
+    int32_t* list_out = (k & 1) ? a.tlist1 : a.tlist0;
     for (;;) {
       int32_t t = 0;
       if (lane == 0) t = int32_t(atomicAdd(&a.task_ctr[rec], 1u));
       t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= a.n_tasks) break;
+      if (t >= n_in) break;
+      if (k > 1) t = list_in[t];
       const int32_t ub = a.task_begin[t], ue = a.task_begin[t + 1];
 
       // window: lane l owns unit ub + l
@@ -354,6 +370,18 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       const bool is_long = has && !skip && U.col_len >= kWarpUnitCols;
       uint32_t longs = __ballot_sync(0xffffffffu, is_long);
       uint32_t active = __ballot_sync(0xffffffffu, has && !skip && !is_long);
+      {
+        const bool all_skipped = (longs | active) == 0u;
+        const uint32_t firsts = __ballot_sync(0xffffffffu, has && U.col_begin == 0);
+        if (lane == 0) {
+          if (a.slimwork && all_skipped && a.tskip[t]) {
+            atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
+          } else {
+            list_out[atomicAdd(&a.task_out[rec], 1u)] = t;
+            a.tskip[t] = all_skipped;
+          }
+        }
+      }
 
       while (longs) {
         const int32_t sl = __ffs(longs) - 1;
@@ -495,11 +523,14 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(1, 4);
     const int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+    n_in = int32_t(*reinterpret_cast<volatile uint32_t*>(&a.task_out[rec]));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const uint64_t t = globaltimer();
       a.stats[rec * kStatW + 5] = int64_t(t - t_prev);
+      a.stats[rec * kStatW + 2] += int64_t(gone);  // retired tasks' chunks: skipped
       t_prev = t;
     }
+    gone += *reinterpret_cast<volatile unsigned long long*>(&a.gone_chunks[rec]);
     if (front == 0) break;  // is_converged: no row newly reached
   }
 }
@@ -693,8 +724,15 @@ void build_plan32(ssb_graph& g, int64_t L) {
   std::vector<ssb_unit> units;
   std::vector<int32_t> split_units;
   units.reserve(g.n_chunks + 16);
+  P.empty_chunks = 0;
   for (int64_t i = 0; i < g.n_chunks; ++i) {
     const int64_t cl = g.cl_host[i];
+    if (cl == 0) {
+      // Chunks without cells (all rows isolated; 1.07M of 2.1M at S26) can
+      // never reach a row: no unit, counted analytically (bfs_run).
+      ++P.empty_chunks;
+      continue;
+    }
     if (L <= 0 || cl <= L) {
       units.push_back({int32_t(i), 0, int32_t(cl), -1});
     } else {
@@ -732,6 +770,8 @@ void build_plan32(ssb_graph& g, int64_t L) {
   P.split_hit.alloc(std::max<size_t>(split_units.size(), 1));
   P.split_best.alloc(std::max<size_t>(split_units.size(), 1) * 32);
   P.split_count.alloc(std::max<size_t>(split_units.size(), 1));
+  P.tlist.alloc(std::max<size_t>(2 * (tb.size() - 1), 2));
+  P.tskip.alloc(std::max<size_t>(tb.size() - 1, 1));
   SSB_CUDA(cudaMemcpyAsync(P.units.p, units.data(), sizeof(ssb_unit) * units.size(),
                            cudaMemcpyHostToDevice, s));
   SSB_CUDA(cudaMemcpyAsync(P.task_begin.p, tb.data(), 4 * tb.size(), cudaMemcpyHostToDevice, s));
@@ -804,11 +844,16 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   g.level.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
   g.parent.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
   g.dstats.ensure(size_t(kItersPerLaunch) * kStatW);
-  g.dctrl.ensure(size_t(kItersPerLaunch));
+  // control words: task_ctr [K] | task_out [K] | gone_chunks [K] (8-byte)
+  g.dctrl.ensure(size_t(kItersPerLaunch) * 4);
+  uint32_t* task_ctr = g.dctrl.p;
+  uint32_t* task_out = task_ctr + kItersPerLaunch;
+  auto* gone = reinterpret_cast<unsigned long long*>(task_out + kItersPerLaunch);
 
   // init_state (semiring.cpp:56-88) in 1-bit form
   SSB_CUDA(cudaMemsetAsync(R.visited, 0, size_t(R.NW4) * 4 * 2, s));  // visited + F0
   SSB_CUDA(cudaMemsetAsync(R.S0, 0, size_t(R.SW4) * 4 * 3, s));
+  SSB_CUDA(cudaMemsetAsync(g.plan.tskip.p, 0, g.plan.tskip.bytes(), s));
   set_root_kernel<<<1, 1, 0, s>>>(R.visited, R.F0, G.SW ? R.S0 : nullptr, g.level.p, g.parent.p,
                                   root_pos, root_code, G.PW, G.gshift);
   SSB_CUDA(cudaGetLastError());
@@ -841,8 +886,14 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   a.level = g.level.p;
   a.parent = g.parent.p;
   a.stats = g.dstats.p;
-  a.task_ctr = g.dctrl.p;
+  a.task_ctr = task_ctr;
+  a.task_out = task_out;
+  a.gone_chunks = gone;
+  a.tlist0 = g.plan.tlist.p;
+  a.tlist1 = g.plan.tlist.p + g.plan.n_tasks;
+  a.tskip = g.plan.tskip.p;
   a.n_tasks = int32_t(g.plan.n_tasks);
+  a.gone_base = 0;
   a.n_chunks = int32_t(g.n_chunks);
   a.PW = G.PW;
   a.SW = G.SW;
@@ -907,7 +958,25 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
       }
     }
     collect_stats(rec, k, ran, stats);
+    {
+      // chunks without cells: processed (0 columns, 0 segments) unless SlimWork
+      // skips the root's own chunk when the root is its only real row
+      const int64_t rc = root_pos / 32;
+      const bool z_skip = o.slimwork && g.cl_host[rc] == 0 && std::min<int64_t>(32, g.n - rc * 32) == 1;
+      for (size_t i = stats.size() - size_t(ran); i < stats.size(); ++i) {
+        stats[i].chunks_processed += g.plan.empty_chunks - (z_skip ? 1 : 0);
+        stats[i].chunks_skipped += z_skip ? 1 : 0;
+      }
+    }
     if (conv) return true;
+    // carry the active task list and the retired-chunk count into the next launch
+    std::vector<uint32_t> outs(static_cast<size_t>(ran));
+    std::vector<unsigned long long> gones(static_cast<size_t>(ran));
+    SSB_CUDA(cudaMemcpyAsync(outs.data(), task_out, 4 * ran, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(gones.data(), gone, 8 * ran, cudaMemcpyDeviceToHost, s));
+    g.sc.sync();
+    a.n_tasks = int32_t(outs.back());
+    for (auto x : gones) a.gone_base += x;
     k += ran;
   }
   return false;

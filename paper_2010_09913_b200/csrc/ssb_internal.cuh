@@ -108,12 +108,15 @@ struct ssb_bfs_plan {  // cached per slimchunk_len
   int64_t n_units = 0;
   int64_t n_tasks = 0;
   int64_t n_split = 0;
+  int64_t empty_chunks = 0;  // chunks with cl == 0 (no unit)
   ssb::DevBuf<ssb_unit> units;
   ssb::DevBuf<int32_t> task_begin;    // n_tasks + 1
   ssb::DevBuf<int32_t> split_units;   // units per split chunk
   ssb::DevBuf<uint32_t> split_hit;    // n_split
   ssb::DevBuf<int32_t> split_best;    // n_split * 32
   ssb::DevBuf<uint32_t> split_count;  // n_split
+  ssb::DevBuf<int32_t> tlist;         // 2 * n_tasks: active task lists (ping-pong)
+  ssb::DevBuf<uint8_t> tskip;         // n_tasks: all units skipped last time
 };
 
 // Device-resident SlimSellRepr (repr.hpp:33-55) plus the BFS workspace.
