@@ -1,0 +1,3 @@
+// Drop-in include path for the reference header slimsell/graph.hpp.
+#pragma once
+#include "slimsell_b200/slimsell.hpp"

@@ -1,0 +1,455 @@
+// slimsell_b200/slimsell.hpp — header-only C++ façade of the B200 BFS-SpMV
+// path with the reference library's spelling (namespace slimsell, the types
+// and functions of /root/reference/proj/include/slimsell/{graph,generator,
+// repr,semiring,bfs}.hpp). Every data-path call crosses the C-ABI in
+// <slimsell_b200.h> into libslimsell_b200.so (sm_100a); link with
+// -lslimsell_b200. There is no CPU fallback: a device failure throws.
+//
+// Everything lives in the inline namespace slimsell::b200, so user code keeps
+// writing slimsell::bfs_spmv(...) while the mangled names differ from the
+// reference's — both libraries can be linked into one test binary.
+//
+// Differences a maintainer should know:
+//  * Graph and SlimSellRepr own DEVICE handles; their host arrays
+//    (Graph::edges(), SlimSellRepr::col/cs/cl/perm/inv_perm) are exported
+//    lazily on first access and cached.
+//  * BfsOptions::schedule / workers are accepted and ignored.
+//  * BfsOptions::selmax_compat (default true) reproduces the reference's
+//    sel-max root encoding; false gives corrected parents.
+//  * bfs_traditional is the reference's CPU oracle and is not part of this
+//    library.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+#include "slimsell_b200.h"
+
+namespace slimsell {
+inline namespace b200 {
+
+// ---- graph.hpp ----------------------------------------------------------
+using vid_t = std::int64_t;
+
+namespace detail {
+[[noreturn]] inline void raise(int rc) {
+  const std::string msg = ssb_last_error();
+  switch (rc) {
+    case SSB_EINVAL: throw std::invalid_argument(msg);
+    case SSB_ERANGE: throw std::out_of_range(msg);
+    default: throw std::runtime_error("slimsell_b200: " + msg);
+  }
+}
+inline void check(int rc) {
+  if (rc != SSB_OK) raise(rc);
+}
+}  // namespace detail
+
+/// Normalised undirected graph (graph.hpp:31-51) held on the device.
+class Graph {
+ public:
+  Graph() = default;
+
+  /// graph.hpp:36 — orient, drop self-loops, sort, dedup (on the device).
+  static Graph from_pairs(std::vector<std::pair<vid_t, vid_t>> pairs, vid_t n = -1) {
+    std::vector<std::int64_t> uv(2 * pairs.size());
+    for (std::size_t i = 0; i < pairs.size(); ++i) {
+      uv[2 * i] = pairs[i].first;
+      uv[2 * i + 1] = pairs[i].second;
+    }
+    ssb_edges* h = nullptr;
+    detail::check(ssb_edges_from_pairs(uv.data(), static_cast<std::int64_t>(pairs.size()), n, &h));
+    return Graph(h);
+  }
+
+  vid_t num_vertices() const { return n_; }
+  vid_t num_edges() const { return m_; }
+
+  /// graph.hpp:44 — exported from the device on first use.
+  const std::vector<std::pair<vid_t, vid_t>>& edges() const {
+    if (!edges_cache_) {
+      std::vector<std::int64_t> uv(2 * m_);
+      if (m_) detail::check(ssb_edges_export(h_.get(), uv.data()));
+      auto e = std::make_shared<std::vector<std::pair<vid_t, vid_t>>>(m_);
+      for (vid_t i = 0; i < m_; ++i) (*e)[i] = {uv[2 * i], uv[2 * i + 1]};
+      edges_cache_ = std::move(e);
+    }
+    return *edges_cache_;
+  }
+
+  bool has_edge(vid_t u, vid_t v) const {  // graph.cpp:88-92
+    if (u == v) return false;
+    if (u > v) std::swap(u, v);
+    const auto& e = edges();
+    auto it = std::lower_bound(e.begin(), e.end(), std::make_pair(u, v));
+    return it != e.end() && *it == std::make_pair(u, v);
+  }
+
+  ssb_edges* handle() const { return h_.get(); }
+  explicit Graph(ssb_edges* h) : h_(h, &ssb_edges_destroy) {
+    detail::check(ssb_edges_info(h, &n_, &m_));
+  }
+
+ private:
+  std::shared_ptr<ssb_edges> h_;
+  vid_t n_ = 0, m_ = 0;
+  mutable std::shared_ptr<std::vector<std::pair<vid_t, vid_t>>> edges_cache_;
+};
+
+/// graph.hpp:63-69
+struct CsrView {
+  std::vector<vid_t> row;
+  std::vector<vid_t> col;
+  vid_t num_vertices() const { return static_cast<vid_t>(row.size()) - 1; }
+  bool has_edge(vid_t u, vid_t v) const {
+    if (u < 0 || u >= num_vertices() || v < 0 || v >= num_vertices()) return false;
+    return std::binary_search(col.begin() + row[u], col.begin() + row[u + 1], v);
+  }
+};
+
+/// graph.hpp:71 (graph.cpp:212-232), on the device.
+inline CsrView to_csr(const Graph& g) {
+  CsrView c;
+  c.row.resize(g.num_vertices() + 1);
+  c.col.resize(2 * g.num_edges());
+  detail::check(ssb_to_csr(g.handle(), c.row.data(), c.col.data()));
+  return c;
+}
+
+// ---- generator.hpp ------------------------------------------------------
+/// generator.hpp:55 — bit-exact counter-based generation on the device.
+inline Graph gen_kronecker(std::int64_t scale, std::int64_t edgefactor, std::uint64_t seed,
+                           const std::array<double, 4>& initiator = {0.57, 0.19, 0.19, 0.05}) {
+  ssb_edges* h = nullptr;
+  detail::check(ssb_gen_kronecker(scale, edgefactor, seed, initiator.data(), &h));
+  return Graph(h);
+}
+
+inline Graph gen_path(vid_t n) {  // generator.hpp:62
+  if (n < 1) throw std::invalid_argument("path needs n >= 1");
+  std::vector<std::pair<vid_t, vid_t>> p;
+  for (vid_t i = 0; i + 1 < n; ++i) p.emplace_back(i, i + 1);
+  return Graph::from_pairs(std::move(p), n);
+}
+
+inline Graph gen_clique(vid_t n) {  // generator.hpp:63
+  if (n < 1) throw std::invalid_argument("clique needs n >= 1");
+  std::vector<std::pair<vid_t, vid_t>> p;
+  for (vid_t u = 0; u < n; ++u)
+    for (vid_t v = u + 1; v < n; ++v) p.emplace_back(u, v);
+  return Graph::from_pairs(std::move(p), n);
+}
+
+inline Graph gen_star(vid_t n) {  // generator.hpp:64
+  if (n < 1) throw std::invalid_argument("star needs n >= 1");
+  std::vector<std::pair<vid_t, vid_t>> p;
+  for (vid_t v = 1; v < n; ++v) p.emplace_back(0, v);
+  return Graph::from_pairs(std::move(p), n);
+}
+
+// ---- semiring.hpp -------------------------------------------------------
+using val_t = std::int64_t;
+inline constexpr val_t kInf = std::numeric_limits<val_t>::max();
+inline constexpr vid_t kNoParent = -1;
+
+enum class Variant { tropical, real, boolean, selmax };
+inline constexpr Variant kAllVariants[] = {Variant::tropical, Variant::real, Variant::boolean,
+                                           Variant::selmax};
+
+/// semiring.hpp:37-49 — the scalar algebra, for API parity (the device
+/// kernels implement the same operations).
+struct SemiringSpec {
+  Variant variant;
+  const char* name;
+  val_t zero, one, edge_value, pad_value;
+  val_t (*plus)(val_t, val_t);
+  val_t (*times)(val_t, val_t);
+};
+
+inline const SemiringSpec& semiring(Variant v) {
+  static const SemiringSpec specs[] = {
+      {Variant::tropical, "tropical", kInf, 0, 1, kInf,
+       [](val_t a, val_t b) { return a < b ? a : b; },
+       [](val_t a, val_t b) { return (a == kInf || b == kInf) ? kInf : a + b; }},
+      {Variant::real, "real", 0, 1, 1, 0,
+       [](val_t a, val_t b) { return static_cast<val_t>(static_cast<std::uint64_t>(a) + static_cast<std::uint64_t>(b)); },
+       [](val_t a, val_t b) { return static_cast<val_t>(static_cast<std::uint64_t>(a) * static_cast<std::uint64_t>(b)); }},
+      {Variant::boolean, "boolean", 0, 1, 1, 0, [](val_t a, val_t b) { return a | b; },
+       [](val_t a, val_t b) { return a & b; }},
+      {Variant::selmax, "selmax", 0, 1, 1, 0, [](val_t a, val_t b) { return a > b ? a : b; },
+       [](val_t a, val_t b) { return static_cast<val_t>(static_cast<std::uint64_t>(a) * static_cast<std::uint64_t>(b)); }},
+  };
+  return specs[static_cast<int>(v)];
+}
+
+inline const char* variant_name(Variant v) { return semiring(v).name; }
+
+inline std::optional<Variant> parse_variant(std::string_view name) {
+  for (Variant v : kAllVariants)
+    if (name == semiring(v).name) return v;
+  return std::nullopt;
+}
+
+// ---- repr.hpp -----------------------------------------------------------
+inline constexpr vid_t kPadMarker = -1;
+
+namespace detail {
+/// A host view of one layout array, exported from the device on first use.
+class LazyArray {
+ public:
+  using Fill = std::function<void(std::vector<std::int64_t>&)>;
+  LazyArray() = default;
+  explicit LazyArray(Fill f) : fill_(std::make_shared<Fill>(std::move(f))) {}
+  const std::vector<std::int64_t>& get() const {
+    if (!cache_) {
+      cache_ = std::make_shared<std::vector<std::int64_t>>();
+      (*fill_)(*cache_);
+    }
+    return *cache_;
+  }
+  std::int64_t operator[](std::size_t i) const { return get()[i]; }
+  std::size_t size() const { return get().size(); }
+  const std::int64_t* data() const { return get().data(); }
+  auto begin() const { return get().begin(); }
+  auto end() const { return get().end(); }
+  operator const std::vector<std::int64_t>&() const { return get(); }
+
+ private:
+  std::shared_ptr<Fill> fill_;
+  mutable std::shared_ptr<std::vector<std::int64_t>> cache_;
+};
+}  // namespace detail
+
+/// repr.hpp:33-55 — the SlimSell layout, resident on the device.
+struct SlimSellRepr {
+  std::int64_t C = 1;
+  std::int64_t sigma = 1;
+  vid_t n = 0;
+  vid_t n_padded = 0;
+  std::int64_t n_chunks = 0;
+  vid_t nonzeros = 0;
+  detail::LazyArray col, cs, cl, perm, inv_perm;
+  std::int64_t padding = 0;
+
+  vid_t chunk_row_begin(std::int64_t chunk) const { return static_cast<vid_t>(chunk * C); }
+  vid_t chunk_row_end(std::int64_t chunk) const {
+    const vid_t end = static_cast<vid_t>((chunk + 1) * C);
+    return end < n ? end : n;
+  }
+  std::int64_t n_cells() const { return n_cells_; }
+  ssb_graph* handle() const { return h_.get(); }
+
+  explicit SlimSellRepr(ssb_graph* h) : h_(h, &ssb_graph_destroy) {
+    ssb_layout_info info;
+    detail::check(ssb_graph_info(h, &info));
+    C = info.C;
+    sigma = info.sigma;
+    n = info.n;
+    n_padded = info.n_padded;
+    n_chunks = info.n_chunks;
+    nonzeros = info.nonzeros;
+    padding = info.padding;
+    n_cells_ = info.n_cells;
+    auto hp = h_;
+    auto exp = [hp](int which, std::int64_t count) {
+      return [hp, which, count](std::vector<std::int64_t>& v) {
+        v.resize(static_cast<std::size_t>(count));
+        std::int64_t* p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+        p[which] = v.data();
+        if (count) detail::check(ssb_graph_export(hp.get(), p[0], p[1], p[2], p[3], p[4]));
+      };
+    };
+    col = detail::LazyArray(exp(0, n_cells_));
+    cs = detail::LazyArray(exp(1, n_chunks));
+    cl = detail::LazyArray(exp(2, n_chunks));
+    perm = detail::LazyArray(exp(3, n));
+    inv_perm = detail::LazyArray(exp(4, n));
+  }
+
+ private:
+  std::shared_ptr<ssb_graph> h_;
+  std::int64_t n_cells_ = 0;
+};
+
+/// repr.hpp:66 — built on the device. Throws invalid_argument for C<=0, σ<=0.
+inline SlimSellRepr build_slimsell(const Graph& g, std::int64_t C, std::int64_t sigma) {
+  ssb_graph* h = nullptr;
+  detail::check(ssb_build_slimsell(g.handle(), C, sigma, &h));
+  return SlimSellRepr(h);
+}
+
+inline std::int64_t storage_cells(const SlimSellRepr& r) {  // repr.hpp:62 (col + cs + cl)
+  return r.n_cells() + 2 * r.n_chunks;
+}
+
+/// repr.hpp:90-92 — chunk-range product with the literal int64 semiring.
+inline void spmv_step(const SlimSellRepr& r, const SemiringSpec& s, std::span<const val_t> x_prev,
+                      std::span<val_t> out, std::int64_t chunk_begin, std::int64_t chunk_end) {
+  if (x_prev.size() != static_cast<std::size_t>(r.n_padded) ||
+      out.size() != static_cast<std::size_t>(r.n_padded))
+    throw std::invalid_argument("x_prev/out length must be n_padded");
+  if (r.n_padded == 0) {
+    if (chunk_begin != 0 || chunk_end != 0) throw std::invalid_argument("chunk range out of bounds");
+    return;
+  }
+  detail::check(ssb_spmv_step(r.handle(), static_cast<int>(s.variant), x_prev.data(), out.data(),
+                              chunk_begin, chunk_end));
+}
+
+/// repr.hpp:97-98
+inline std::vector<val_t> spmv_step(const SlimSellRepr& r, const SemiringSpec& s,
+                                    std::span<const val_t> x_prev) {
+  std::vector<val_t> out(x_prev.size());
+  spmv_step(r, s, x_prev, out, 0, r.n_chunks);
+  return out;
+}
+
+/// repr.hpp:104-107 (repr.cpp:239-253) — pure relabelling through perm.
+inline std::vector<val_t> permute_in(std::span<const val_t> v, const SlimSellRepr& r, val_t fill) {
+  if (v.size() != static_cast<std::size_t>(r.n)) throw std::invalid_argument("input vector length");
+  std::vector<val_t> out(r.n_padded, fill);
+  for (vid_t p = 0; p < r.n; ++p) out[p] = v[r.perm[p]];
+  return out;
+}
+
+inline std::vector<val_t> permute_out(std::span<const val_t> v, const SlimSellRepr& r) {
+  if (v.size() != static_cast<std::size_t>(r.n_padded))
+    throw std::invalid_argument("permuted vector length");
+  std::vector<val_t> out(r.n);
+  for (vid_t p = 0; p < r.n; ++p) out[r.perm[p]] = v[p];
+  return out;
+}
+
+// ---- bfs.hpp ------------------------------------------------------------
+enum class Schedule { static_blocks, dynamic_queue };
+
+struct BfsOptions {  // bfs.hpp:16-24
+  Variant variant = Variant::tropical;
+  bool slimwork = false;
+  std::int64_t slimchunk_len = 0;
+  Schedule schedule = Schedule::static_blocks;  // ignored
+  int workers = 1;                              // ignored
+  std::int64_t max_iterations = 0;
+  bool want_parents = true;
+  bool selmax_compat = true;
+};
+
+struct IterStats {  // bfs.hpp:26-34
+  std::int64_t iteration = 0;
+  std::int64_t elapsed_ns = 0;
+  std::int64_t chunks_processed = 0;
+  std::int64_t chunks_skipped = 0;
+  std::int64_t subchunks_processed = 0;
+  std::int64_t columns_processed = 0;
+  std::int64_t frontier_size = 0;
+};
+
+struct BfsResult {  // bfs.hpp:36-42
+  std::vector<val_t> dist;
+  std::vector<vid_t> parent;
+  std::int64_t iterations = 0;
+  std::vector<IterStats> per_iter;
+};
+
+class BfsCapError : public std::runtime_error {  // bfs.hpp:46-54
+ public:
+  BfsCapError(std::string what, BfsResult partial)
+      : std::runtime_error(std::move(what)), partial_(std::move(partial)) {}
+  const BfsResult& partial() const { return partial_; }
+
+ private:
+  BfsResult partial_;
+};
+
+struct SubchunkPlan {  // bfs.hpp:58-66
+  struct Segment {
+    std::int64_t chunk = 0;
+    std::int64_t col_begin = 0;
+    std::int64_t col_len = 0;
+  };
+  std::vector<Segment> segments;
+  std::vector<std::int64_t> chunk_first;
+};
+
+/// bfs.hpp:69 (bfs.cpp:10-22) — the reference's segment list; the device
+/// builds the same segments as its work units.
+inline SubchunkPlan plan_subchunks(const SlimSellRepr& r, std::int64_t L) {
+  if (L < 1) throw std::invalid_argument("subchunk length must be >= 1");
+  SubchunkPlan plan;
+  plan.chunk_first.reserve(r.n_chunks + 1);
+  for (std::int64_t i = 0; i < r.n_chunks; ++i) {
+    plan.chunk_first.push_back(static_cast<std::int64_t>(plan.segments.size()));
+    for (std::int64_t c = 0; c < r.cl[i]; c += L)
+      plan.segments.push_back({i, c, std::min(L, r.cl[i] - c)});
+  }
+  plan.chunk_first.push_back(static_cast<std::int64_t>(plan.segments.size()));
+  return plan;
+}
+
+/// bfs.hpp:73-74
+inline std::vector<val_t> combine_partials(const SemiringSpec& s,
+                                           const std::vector<std::vector<val_t>>& partials) {
+  if (partials.empty()) return {};
+  std::vector<val_t> out = partials.front();
+  for (std::size_t i = 1; i < partials.size(); ++i) {
+    if (partials[i].size() != out.size())
+      throw std::invalid_argument("partial accumulator length mismatch");
+    for (std::size_t j = 0; j < out.size(); ++j) out[j] = s.plus(out[j], partials[i][j]);
+  }
+  return out;
+}
+
+/// bfs.hpp:80-81 — algebraic BFS on the device. As the reference: sel-max
+/// parents always (when want_parents), the other variants only with a CSR
+/// (dp_transform semantics, evaluated on the device over the layout).
+inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& opts,
+                          const CsrView* csr_for_parents = nullptr) {
+  ssb_bfs_options o{};
+  o.variant = static_cast<std::int32_t>(opts.variant);
+  o.slimwork = opts.slimwork;
+  o.slimchunk_len = opts.slimchunk_len;
+  o.schedule = static_cast<std::int32_t>(opts.schedule);
+  o.workers = opts.workers;
+  o.max_iterations = opts.max_iterations;
+  o.want_parents = opts.want_parents &&
+                   (opts.variant == Variant::selmax || csr_for_parents != nullptr);
+  o.selmax_compat = opts.selmax_compat;
+  BfsResult res;
+  res.dist.resize(r.n);
+  res.parent.resize(r.n);
+  std::int64_t plen = 0, iters = 0;
+  std::vector<ssb_iter_stats> st(std::min<std::int64_t>(r.n + 2, 1 << 16));
+  int rc = ssb_bfs_spmv(r.handle(), root, &o, res.dist.data(), res.parent.data(), &plen, st.data(),
+                        static_cast<std::int64_t>(st.size()), &iters);
+  if (rc == SSB_OK || rc == SSB_ECAP) {
+    if (iters > static_cast<std::int64_t>(st.size())) {  // very deep BFS: rerun with room
+      st.resize(iters);
+      rc = ssb_bfs_spmv(r.handle(), root, &o, res.dist.data(), res.parent.data(), &plen, st.data(),
+                        static_cast<std::int64_t>(st.size()), &iters);
+    }
+  }
+  if (rc != SSB_OK && rc != SSB_ECAP) detail::raise(rc);
+  res.parent.resize(plen);
+  res.iterations = iters;
+  for (std::int64_t i = 0; i < iters; ++i) {
+    const auto& s = st[i];
+    res.per_iter.push_back({s.iteration, s.elapsed_ns, s.chunks_processed, s.chunks_skipped,
+                            s.subchunks_processed, s.columns_processed, s.frontier_size});
+  }
+  if (rc == SSB_ECAP) throw BfsCapError(ssb_last_error(), std::move(res));
+  return res;
+}
+
+}  // namespace b200
+}  // namespace slimsell

@@ -1,0 +1,154 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): chunk-range sharding with
+the per-iteration frontier all-gather reproduces the single-process reference
+result bit for bit (dist, sel-max parents incl. the root encoding, counters).
+The per-rank sweep here is a plain numpy restatement of the 1-bit iteration
+(test helper); on B200s it is the device kernel."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2010_09913_b200.sharding import ShardedFrontierExchange, partition_chunks, root_shard
+
+KINF = np.iinfo(np.int64).max
+
+
+def test_partition_chunks_balanced():
+    rng = np.random.default_rng(0)
+    cl = np.sort(rng.integers(0, 300, 5000))[::-1].copy()
+    for world in (1, 2, 3, 8):
+        rs = partition_chunks(cl, 32, world)
+        assert rs[0][0] == 0 and rs[-1][1] == cl.shape[0]
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+        cells = [int((32 * cl[b:e] + 1).sum()) for b, e in rs]
+        assert max(cells) <= (sum(cells) / world) * 1.05 + 32 * cl.max()
+    assert root_shard(range(10), 1, 4) == [1, 5, 9]
+
+
+def sweep_range(L, b, e, F, visited, k, root_code, level, parent, slimwork, Lseg):
+    """One BFS iteration over chunks [b, e) in 1-bit form (C = 32)."""
+    n = L.n
+    newF = np.zeros(e - b, dtype=np.uint32)
+    proc = skip = cols = subs = front = 0
+    for i in range(b, e):
+        real = (1 << min(32, n - 32 * i)) - 1
+        if slimwork and visited[i] == real:
+            skip += 1
+            continue
+        proc += 1
+        cl = int(L.cl[i])
+        cols += cl
+        if Lseg > 0 and cl > 0:
+            subs += (cl + Lseg - 1) // Lseg
+        if cl == 0:
+            continue
+        grid = L.col[L.cs[i]: L.cs[i] + 32 * cl].reshape(cl, 32)
+        cells = np.where(grid >= 0, grid, 0)
+        bits = ((F[cells >> 5] >> (cells & 31)) & 1).astype(bool) & (grid >= 0)
+        hit = bits.any(axis=0)
+        mask = sum(1 << r for r in range(32) if hit[r])
+        newly = mask & ~int(visited[i]) & real
+        if newly:
+            visited[i] |= newly
+            newF[i - b] = newly
+            front += bin(newly).count("1")
+            for r in range(32):
+                if (newly >> r) & 1:
+                    row = 32 * i + r
+                    level[row] = k
+                    last = np.nonzero(bits[:, r])[0][-1]
+                    parent[row] = root_code if k == 1 else int(grid[last, r])
+    return newF, np.array([proc, skip, subs, cols, front], dtype=np.int64)
+
+
+def worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import Port
+        port_ = Port()
+        n, uv = port_.gen_kronecker(11, 16, 4)
+        row, col = port_.to_csr(n, uv)
+        L = port_.build_slimsell(n, row, col, 32, n)
+        ranges = partition_chunks(L.cl, 32, world)
+        b, e = ranges[rank]
+        ex = ShardedFrontierExchange(ranges, L.n_chunks, dist)
+        out = {}
+        for root, slimwork, Lseg in ((3, True, 8), (int(L.perm[0]), False, 0), (700, True, 0)):
+            root_pos = int(L.inv_perm[root])
+            root_code = root  # sel-max compat encoding
+            visited = np.zeros(L.n_chunks, dtype=np.uint32)
+            F = np.zeros(L.n_chunks, dtype=np.uint32)
+            visited[root_pos >> 5] |= np.uint32(1 << (root_pos & 31))
+            F[root_pos >> 5] |= np.uint32(1 << (root_pos & 31))
+            level = np.full(L.n_padded, -1, dtype=np.int64)
+            parent = np.full(L.n_padded, -1, dtype=np.int64)
+            level[root_pos], parent[root_pos] = 0, root_code
+            stats = []
+            k = 0
+            while True:
+                k += 1
+                newF, st = sweep_range(L, b, e, F, visited, k, root_code, level, parent, slimwork, Lseg)
+                res = ex.exchange(rank, newF)
+                # replicated state: everyone ORs the gathered frontier into visited
+                visited |= res.frontier
+                F = res.frontier
+                stats.append(st)
+                if not res.any_new:
+                    break
+            tot = np.stack(stats)
+            import torch
+            t = torch.from_numpy(tot.copy())
+            dist.all_reduce(t)
+            lv = torch.from_numpy(np.where(level >= 0, level, KINF))
+            pr = torch.from_numpy(parent.copy())
+            gl = [torch.zeros_like(lv) for _ in range(world)]
+            gp = [torch.zeros_like(pr) for _ in range(world)]
+            dist.all_gather(gl, lv)
+            dist.all_gather(gp, pr)
+            lvl = np.full(L.n_padded, KINF, dtype=np.int64)
+            par = np.full(L.n_padded, -1, dtype=np.int64)
+            for r, (rb, re) in enumerate(ranges):
+                lvl[32 * rb: 32 * re] = gl[r].numpy()[32 * rb: 32 * re]
+                par[32 * rb: 32 * re] = gp[r].numpy()[32 * rb: 32 * re]
+            lvl[root_pos], par[root_pos] = 0, root_code
+            d = np.empty(n, dtype=np.int64)
+            p = np.full(n, -1, dtype=np.int64)
+            d[L.perm] = lvl[:n]
+            reached = lvl[:n] != KINF
+            p[L.perm[reached]] = L.perm[par[:n][reached]]
+            ref = port_.bfs_spmv(L, root, 3, slimwork, Lseg)
+            rows = [[int(r[c]) for c in (2, 3, 4, 5, 6)] for r in ref.stats]
+            out[(root, slimwork, Lseg)] = (bool(np.array_equal(d, ref.dist)), bool(np.array_equal(p, ref.parent)),
+                                           t.numpy().tolist() == rows, k == ref.iterations)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_chunk_sharded_bfs_world2_matches_reference():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for key, (d_ok, p_ok, st_ok, it_ok) in out.items():
+        assert d_ok and p_ok and st_ok and it_ok, key
