@@ -50,7 +50,7 @@ def args_():
     ap.add_argument("--scale", type=int, default=26)
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--roots", type=int, default=64)
-    ap.add_argument("--slimchunk", type=int, default=128)
+    ap.add_argument("--slimchunk", type=int, default=2048)
     ap.add_argument("--variant", default="selmax", choices=["tropical", "real", "boolean", "selmax"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=1)

@@ -10,7 +10,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libslimsell_b200.so")
+LIB_PATH = os.environ.get("SSB_LIB", os.path.join(HERE, "libslimsell_b200.so"))  # override: experiments
 CSRC = os.path.join(HERE, "csrc")
 
 SSB_OK, SSB_EINVAL, SSB_ERANGE, SSB_ECAP, SSB_ECUDA, SSB_ENOMEM = range(6)

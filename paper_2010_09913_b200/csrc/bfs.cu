@@ -40,6 +40,7 @@
 #include <memory>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <unistd.h>
 
 #include "ssb_internal.cuh"
@@ -124,6 +125,8 @@ struct Args32 {
   unsigned long long* gone_chunks;  // chunks of retired tasks (skipped forever)
   int32_t n_tasks;     // active tasks entering iteration k_begin
   unsigned long long gone_base;  // chunks of tasks retired before k_begin
+  int64_t front_in;    // frontier size entering iteration k_begin
+  int64_t dense_thr;   // frontiers above this use the early-exit sweeps
   int32_t n_chunks;
   int32_t PW;      // frontier prefix words staged in shared memory
   int32_t SW;      // summary words staged in shared memory
@@ -148,19 +151,25 @@ struct Args32 {
 //   bits [P, P+G)    summary of the rest: bit P + t says vertices
 //                    [P + 256t, P + 256t + 256) hold a frontier vertex
 // preceded by 4 zero words, the target of padding cells (c = -1). Cell c maps
-// to virtual bit v = min(c, P + ((c - P) >> 8)) — c itself in the prefix, its
-// summary bit in the tail — so every probe is the same shared load; only a
-// set summary bit needs the exact word from global memory (L2-resident).
-constexpr int kSummaryShift = 8;  // 256 vertices (8 frontier words) per summary bit
+// to virtual bit v = min(c, (c >> S) + P - (P >> S)) — c itself in the prefix,
+// the bit of its absolute 2^S-vertex group in the tail (P is a multiple of
+// 2^S and x - (x >> S) is monotone, so the min picks the right branch) — so
+// every probe is the same shared load; only a set summary bit needs the exact
+// word from global memory (L2-resident).
+#ifndef SSB_SUMMARY_SHIFT
+#define SSB_SUMMARY_SHIFT 8
+#endif
+constexpr int kSummaryShift = SSB_SUMMARY_SHIFT;  // 2^S vertices per summary bit
 constexpr int kSummaryWordShift = kSummaryShift - 5;
 
 struct Probe {
   const uint32_t* sm;  // word 0 = first prefix word; sm[-4..-1] are zero
   const uint32_t* Fc;  // the full frontier in global memory
-  int32_t P;
+  int32_t P;           // prefix vertices (multiple of 2^S)
+  int32_t Pt;          // P - (P >> S)
 
   __device__ __forceinline__ uint32_t vbit(int32_t c) const {
-    const int32_t v = min(c, P + ((c - P) >> kSummaryShift));
+    const int32_t v = min(c, (c >> kSummaryShift) + Pt);
     const uint32_t word = sm[v >> 5];
     return __funnelshift_r(word, word, v) & 1u;  // bit (v mod 32)
   }
@@ -169,34 +178,40 @@ struct Probe {
   }
 };
 
-// Four cells of one column (rows 4·lg .. 4·lg+3). Prefix hits are final; a
-// set summary bit is resolved against the global frontier right away, before
-// the next column, so each row still sees its cells in ascending order.
-template <bool kSelMax>
+// Four cells of one column (rows 4·lg .. 4·lg+3). `hit` bit q says row q is
+// decided: for the "any" semirings the first frontier neighbour decides the
+// row (columns are swept forward), for sel-max the first one met sweeping the
+// columns BACKWARD is the largest position (rows are ascending), i.e. the
+// reference's max. Decided rows skip their remaining probes — the reduction
+// short-circuits, the column stream itself is still read in full. Prefix hits
+// are final; a set summary bit is resolved against the global frontier before
+// the next column, so each row still sees its cells in sweep order.
+// kEarly = false (sparse frontiers, where hits are rare): no masking, every
+// column is probed in ascending order and sel-max keeps the LAST hit — the
+// cheapest instruction stream. kEarly = true (dense frontiers, where the exact
+// lookups dominate): decided rows are masked out as described above.
+template <bool kSelMax, bool kEarly>
 __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32_t& hit,
                                            int32_t (&best)[4]) {
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
+  const uint32_t open = kEarly ? ~hit : 0xffffffffu;
   uint32_t need = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t b = pr.vbit(c[q]);
+    const uint32_t b = pr.vbit(c[q]) & (open >> q);
     const bool def = b && c[q] < pr.P;
-    if (kSelMax) {
-      best[q] = def ? c[q] : best[q];  // ascending columns: the last hit is the max
-    } else {
-      hit |= uint32_t(def) << q;
-    }
+    if (kSelMax) best[q] = def ? c[q] : best[q];
+    // sel-max without early exit derives its row mask from best afterwards
+    if (!kSelMax || kEarly) hit |= uint32_t(def) << q;
     need |= uint32_t(b && c[q] >= pr.P) << q;
   }
-  if (need) {
+  if (__any_sync(0xffffffffu, need)) {  // warp-uniform: no reconvergence bookkeeping
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if ((need >> q) & 1u) {
-        const uint32_t e = pr.exact(c[q]);
-        if (kSelMax) {
-          best[q] = e ? c[q] : best[q];
-        } else {
-          hit |= e << q;
+        if (pr.exact(c[q])) {
+          hit |= 1u << q;
+          if (kSelMax) best[q] = c[q];
         }
       }
     }
@@ -279,6 +294,138 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
   }
 }
 
+// Whole-warp sweep of one long unit starting at `base` (len columns). int4 i
+// of the unit = column i/8, rows 4(i%8)..+3; lane l takes i = 32s + l, so lg
+// (rows) is fixed per lane and grp picks the column within each 4-column
+// step. Out-of-range indices re-read the lane's own rows of the last column
+// (idempotent). Loads run four steps ahead of the probes. On return `hit` and
+// `best` are combined over the four lanes that share rows.
+template <bool kSelMax, bool kEarly>
+__device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int lane, int lg,
+                                           const Probe& pr, uint64_t pol, uint32_t& hit,
+                                           int32_t (&best)[4]) {
+  const int32_t nv = len * 8, imax = nv - 8 + lg;
+  const int32_t nsteps = (nv + 31) >> 5;
+  // lanes sharing rows exchange decided-row bits after every 4 steps
+  auto share = [&]() {
+    if (kEarly) {
+      hit |= __shfl_xor_sync(0xffffffffu, hit, 8);
+      hit |= __shfl_xor_sync(0xffffffffu, hit, 16);
+    }
+  };
+  if (!(kSelMax && kEarly)) {
+    // forward sweep: step s = 0, 1, ...
+    int4 v0 = ld_stream(base + min(lane, imax), pol);
+    int4 v1 = ld_stream(base + min(32 + lane, imax), pol);
+    int4 v2 = ld_stream(base + min(64 + lane, imax), pol);
+    int4 v3 = ld_stream(base + min(96 + lane, imax), pol);
+    // Steps s+4..s+7 are all full (no clamping) while s + 9 <= nsteps; the
+    // prefetch pointer then advances by 2 KB per 4 steps, offsets immediate.
+    const int4* pf = base + 128 + lane;
+    int32_t s = 0;
+    for (; s + 9 <= nsteps; s += 4, pf += 128) {
+      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      v0 = ld_stream(pf, pol);
+      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      v1 = ld_stream(pf + 32, pol);
+      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      v2 = ld_stream(pf + 64, pol);
+      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      v3 = ld_stream(pf + 96, pol);
+      share();
+    }
+    for (; s < nsteps; s += 4) {
+      const bool more = s + 4 < nsteps;  // warp-uniform
+      const int32_t i0 = (s + 4) * 32 + lane;
+      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      if (more) v0 = ld_stream(base + min(i0, imax), pol);
+      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      if (more) v1 = ld_stream(base + min(i0 + 32, imax), pol);
+      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      if (more) v2 = ld_stream(base + min(i0 + 64, imax), pol);
+      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      if (more) v3 = ld_stream(base + min(i0 + 96, imax), pol);
+      share();
+    }
+  } else {
+    // backward sweep (sel-max, early exit): steps nsteps-1 .. 0, clamped at 0
+    const int32_t top = nsteps - 1;
+    auto at = [&](int32_t st) { return base + min(32 * max(st, 0) + lane, imax); };
+    int4 v0 = ld_stream(at(top), pol);
+    int4 v1 = ld_stream(at(top - 1), pol);
+    int4 v2 = ld_stream(at(top - 2), pol);
+    int4 v3 = ld_stream(at(top - 3), pol);
+    // steps top-r-4 .. top-r-7 are all full and >= 0 while r + 8 <= nsteps
+    const int4* pf = base + 32 * (top - 4) + lane;
+    int32_t r = 0;
+    for (; r + 8 <= nsteps; r += 4, pf -= 128) {
+      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      v0 = ld_stream(pf, pol);
+      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      v1 = ld_stream(pf - 32, pol);
+      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      v2 = ld_stream(pf - 64, pol);
+      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      v3 = ld_stream(pf - 96, pol);
+      share();
+    }
+    for (; r < nsteps; r += 4) {
+      const bool more = r + 4 < nsteps;  // warp-uniform
+      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      if (more) v0 = ld_stream(at(top - r - 4), pol);
+      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      if (more) v1 = ld_stream(at(top - r - 5), pol);
+      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      if (more) v2 = ld_stream(at(top - r - 6), pol);
+      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      if (more) v3 = ld_stream(at(top - r - 7), pol);
+      share();
+    }
+  }
+  // combine the four column groups
+  if (kSelMax) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      best[q] = max(best[q], __shfl_xor_sync(0xffffffffu, best[q], 8));
+      best[q] = max(best[q], __shfl_xor_sync(0xffffffffu, best[q], 16));
+      hit |= uint32_t(best[q] >= 0) << q;
+    }
+  }
+  hit |= __shfl_xor_sync(0xffffffffu, hit, 8);
+  hit |= __shfl_xor_sync(0xffffffffu, hit, 16);
+}
+
+// One short unit per 8-lane group: column j of the unit is int4 p[8j] (lane
+// lg: rows 4lg..4lg+3). Groups shorter than maxlen re-read their last (or,
+// backward, first) column — idempotent for both reductions; groups without a
+// unit read a padding column. Loads run 4 columns ahead of the probes.
+template <bool kSelMax, bool kEarly>
+__device__ __forceinline__ void sweep_group(const int4* p, int32_t jlast, int64_t stride,
+                                            int32_t maxlen, const Probe& pr, uint64_t pol,
+                                            uint32_t& hit, int32_t (&best)[4]) {
+  constexpr bool kBack = kSelMax && kEarly;
+  auto at = [&](int32_t j) { return p + (kBack ? max(jlast - j, 0) : min(j, jlast)) * stride; };
+  int4 v0 = ld_stream(at(0), pol);
+  int4 v1 = ld_stream(at(1), pol);
+  int4 v2 = ld_stream(at(2), pol);
+  int4 v3 = ld_stream(at(3), pol);
+  for (int32_t j = 0; j < maxlen; j += 4) {
+    const bool more = j + 4 < maxlen;  // warp-uniform
+    take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+    if (more) v0 = ld_stream(at(j + 4), pol);
+    take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+    if (more) v1 = ld_stream(at(j + 5), pol);
+    take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+    if (more) v2 = ld_stream(at(j + 6), pol);
+    take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+    if (more) v3 = ld_stream(at(j + 7), pol);
+  }
+  if (kSelMax) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) hit |= uint32_t(best[q] >= 0) << q;
+  }
+}
+
 template <bool kSelMax>
 __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   extern __shared__ uint4 smem_v4[];
@@ -295,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   uint64_t t_prev = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
   int32_t n_in = a.n_tasks;                  // active tasks entering iteration k
+  int64_t front_in = a.front_in;             // |F_{k-1}|
   unsigned long long gone = a.gone_base;     // chunks of tasks retired before k
 
   for (int32_t k = a.k_begin; k < a.k_end; ++k) {
@@ -325,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
-    const Probe pr{sm + 4, Fc, a.PW * 32};
+    const Probe pr{sm + 4, Fc, a.PW * 32, a.PW * 32 - ((a.PW * 32) >> kSummaryShift)};
 
     // Active task list: iteration 1 walks every task; later iterations only the
     // tasks kept by the previous one. A task whose units were all skipped in
@@ -334,6 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     // counted as skipped through gone_chunks.
     const int32_t* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
     int32_t* list_out = (k & 1) ? a.tlist1 : a.tlist0;
+    // dense previous frontier -> early-exit sweeps (see take_cells)
+    const bool dense = front_in > a.dense_thr;
+    auto run_tasks = [&](auto early_tag) {
+    constexpr bool kEarly = decltype(early_tag)::value;
     for (;;) {
       int32_t t = 0;
       if (lane == 0) t = int32_t(atomicAdd(&a.task_ctr[rec], 1u));
@@ -397,38 +549,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         // within each 4-column step. Out-of-range indices re-read the lane's
         // own rows of the last column (idempotent).
         const int4* base = reinterpret_cast<const int4*>(a.col + a.cs[chunk] + int64_t(cb) * 32);
-        const int32_t nv = len * 8, imax = nv - 8 + lg;
-        const int32_t nsteps = (nv + 31) >> 5;
         uint32_t hit = 0;
         int32_t best[4] = {-1, -1, -1, -1};
-        int4 v0 = ld_stream(base + min(lane, imax), pol);
-        int4 v1 = ld_stream(base + min(32 + lane, imax), pol);
-        int4 v2 = ld_stream(base + min(64 + lane, imax), pol);
-        int4 v3 = ld_stream(base + min(96 + lane, imax), pol);
-        for (int32_t s = 0; s < nsteps; s += 4) {
-          const bool more = s + 4 < nsteps;  // warp-uniform
-          const int32_t i0 = (s + 4) * 32 + lane;
-          take_cells<kSelMax>(v0, pr, hit, best);
-          if (more) v0 = ld_stream(base + min(i0, imax), pol);
-          take_cells<kSelMax>(v1, pr, hit, best);
-          if (more) v1 = ld_stream(base + min(i0 + 32, imax), pol);
-          take_cells<kSelMax>(v2, pr, hit, best);
-          if (more) v2 = ld_stream(base + min(i0 + 64, imax), pol);
-          take_cells<kSelMax>(v3, pr, hit, best);
-          if (more) v3 = ld_stream(base + min(i0 + 96, imax), pol);
-        }
-        // combine the four column groups, then form the unit's row mask
-        if (kSelMax) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            best[q] = max(best[q], __shfl_xor_sync(0xffffffffu, best[q], 8));
-            best[q] = max(best[q], __shfl_xor_sync(0xffffffffu, best[q], 16));
-            hit |= uint32_t(best[q] >= 0) << q;
-          }
-        } else {
-          hit |= __shfl_xor_sync(0xffffffffu, hit, 8);
-          hit |= __shfl_xor_sync(0xffffffffu, hit, 16);
-        }
+        sweep_long<kSelMax, kEarly>(base, len, lane, lg, pr, pol, hit, best);
         uint32_t m = hit << (4 * lg);
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
         m |= __shfl_xor_sync(0xffffffffu, m, 2);
@@ -469,25 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         const int64_t stride = len > 0 ? 8 : 0;
         uint32_t hit = 0;
         int32_t best[4] = {-1, -1, -1, -1};
-        int4 v0 = ld_stream(p, pol);
-        int4 v1 = ld_stream(p + min(1, jlast) * stride, pol);
-        int4 v2 = ld_stream(p + min(2, jlast) * stride, pol);
-        int4 v3 = ld_stream(p + min(3, jlast) * stride, pol);
-        for (int32_t j = 0; j < maxlen; j += 4) {
-          const bool more = j + 4 < maxlen;  // warp-uniform
-          take_cells<kSelMax>(v0, pr, hit, best);
-          if (more) v0 = ld_stream(p + min(j + 4, jlast) * stride, pol);
-          take_cells<kSelMax>(v1, pr, hit, best);
-          if (more) v1 = ld_stream(p + min(j + 5, jlast) * stride, pol);
-          take_cells<kSelMax>(v2, pr, hit, best);
-          if (more) v2 = ld_stream(p + min(j + 6, jlast) * stride, pol);
-          take_cells<kSelMax>(v3, pr, hit, best);
-          if (more) v3 = ld_stream(p + min(j + 7, jlast) * stride, pol);
-        }
-        if (kSelMax) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) hit |= uint32_t(best[q] >= 0) << q;
-        }
+        sweep_group<kSelMax, kEarly>(p, jlast, stride, maxlen, pr, pol, hit, best);
         // 32-bit row mask of the unit (rows 4*lg+q)
         uint32_t m = hit << (4 * lg);
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
@@ -498,6 +603,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
                              gmask, c_front);
       }
     }
+    };  // run_tasks
+    if (dense) run_tasks(std::true_type{});
+    else run_tasks(std::false_type{});
 
     // -- iteration counters: warp -> block -> grid --------------------------
 #pragma unroll
@@ -523,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(1, 4);
     const int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+    front_in = front;
     n_in = int32_t(*reinterpret_cast<volatile uint32_t*>(&a.task_out[rec]));
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const uint64_t t = globaltimer();
@@ -708,7 +817,9 @@ Geometry geometry32(const ssb_graph& g) {
     // summary over the whole id range (an upper bound for the tail), rest prefix
     const int64_t groups = (G.NW + (int64_t{1} << G.gshift) - 1) >> G.gshift;
     G.SW = int32_t(((groups + 31) / 32 + 3) / 4 * 4);
-    G.PW = int32_t(std::max<int64_t>(0, budget_words - G.SW) & ~int64_t(3));
+    // prefix: a multiple of one summary group (and of 4 words for uint4 staging)
+    const int64_t align = std::max<int64_t>(4, int64_t{1} << G.gshift);
+    G.PW = int32_t(std::max<int64_t>(0, budget_words - G.SW) / align * align);
   }
   G.smem = size_t(4 + G.PW + G.SW) * 4;  // + 4 zero words for padding cells
   return G;
@@ -894,6 +1005,11 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   a.tskip = g.plan.tskip.p;
   a.n_tasks = int32_t(g.plan.n_tasks);
   a.gone_base = 0;
+  a.front_in = 1;  // F_0 = {root}
+  {
+    const int div = std::max(1, env_int("SSB_DENSE_DIV", 4096));
+    a.dense_thr = std::max<int64_t>(1, g.n / div);
+  }
   a.n_chunks = int32_t(g.n_chunks);
   a.PW = G.PW;
   a.SW = G.SW;
@@ -977,6 +1093,7 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
     g.sc.sync();
     a.n_tasks = int32_t(outs.back());
     for (auto x : gones) a.gone_base += x;
+    a.front_in = rec[size_t(ran - 1) * kStatW];
     k += ran;
   }
   return false;

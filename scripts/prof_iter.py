@@ -1,0 +1,21 @@
+"""Run the first --iters BFS iterations of one root (S --scale) twice: the second
+launch is the one to profile (ncu -k regex:bfs32 -s 1 -c 1)."""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2010_09913_b200 as ssb
+ap = argparse.ArgumentParser()
+ap.add_argument("--scale", type=int, default=26)
+ap.add_argument("--root", type=int, default=2564265)
+ap.add_argument("--iters", type=int, default=1)
+ap.add_argument("--variant", type=int, default=3)
+ap.add_argument("--L", type=int, default=128)
+a = ap.parse_args()
+g = ssb.gen_kronecker(a.scale, 16, 1)
+r = ssb.build_slimsell(g, 32, g.num_vertices())
+del g
+db = ssb.DeviceBfs(r)
+o = ssb.BfsOptions(variant=ssb.Variant(a.variant), slimwork=True, slimchunk_len=a.L, max_iterations=a.iters)
+for _ in range(2):
+    k, ms, st, rc = db.run(a.root, o)
+    print(f"iters={k} device_ms={ms:.3f} kernel_ms={db.last_timing()[0]:.3f}",
+          [(s.iteration, round(s.elapsed_ns / 1e6, 3), s.columns_processed) for s in st])
