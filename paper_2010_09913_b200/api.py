@@ -316,7 +316,7 @@ def bfs_spmv(r: SlimSellRepr, root: int, opts: BfsOptions | None = None,
     parent = np.empty(max(n, 1), np.int64) if out_parent is None else out_parent
     plen = np.zeros(1, np.int64)
     iters = np.zeros(1, np.int64)
-    cap = min(max(n + 2, 2), 1 << 16)
+    cap = min(max(n + 2, 2), 1 << 12)  # deeper BFS: rerun below with an exact-size buffer
     while True:
         stats = (_L.IterStatsC * cap)()
         rc = _L.lib().ssb_bfs_spmv(r._h, int(root), C.byref(o), _p(dist), _p(parent), _p(plen),

@@ -740,15 +740,20 @@ __global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_
 // permute_out (repr.cpp:247-253) + selmax_parents (bfs.cpp:94-101): results in
 // original ids; sel-max positions decode through perm exactly like the
 // reference, including its root encoding when compat is on.
+// Gather form (one thread per ORIGINAL id, so the int64 outputs are written
+// coalesced — straight into pinned host memory over PCIe when the caller's
+// buffers allow it).
 __global__ void unpermute_kernel(const uint32_t* __restrict__ visited,
                                  const int32_t* __restrict__ level,
                                  const int32_t* __restrict__ parent,
-                                 const int32_t* __restrict__ perm, int64_t n, int selmax_parents,
-                                 int64_t* __restrict__ dist, int64_t* __restrict__ par) {
-  GRID_STRIDE(p, n) {
+                                 const int32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ inv_perm, int64_t n,
+                                 int selmax_parents, int64_t* __restrict__ dist,
+                                 int64_t* __restrict__ par) {
+  GRID_STRIDE(o, n) {
+    const int32_t p = inv_perm[o];
     const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
-    const int32_t o = perm[p];
-    dist[o] = reached ? int64_t(level[p]) : INT64_MAX;
+    if (dist) dist[o] = reached ? int64_t(level[p]) : INT64_MAX;
     if (selmax_parents) par[o] = reached ? int64_t(perm[parent[p]]) : -1;
   }
 }
@@ -759,17 +764,18 @@ __global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t*
                                  const int32_t* __restrict__ cl, int64_t C,
                                  const uint32_t* __restrict__ visited,
                                  const int32_t* __restrict__ level,
-                                 const int32_t* __restrict__ perm, int64_t n,
+                                 const int32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ inv_perm, int64_t n,
                                  int64_t* __restrict__ par, int* __restrict__ bad) {
-  GRID_STRIDE(p, n) {
-    const int32_t o = perm[p];
+  GRID_STRIDE(o, n) {
+    const int32_t p = inv_perm[o];
     if (!((visited[p >> 5] >> (p & 31)) & 1u)) {
       par[o] = -1;
       continue;
     }
     const int32_t lv = level[p];
     if (lv == 0) {
-      par[o] = o;
+      par[o] = int64_t(o);
       continue;
     }
     const int64_t ch = p / C, lane = p % C;
@@ -1234,27 +1240,50 @@ void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
   if (!g.last_valid) fail(SSB_EINVAL, "no BFS result on this graph");
   cudaStream_t s = g.sc.s;
   const int64_t n = g.n;
+  if (n == 0) {
+    if (parent_len) *parent_len = 0;
+    return;
+  }
   BitRegions R = bit_regions(g, 0);  // visited is the first region for both engines
-  DevBuf<int64_t> dd(std::max<int64_t>(n, 1)), dp(std::max<int64_t>(n, 1));
   const bool sel = g.last_variant == SSB_SELMAX;
-  unpermute_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p, n,
-                                               sel && want_parents, dd.p, dp.p);
+  // Pinned (page-locked) host buffers are written by the kernels directly over
+  // PCIe; pageable ones go through a persistent device staging buffer.
+  auto direct = [](int64_t* h) -> int64_t* {
+    if (!h) return nullptr;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? static_cast<int64_t*>(at.devicePointer) : nullptr;
+  };
+  int64_t* dd = direct(dist);
+  int64_t* dp = want_parents ? direct(parent) : nullptr;
+  if ((dist && !dd) || (want_parents && parent && !dp)) g.stage.ensure(size_t(2 * n));
+  int64_t* d_out = dd ? dd : (dist ? g.stage.p : nullptr);
+  int64_t* p_out = dp ? dp : (want_parents && parent ? g.stage.p + n : nullptr);
+  unpermute_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
+                                               g.inv_perm.p, n, sel && p_out != nullptr, d_out,
+                                               p_out);
   SSB_CUDA(cudaGetLastError());
   int64_t plen = 0;
   if (want_parents && !sel) {
-    DevBuf<int> bad(1);
-    SSB_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
-    dp_parent_kernel<<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
-                                                 g.level.p, g.perm.p, n, dp.p, bad.p);
+    g.flag.ensure(1);
+    SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, 4, s));
+    if (p_out)
+      dp_parent_kernel<<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
+                                                   g.level.p, g.perm.p, g.inv_perm.p, n, p_out,
+                                                   g.flag.p);
     SSB_CUDA(cudaGetLastError());
     int hbad = 0;
-    SSB_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
     g.sc.sync();
     if (hbad) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
   }
   if (want_parents) plen = n;
-  if (dist) SSB_CUDA(cudaMemcpyAsync(dist, dd.p, 8 * n, cudaMemcpyDeviceToHost, s));
-  if (parent && plen) SSB_CUDA(cudaMemcpyAsync(parent, dp.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (dist && !dd) SSB_CUDA(cudaMemcpyAsync(dist, d_out, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (parent && plen && !dp)
+    SSB_CUDA(cudaMemcpyAsync(parent, p_out, 8 * n, cudaMemcpyDeviceToHost, s));
   g.sc.sync();
   if (parent_len) *parent_len = plen;
 }

@@ -138,6 +138,8 @@ struct ssb_graph {
   ssb::DevBuf<int64_t> dstats;    // per-iteration counters
   ssb::DevBuf<uint32_t> dctrl;    // task counters + control words
   ssb::DevBuf<uint8_t> gbytes;    // generic engine: skip flags / frontier bytes
+  ssb::DevBuf<int64_t> stage;     // fetch staging for pageable host outputs (2n)
+  ssb::DevBuf<int> flag;          // small device flag
   ssb_bfs_plan plan;
 
   // Last BFS (device-resident result).
