@@ -98,7 +98,8 @@ def profiled_traffic():
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("workload")
+        return d.get("dram_bytes_per_launch"), (f"{d.get('workload')}; algorithmic bytes of that launch "
+                                                f"{d.get('algorithmic_bytes_same_launch')}; {d.get('source')}")
     except Exception:
         return None, None
 

@@ -18,4 +18,4 @@ o = ssb.BfsOptions(variant=ssb.Variant(a.variant), slimwork=True, slimchunk_len=
 for _ in range(2):
     k, ms, st, rc = db.run(a.root, o)
     print(f"iters={k} device_ms={ms:.3f} kernel_ms={db.last_timing()[0]:.3f}",
-          [(s.iteration, round(s.elapsed_ns / 1e6, 3), s.columns_processed) for s in st])
+          [(s.iteration, round(s.elapsed_ns / 1e6, 3), s.columns_processed, s.frontier_size) for s in st])

@@ -283,3 +283,32 @@ def test_errors(ssb):
         res = ssb.bfs_spmv(ssb.build_slimsell(g, C_, 3), 2, opts(ssb, 3))
         assert res.iterations == 1 and res.dist.tolist() == [KINF, KINF, 0]
         assert res.parent.tolist() == [-1, -1, 2]
+
+
+@pytest.mark.parametrize("mode_env", [
+    {"SSB_DENSE_DIV": "1000000000"},   # always the sparse sweep
+    {"SSB_DENSE_DIV": "1"},            # early-exit sweeps whenever |F| > 1
+    {"SSB_DENSE_DIV": "4096"},         # the default switch point
+])
+def test_sweep_modes_with_small_shared_image(ssb, port, monkeypatch, mode_env):
+    """Both sweep modes (sparse / early-exit) with a tiny shared-memory
+    image, so the prefix + summary split and the tail paths are exercised at
+    small scale, against the oracle (all semirings, SlimWork, SlimChunk)."""
+    monkeypatch.setenv("SSB_SMEM_KB", "2")
+    for k_, v_ in mode_env.items():
+        monkeypatch.setenv(k_, v_)
+    n, uv = port.gen_kronecker(14, 16, 9)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    csr = ssb.to_csr(g)
+    r = ssb.build_slimsell(g, 32, n)
+    L = port.build_slimsell(n, row, col, 32, n)
+    for root in (0, 3, 777, 9000):
+        for v in range(4):
+            for sw, Lc in ((True, 16), (False, 0), (True, 0)):
+                a = ssb.bfs_spmv(r, root, opts(ssb, v, sw, Lc), csr)
+                b = port.bfs_spmv(L, root, v, sw, Lc, csr=(row, col))
+                key = (root, v, sw, Lc)
+                assert np.array_equal(a.dist, b.dist), key
+                assert np.array_equal(a.parent, b.parent), key
+                assert dev_rows(a) == port_rows(b.stats), key
