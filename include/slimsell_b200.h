@@ -146,6 +146,21 @@ int ssb_bfs_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent
 /* Timing of the last ssb_bfs_run: CUDA-event time of the main BFS kernel
  * launches alone (kernel_ms) and how many kernels the BFS launched. */
 int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches);
+/* ---- multi-GPU: chunk-range shards -------------------
+ * Each rank builds (or holds) the layout, owns chunks [chunk_begin, chunk_end)
+ * (C = 32: chunk i <-> frontier word i) and the replicated 1-bit frontier.
+ * Per BFS iteration: ssb_bfs_shard_step sweeps the owned chunks and copies the
+ * owned frontier words (chunk_end - chunk_begin uint32, device memory) to
+ * owned_words; the caller all-gathers them (NCCL) into the full n_chunks-word
+ * frontier and sums |newly| over ranks; ssb_bfs_shard_exchange installs it.
+ * Stop after the iteration whose global newly count is 0 (is_converged,
+ * semiring.cpp:152-157). ssb_bfs_shard_fetch writes dist/parent (original
+ * ids) of the owned rows only; other entries of the host arrays are kept. */
+int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
+                        int64_t chunk_begin, int64_t chunk_end);
+int ssb_bfs_shard_step(ssb_graph* g, ssb_iter_stats* local, uint32_t* owned_words);
+int ssb_bfs_shard_exchange(ssb_graph* g, const uint32_t* frontier_words, int64_t newly_total);
+int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent);
 /* m_cc of the last run: Σ_{reached v} deg(v) / 2 (the GTEPS numerator). */
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc);
 

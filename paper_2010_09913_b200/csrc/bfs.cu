@@ -740,6 +740,22 @@ __global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_
 // permute_out (repr.cpp:247-253) + selmax_parents (bfs.cpp:94-101): results in
 // original ids; sel-max positions decode through perm exactly like the
 // reference, including its root encoding when compat is on.
+// Summary of a full frontier bitmap (after a shard exchange): bit t of the
+// summary <-> frontier words [PW + 8t, PW + 8t + 8) hold a set bit.
+__global__ void summary_from_words_kernel(const uint32_t* __restrict__ F, int64_t PW, int64_t NW,
+                                          uint32_t* __restrict__ S, int64_t SW, int gshift) {
+  GRID_STRIDE(sw, SW) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t w0 = PW + ((sw * 32 + b) << gshift);
+      uint32_t any = 0;
+      for (int64_t w = w0; w < w0 + (int64_t{1} << gshift) && w < NW; ++w) any |= F[w];
+      bits |= uint32_t(any != 0) << b;
+    }
+    S[sw] = bits;
+  }
+}
+
 // Gather form (one thread per ORIGINAL id, so the int64 outputs are written
 // coalesced — straight into pinned host memory over PCIe when the caller's
 // buffers allow it).
@@ -749,9 +765,10 @@ __global__ void unpermute_kernel(const uint32_t* __restrict__ visited,
                                  const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ inv_perm, int64_t n,
                                  int selmax_parents, int64_t* __restrict__ dist,
-                                 int64_t* __restrict__ par) {
+                                 int64_t* __restrict__ par, int64_t pb, int64_t pe) {
   GRID_STRIDE(o, n) {
     const int32_t p = inv_perm[o];
+    if (p < pb || p >= pe) continue;  // another shard's row
     const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
     if (dist) dist[o] = reached ? int64_t(level[p]) : INT64_MAX;
     if (selmax_parents) par[o] = reached ? int64_t(perm[parent[p]]) : -1;
@@ -766,9 +783,11 @@ __global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t*
                                  const int32_t* __restrict__ level,
                                  const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ inv_perm, int64_t n,
-                                 int64_t* __restrict__ par, int* __restrict__ bad) {
+                                 int64_t* __restrict__ par, int* __restrict__ bad, int64_t pb,
+                                 int64_t pe) {
   GRID_STRIDE(o, n) {
     const int32_t p = inv_perm[o];
+    if (p < pb || p >= pe) continue;  // another shard's row
     if (!((visited[p >> 5] >> (p & 31)) & 1u)) {
       par[o] = -1;
       continue;
@@ -835,14 +854,14 @@ Geometry geometry32(const ssb_graph& g) {
 // most L columns (the whole chunk when L <= 0, as the reference's task list,
 // bfs.cpp:122-138); a task groups up to 32 consecutive units whose cost stays
 // under a budget, the grain of the dynamic scheduler.
-void build_plan32(ssb_graph& g, int64_t L) {
+void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
   ssb_bfs_plan& P = g.plan;
-  if (P.L == L && P.n_units > 0) return;
+  if (P.L == L && P.cb == cb && P.ce == ce && P.built) return;
   std::vector<ssb_unit> units;
   std::vector<int32_t> split_units;
-  units.reserve(g.n_chunks + 16);
+  units.reserve(ce - cb + 16);
   P.empty_chunks = 0;
-  for (int64_t i = 0; i < g.n_chunks; ++i) {
+  for (int64_t i = cb; i < ce; ++i) {
     const int64_t cl = g.cl_host[i];
     if (cl == 0) {
       // Chunks without cells (all rows isolated; 1.07M of 2.1M at S26) can
@@ -878,6 +897,9 @@ void build_plan32(ssb_graph& g, int64_t L) {
   if (units.size() >= size_t(INT32_MAX)) fail(SSB_EINVAL, "too many work units");
   cudaStream_t s = g.sc.s;
   P.L = L;
+  P.cb = cb;
+  P.ce = ce;
+  P.built = true;
   P.n_units = int64_t(units.size());
   P.n_tasks = int64_t(tb.size()) - 1;
   P.n_split = int64_t(split_units.size());
@@ -950,13 +972,36 @@ void configure32(size_t dyn_smem) {
                                 int(dyn_smem)));
 }
 
-// Returns true when converged; appends per-iteration stats.
-bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
-           int64_t cap, std::vector<ssb_iter_stats>& stats) {
+// One C=32 BFS in flight: the kernel arguments and the host-side carry between
+// cooperative launches. A full BFS is one launch (or several when it is deeper
+// than kItersPerLaunch); a shard of a multi-GPU BFS is stepped one iteration
+// per launch with a frontier exchange in between (ssb_bfs_shard_*).
+struct Run32 {
+  Args32 a;
+  Geometry G;
+  bool sel = false;
+  int grid = 0;
+  int64_t k = 1;                 // next iteration
+  int32_t root_pos = 0;
+  bool z_skip = false;           // SlimWork skips the root's cell-less chunk
+  uint32_t* task_out = nullptr;
+  unsigned long long* gone = nullptr;
+  std::vector<int64_t> rec;
+  bool stepping = false;         // shard mode: always carry state to the next launch
+  int64_t cb = 0, ce = 0;        // owned chunk range
+};
+
+// init_state (semiring.cpp:56-88) in 1-bit form + kernel arguments for the
+// chunk range [cb, ce) (all chunks for a single-GPU BFS).
+Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
+                int64_t cb, int64_t ce) {
   cudaStream_t s = g.sc.s;
-  const bool sel = o.variant == SSB_SELMAX;
-  build_plan32(g, o.slimchunk_len);
-  const Geometry G = geometry32(g);
+  Run32 r;
+  r.sel = o.variant == SSB_SELMAX;
+  r.root_pos = root_pos;
+  build_plan32(g, o.slimchunk_len, cb, ce);
+  r.G = geometry32(g);
+  const Geometry& G = r.G;
   BitRegions R = bit_regions(g, G.SW);
   g.level.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
   g.parent.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
@@ -964,10 +1009,9 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   // control words: task_ctr [K] | task_out [K] | gone_chunks [K] (8-byte)
   g.dctrl.ensure(size_t(kItersPerLaunch) * 4);
   uint32_t* task_ctr = g.dctrl.p;
-  uint32_t* task_out = task_ctr + kItersPerLaunch;
-  auto* gone = reinterpret_cast<unsigned long long*>(task_out + kItersPerLaunch);
+  r.task_out = task_ctr + kItersPerLaunch;
+  r.gone = reinterpret_cast<unsigned long long*>(r.task_out + kItersPerLaunch);
 
-  // init_state (semiring.cpp:56-88) in 1-bit form
   SSB_CUDA(cudaMemsetAsync(R.visited, 0, size_t(R.NW4) * 4 * 2, s));  // visited + F0
   SSB_CUDA(cudaMemsetAsync(R.S0, 0, size_t(R.SW4) * 4 * 3, s));
   SSB_CUDA(cudaMemsetAsync(g.plan.tskip.p, 0, g.plan.tskip.bytes(), s));
@@ -976,15 +1020,15 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   SSB_CUDA(cudaGetLastError());
   g.last_launches += 1;  // set_root_kernel
 
-  if (sel) configure32<true>(G.smem); else configure32<false>(G.smem);
+  if (r.sel) configure32<true>(G.smem); else configure32<false>(G.smem);
   int per_sm = 0;
   SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, kThreads,
-      G.smem));
+      &per_sm, r.sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>,
+      kThreads, G.smem));
   if (per_sm < 1) fail(SSB_ECUDA, "bfs32 kernel does not fit on an SM");
-  const int grid = num_sms();
+  r.grid = num_sms();
 
-  Args32 a;
+  Args32& a = r.a;
   a.col = g.col.p;
   a.cs = g.cs.p;
   a.cl = g.cl.p;
@@ -1004,8 +1048,8 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
   a.parent = g.parent.p;
   a.stats = g.dstats.p;
   a.task_ctr = task_ctr;
-  a.task_out = task_out;
-  a.gone_chunks = gone;
+  a.task_out = r.task_out;
+  a.gone_chunks = r.gone;
   a.tlist0 = g.plan.tlist.p;
   a.tlist1 = g.plan.tlist.p + g.plan.n_tasks;
   a.tskip = g.plan.tskip.p;
@@ -1034,73 +1078,93 @@ bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_opti
     const int64_t real_last = g.n - (g.n_chunks - 1) * 32;  // 1..32
     a.last_real = real_last >= 32 ? 0xffffffffu : ((1u << real_last) - 1u);
   }
-  std::vector<int64_t> rec(size_t(kItersPerLaunch) * kStatW);
-  int64_t k = 1;
-  while (k <= cap) {
-    const int64_t kend = std::min<int64_t>(cap + 1, k + kItersPerLaunch);
-    a.k_begin = int32_t(k);
-    a.k_end = int32_t(kend);
-    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, g.dstats.bytes(), s));
-    SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
-    void* params[] = {&a};
-    SSB_CUDA(cudaEventRecord(g.sc.e0, s));
-    SSB_CUDA(cudaLaunchCooperativeKernel(
-        sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, dim3(grid),
-        dim3(kThreads), params, G.smem, s));
-    SSB_CUDA(cudaGetLastError());
-    SSB_CUDA(cudaEventRecord(g.sc.e1, s));
-    if (a.trace) {  // debug: poll progress instead of blocking forever
-      cudaEvent_t done;
-      SSB_CUDA(cudaEventCreate(&done));
-      SSB_CUDA(cudaEventRecord(done, s));
-      for (int spin = 0; cudaEventQuery(done) == cudaErrorNotReady; ++spin) {
-        if (spin % 1000 == 999)
-          fprintf(stderr, "[ssb trace] k=%d phase=%d arrived=%d\n", a.trace[0], a.trace[1], a.trace[2]);
-        if (spin > 10000) { fprintf(stderr, "[ssb trace] giving up\n"); std::abort(); }
-        usleep(1000);
-      }
-      cudaEventDestroy(done);
+  // chunks without cells are processed (0 columns, 0 segments) unless SlimWork
+  // skips the root's own chunk when the root is its only real row
+  const int64_t rc = root_pos / 32;
+  r.z_skip = o.slimwork && rc >= cb && rc < ce && g.cl_host[rc] == 0 &&
+             std::min<int64_t>(32, g.n - rc * 32) == 1;
+  r.rec.resize(size_t(kItersPerLaunch) * kStatW);
+  r.k = 1;
+  return r;
+}
+
+// Runs iterations r.k .. kend-1 (stopping early when no row is newly reached
+// in this launch's range); appends their stats. Returns the number run.
+int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stats>& stats,
+                 bool& conv) {
+  cudaStream_t s = g.sc.s;
+  Args32& a = r.a;
+  a.k_begin = int32_t(r.k);
+  a.k_end = int32_t(kend);
+  SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, g.dstats.bytes(), s));
+  SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
+  void* params[] = {&a};
+  SSB_CUDA(cudaEventRecord(g.sc.e0, s));
+  SSB_CUDA(cudaLaunchCooperativeKernel(
+      r.sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, dim3(r.grid),
+      dim3(kThreads), params, r.G.smem, s));
+  SSB_CUDA(cudaGetLastError());
+  SSB_CUDA(cudaEventRecord(g.sc.e1, s));
+  if (a.trace) {  // debug: poll progress instead of blocking forever
+    cudaEvent_t done;
+    SSB_CUDA(cudaEventCreate(&done));
+    SSB_CUDA(cudaEventRecord(done, s));
+    for (int spin = 0; cudaEventQuery(done) == cudaErrorNotReady; ++spin) {
+      if (spin % 1000 == 999)
+        fprintf(stderr, "[ssb trace] k=%d phase=%d arrived=%d\n", a.trace[0], a.trace[1], a.trace[2]);
+      if (spin > 10000) { fprintf(stderr, "[ssb trace] giving up\n"); std::abort(); }
+      usleep(1000);
     }
-    SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, rec.size() * 8, cudaMemcpyDeviceToHost, s));
-    g.sc.sync();
-    {
-      float kms = 0;
-      SSB_CUDA(cudaEventElapsedTime(&kms, g.sc.e0, g.sc.e1));
-      g.last_kernel_ms += kms;
-      g.last_launches += 1;  // bfs32_kernel
+    cudaEventDestroy(done);
+  }
+  SSB_CUDA(cudaMemcpyAsync(r.rec.data(), g.dstats.p, r.rec.size() * 8, cudaMemcpyDeviceToHost, s));
+  g.sc.sync();
+  {
+    float kms = 0;
+    SSB_CUDA(cudaEventElapsedTime(&kms, g.sc.e0, g.sc.e1));
+    g.last_kernel_ms += kms;
+    g.last_launches += 1;  // bfs32_kernel
+  }
+  // the launch ran iterations k .. until a record with frontier 0 or kend
+  int64_t ran = 0;
+  conv = false;
+  for (int64_t i = 0; i < kend - r.k; ++i) {
+    ++ran;
+    if (r.rec[size_t(i) * kStatW] == 0) {
+      conv = true;
+      break;
     }
-    // the launch ran iterations k .. until a record with frontier 0 or kend
-    int64_t ran = 0;
+  }
+  collect_stats(r.rec, r.k, ran, stats);
+  for (size_t i = stats.size() - size_t(ran); i < stats.size(); ++i) {
+    stats[i].chunks_processed += g.plan.empty_chunks - (r.z_skip ? 1 : 0);
+    stats[i].chunks_skipped += r.z_skip ? 1 : 0;
+  }
+  if (conv && !r.stepping) {
+    r.k += ran;
+    return ran;
+  }
+  // carry the active task list and the retired-chunk count into the next launch
+  std::vector<uint32_t> outs(static_cast<size_t>(ran));
+  std::vector<unsigned long long> gones(static_cast<size_t>(ran));
+  SSB_CUDA(cudaMemcpyAsync(outs.data(), r.task_out, 4 * ran, cudaMemcpyDeviceToHost, s));
+  SSB_CUDA(cudaMemcpyAsync(gones.data(), r.gone, 8 * ran, cudaMemcpyDeviceToHost, s));
+  g.sc.sync();
+  a.n_tasks = int32_t(outs.back());
+  for (auto x : gones) a.gone_base += x;
+  a.front_in = r.rec[size_t(ran - 1) * kStatW];
+  r.k += ran;
+  return ran;
+}
+
+// Returns true when converged; appends per-iteration stats.
+bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
+           int64_t cap, std::vector<ssb_iter_stats>& stats) {
+  Run32 r = prepare32(g, root_pos, root_code, o, 0, g.n_chunks);
+  while (r.k <= cap) {
     bool conv = false;
-    for (int64_t i = 0; i < kend - k; ++i) {
-      ++ran;
-      if (rec[size_t(i) * kStatW] == 0) {
-        conv = true;
-        break;
-      }
-    }
-    collect_stats(rec, k, ran, stats);
-    {
-      // chunks without cells: processed (0 columns, 0 segments) unless SlimWork
-      // skips the root's own chunk when the root is its only real row
-      const int64_t rc = root_pos / 32;
-      const bool z_skip = o.slimwork && g.cl_host[rc] == 0 && std::min<int64_t>(32, g.n - rc * 32) == 1;
-      for (size_t i = stats.size() - size_t(ran); i < stats.size(); ++i) {
-        stats[i].chunks_processed += g.plan.empty_chunks - (z_skip ? 1 : 0);
-        stats[i].chunks_skipped += z_skip ? 1 : 0;
-      }
-    }
+    launch32(g, r, std::min<int64_t>(cap + 1, r.k + kItersPerLaunch), stats, conv);
     if (conv) return true;
-    // carry the active task list and the retired-chunk count into the next launch
-    std::vector<uint32_t> outs(static_cast<size_t>(ran));
-    std::vector<unsigned long long> gones(static_cast<size_t>(ran));
-    SSB_CUDA(cudaMemcpyAsync(outs.data(), task_out, 4 * ran, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaMemcpyAsync(gones.data(), gone, 8 * ran, cudaMemcpyDeviceToHost, s));
-    g.sc.sync();
-    a.n_tasks = int32_t(outs.back());
-    for (auto x : gones) a.gone_base += x;
-    a.front_in = rec[size_t(ran - 1) * kStatW];
-    k += ran;
   }
   return false;
 }
@@ -1235,8 +1299,17 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
   return conv ? SSB_OK : SSB_ECAP;
 }
 
+void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
+                int64_t* parent_len, int64_t pb, int64_t pe);
+
 void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
                int64_t* parent_len) {
+  fetch_rows(g, want_parents, dist, parent, parent_len, 0, g.n_padded);
+}
+
+// Results of the rows at positions [pb, pe) only (a shard), original ids.
+void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
+                int64_t* parent_len, int64_t pb, int64_t pe) {
   if (!g.last_valid) fail(SSB_EINVAL, "no BFS result on this graph");
   cudaStream_t s = g.sc.s;
   const int64_t n = g.n;
@@ -1262,9 +1335,14 @@ void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
   if ((dist && !dd) || (want_parents && parent && !dp)) g.stage.ensure(size_t(2 * n));
   int64_t* d_out = dd ? dd : (dist ? g.stage.p : nullptr);
   int64_t* p_out = dp ? dp : (want_parents && parent ? g.stage.p + n : nullptr);
+  const bool partial = pb > 0 || pe < g.n_padded;  // a shard: keep the caller's other rows
+  if (partial && dist && !dd)
+    SSB_CUDA(cudaMemcpyAsync(d_out, dist, 8 * n, cudaMemcpyHostToDevice, s));
+  if (partial && p_out && !dp)
+    SSB_CUDA(cudaMemcpyAsync(p_out, parent, 8 * n, cudaMemcpyHostToDevice, s));
   unpermute_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
                                                g.inv_perm.p, n, sel && p_out != nullptr, d_out,
-                                               p_out);
+                                               p_out, pb, pe);
   SSB_CUDA(cudaGetLastError());
   int64_t plen = 0;
   if (want_parents && !sel) {
@@ -1273,7 +1351,7 @@ void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
     if (p_out)
       dp_parent_kernel<<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
                                                    g.level.p, g.perm.p, g.inv_perm.p, n, p_out,
-                                                   g.flag.p);
+                                                   g.flag.p, pb, pe);
     SSB_CUDA(cudaGetLastError());
     int hbad = 0;
     SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
@@ -1286,6 +1364,87 @@ void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
     SSB_CUDA(cudaMemcpyAsync(parent, p_out, 8 * n, cudaMemcpyDeviceToHost, s));
   g.sc.sync();
   if (parent_len) *parent_len = plen;
+}
+
+// ---- chunk-range shards of a multi-GPU BFS ---------------
+// Each rank owns chunks [cb, ce) and the replicated 1-bit frontier. One
+// iteration = shard_step (this rank's sweep, its owned frontier words copied
+// out) -> the caller all-gathers every rank's words -> shard_exchange (the
+// full frontier installed, the summary rebuilt, |F| made global).
+struct ShardState {
+  Run32 r;
+  ssb_bfs_options o;
+  std::vector<ssb_iter_stats> stats;
+};
+
+void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t cb, int64_t ce) {
+  if (g.C != 32) fail(SSB_EINVAL, "sharded BFS needs the C = 32 layout");
+  if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
+  if (cb < 0 || ce > g.n_chunks || cb > ce) fail(SSB_EINVAL, "chunk range out of bounds");
+  if (root < 0 || root >= g.n)
+    fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g.n) + ")");
+  int32_t root_pos = 0;
+  SSB_CUDA(cudaMemcpy(&root_pos, g.inv_perm.p + root, 4, cudaMemcpyDeviceToHost));
+  const int32_t root_code =
+      (o.variant == SSB_SELMAX && o.selmax_compat) ? int32_t(root) : root_pos;
+  auto st = std::make_shared<ShardState>();
+  g.last_kernel_ms = 0;
+  g.last_launches = 0;
+  st->r = prepare32(g, root_pos, root_code, o, cb, ce);
+  st->r.stepping = true;
+  st->r.cb = cb;
+  st->r.ce = ce;
+  st->o = o;
+  g.shard = st;
+  g.last_root = root;
+  g.last_variant = o.variant;
+  g.last_compat = o.selmax_compat;
+  g.last_valid = false;
+}
+
+void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st) fail(SSB_EINVAL, "no sharded BFS in progress (ssb_bfs_shard_begin)");
+  Run32& r = st->r;
+  const int64_t k = r.k;
+  std::vector<ssb_iter_stats> one;
+  bool conv = false;
+  launch32(g, r, k + 1, one, conv);
+  if (local) *local = one.front();
+  st->stats.push_back(one.front());
+  const uint32_t* Fn = (k & 1) ? r.a.F1 : r.a.F0;
+  if (owned_words && r.ce > r.cb)
+    SSB_CUDA(cudaMemcpyAsync(owned_words, Fn + r.cb, 4 * (r.ce - r.cb), cudaMemcpyDeviceToDevice,
+                             g.sc.s));
+  g.sc.sync();
+}
+
+void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st) fail(SSB_EINVAL, "no sharded BFS in progress (ssb_bfs_shard_begin)");
+  Run32& r = st->r;
+  const int64_t k = r.k - 1;  // the iteration just stepped
+  cudaStream_t s = g.sc.s;
+  uint32_t* Fn = (k & 1) ? r.a.F1 : r.a.F0;
+  if (!frontier_words) fail(SSB_EINVAL, "frontier_words is NULL");
+  SSB_CUDA(cudaMemcpyAsync(Fn, frontier_words, 4 * g.n_chunks, cudaMemcpyDeviceToDevice, s));
+  if (r.G.SW > 0) {
+    uint32_t* Sn = (k % 3) == 0 ? r.a.S0 : ((k % 3) == 1 ? r.a.S1 : r.a.S2);
+    summary_from_words_kernel<<<grid_for(r.G.SW), 256, 0, s>>>(Fn, r.G.PW, g.n_chunks, Sn, r.G.SW,
+                                                               r.G.gshift);
+    SSB_CUDA(cudaGetLastError());
+  }
+  r.a.front_in = newly_total;
+  g.sc.sync();
+  g.last_iterations = int64_t(st->stats.size());
+  g.last_valid = true;  // results of the owned rows can be fetched at any point
+}
+
+void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st) fail(SSB_EINVAL, "no sharded BFS (ssb_bfs_shard_begin)");
+  g.last_valid = true;
+  fetch_rows(g, want_parents, dist, parent, nullptr, st->r.cb * 32, st->r.ce * 32);
 }
 
 int64_t bfs_edges_traversed(ssb_graph& g) {

@@ -246,6 +246,36 @@ int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches) {
   });
 }
 
+int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
+                        int64_t chunk_begin, int64_t chunk_end) {
+  return guarded([&] {
+    need(g, "graph");
+    need(opts, "opts");
+    ssb::shard_begin(*g, root, *opts, chunk_begin, chunk_end);
+  });
+}
+
+int ssb_bfs_shard_step(ssb_graph* g, ssb_iter_stats* local, uint32_t* owned_words) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::shard_step(*g, local, owned_words);
+  });
+}
+
+int ssb_bfs_shard_exchange(ssb_graph* g, const uint32_t* frontier_words, int64_t newly_total) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::shard_exchange(*g, frontier_words, newly_total);
+  });
+}
+
+int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::shard_fetch(*g, want_parents, dist, parent);
+  });
+}
+
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc) {
   return guarded([&] {
     need(g, "graph");

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -109,6 +110,8 @@ struct ssb_bfs_plan {  // cached per slimchunk_len
   int64_t n_tasks = 0;
   int64_t n_split = 0;
   int64_t empty_chunks = 0;  // chunks with cl == 0 (no unit)
+  int64_t cb = 0, ce = 0;    // chunk range the plan covers (a shard, or all)
+  bool built = false;
   ssb::DevBuf<ssb_unit> units;
   ssb::DevBuf<int32_t> task_begin;    // n_tasks + 1
   ssb::DevBuf<int32_t> split_units;   // units per split chunk
@@ -150,6 +153,7 @@ struct ssb_graph {
   bool last_valid = false;
   double last_kernel_ms = 0;  // CUDA-event time of the main BFS kernel launches
   int64_t last_launches = 0;  // kernels launched by the last BFS
+  std::shared_ptr<void> shard;  // state of a sharded (multi-GPU) BFS in progress
 
   ssb::StreamCtx sc;
 };
@@ -173,4 +177,8 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
 void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
                int64_t* parent_len);
 int64_t bfs_edges_traversed(ssb_graph& g);
+void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t cb, int64_t ce);
+void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);
+void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total);
+void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent);
 }  // namespace ssb

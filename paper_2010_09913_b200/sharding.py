@@ -93,3 +93,127 @@ class ShardedFrontierExchange:
             frontier[rb:re] = gathered[r * self.slot: r * self.slot + (re - rb)]
         newly = int(np.unpackbits(frontier.view(np.uint8)).sum())
         return ExchangeResult(frontier, newly > 0, newly)
+
+
+# ---- the device path of chunk-range sharding --------------------------------
+
+class DeviceShard:
+    """One rank's shard of a sharded BFS: a device SlimSellRepr (the whole
+    layout; this rank sweeps chunks [cb, ce)) driven through the C-ABI
+    ssb_bfs_shard_* calls."""
+
+    def __init__(self, r, cb: int, ce: int):
+        import torch
+
+        self.r, self.cb, self.ce = r, int(cb), int(ce)
+        self.owned = torch.zeros(max(self.ce - self.cb, 1), dtype=torch.int32, device="cuda")
+
+    def begin(self, root: int, opts) -> None:
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        o = opts._c()
+        _check(L.lib().ssb_bfs_shard_begin(self.r._h, int(root), C.byref(o), self.cb, self.ce))
+
+    def step(self):
+        """One iteration over the owned chunks: (local IterStats, owned words)."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import IterStats, _check
+        st = L.IterStatsC()
+        _check(L.lib().ssb_bfs_shard_step(self.r._h, C.byref(st), C.c_void_p(self.owned.data_ptr())))
+        s = IterStats(st.iteration, st.elapsed_ns, st.chunks_processed, st.chunks_skipped,
+                      st.subchunks_processed, st.columns_processed, st.frontier_size)
+        return s, self.owned[: self.ce - self.cb]
+
+    def exchange(self, full_words, newly_total: int) -> None:
+        import ctypes as C
+
+        import torch
+
+        from . import _lib as L
+        from .api import _check
+        torch.cuda.current_stream().synchronize()
+        _check(L.lib().ssb_bfs_shard_exchange(self.r._h, C.c_void_p(full_words.data_ptr()),
+                                              int(newly_total)))
+
+    def fetch(self, want_parents: bool, dist: np.ndarray, parent: np.ndarray) -> None:
+        from . import _lib as L
+        from .api import _check, _p
+        _check(L.lib().ssb_bfs_shard_fetch(self.r._h, int(want_parents), _p(dist), _p(parent)))
+
+
+class LocalComm:
+    """Every shard lives in this process (one GPU emulating several ranks):
+    the all-gather is a concatenation in rank order, reductions are sums."""
+
+    def allgather_frontier(self, owned_list):
+        import torch
+        return torch.cat(list(owned_list)).contiguous()
+
+    def allreduce_sum(self, arrays):
+        return np.sum(np.stack(arrays), axis=0)
+
+
+class TorchComm:
+    """One shard per process over torch.distributed (NCCL on B200s): a padded
+    all_gather_into_tensor of the owned frontier words, all_reduce for the
+    counters."""
+
+    def __init__(self, ranges, group=None):
+        self.ranges = ranges
+        self.group = group
+        self.slot = max(1, max(e - b for b, e in ranges))
+
+    def allgather_frontier(self, owned_list):
+        import torch
+        import torch.distributed as dist
+        (owned,) = owned_list
+        send = torch.zeros(self.slot, dtype=torch.int32, device=owned.device)
+        send[: owned.shape[0]] = owned
+        recv = torch.empty(self.slot * len(self.ranges), dtype=torch.int32, device=owned.device)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        return torch.cat([recv[r * self.slot: r * self.slot + (e - b)]
+                          for r, (b, e) in enumerate(self.ranges)]).contiguous()
+
+    def allreduce_sum(self, arrays):
+        import torch
+        import torch.distributed as dist
+        (a,) = arrays
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).cuda()
+        dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+
+def run_sharded_bfs(shards, comm, root: int, opts, max_iterations: int = 0):
+    """A BFS over chunk-range shards: per iteration every shard sweeps its
+    chunks, the owned frontier words are all-gathered, |newly| is summed, and
+    the full frontier is installed on every shard. Returns (dist, parent,
+    per_iter) — dist/parent of the rows this process owns (other rows hold the
+    sentinels KINF / -1) and the global per-iteration counters."""
+    from .api import IterStats, KINF
+    for sh in shards:
+        sh.begin(root, opts)
+    n = shards[0].r.n
+    cap = max_iterations if max_iterations > 0 else n + 1
+    per_iter = []
+    for k in range(1, cap + 1):
+        locals_, owned = zip(*[sh.step() for sh in shards])
+        counts = comm.allreduce_sum([np.array([s.chunks_processed, s.chunks_skipped,
+                                               s.subchunks_processed, s.columns_processed,
+                                               s.frontier_size, s.elapsed_ns], dtype=np.int64)
+                                     for s in locals_])
+        full = comm.allgather_frontier(owned)
+        for sh in shards:
+            sh.exchange(full, int(counts[4]))
+        per_iter.append(IterStats(k, int(counts[5]), *[int(x) for x in counts[:5]]))
+        if counts[4] == 0:
+            break
+    dist = np.full(n, KINF, dtype=np.int64)
+    parent = np.full(n, -1, dtype=np.int64)
+    want = bool(opts.want_parents) and int(opts.variant) == 3
+    for sh in shards:
+        sh.fetch(want, dist, parent)
+    return dist, (parent if want else parent[:0]), per_iter

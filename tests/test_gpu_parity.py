@@ -312,3 +312,29 @@ def test_sweep_modes_with_small_shared_image(ssb, port, monkeypatch, mode_env):
                 assert np.array_equal(a.dist, b.dist), key
                 assert np.array_equal(a.parent, b.parent), key
                 assert dev_rows(a) == port_rows(b.stats), key
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_chunk_sharded_device_bfs_matches_single_gpu(ssb, port, monkeypatch, world):
+    """The multi-GPU decomposition (chunk-range shards + per-iteration frontier
+    all-gather) run with `world` shards emulated on one GPU — separate device
+    layouts and workspaces, stepped in lockstep, the all-gather done in-process
+    — equals the reference (oracle) in dist, sel-max parents and counters."""
+    from paper_2010_09913_b200.sharding import DeviceShard, LocalComm, partition_chunks, run_sharded_bfs
+    monkeypatch.setenv("SSB_SMEM_KB", "4")  # exercise prefix + summary + exact lookups
+    n, uv = port.gen_kronecker(15, 16, 2)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    reprs = [ssb.build_slimsell(g, 32, n) for _ in range(world)]
+    ranges = partition_chunks(reprs[0].cl, 32, world)
+    shards = [DeviceShard(r, b, e) for r, (b, e) in zip(reprs, ranges)]
+    for root in (0, 5, 2000):
+        for v, sw, Lc in ((3, True, 64), (0, True, 0), (3, False, 0), (1, True, 16)):
+            o = opts(ssb, v, sw, Lc)
+            dist, parent, per_iter = run_sharded_bfs(shards, LocalComm(), root, o)
+            b = port.bfs_spmv(L, root, v, sw, Lc)
+            assert np.array_equal(dist, b.dist), (root, v, world)
+            if v == 3:
+                assert np.array_equal(parent, b.parent), (root, v, world)
+            assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
