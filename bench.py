@@ -36,6 +36,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+DATA = {"kronecker": "synthetic (device Kronecker generator, bit-identical to the reference gen_kronecker)",
+        "er": "synthetic (Erdos-Renyi generator, bit-identical to the reference gen_erdos_renyi)"}
 METRIC = "GTEPS (Graph500 BFS) Kronecker scale 26 at 1/2/4/8 B200; % HBM roofline"
 FALLBACK_HBM = 6650.0
 
@@ -53,6 +55,9 @@ def args_():
     ap.add_argument("--slimchunk", type=int, default=2048)
     ap.add_argument("--variant", default="selmax", choices=["tropical", "real", "boolean", "selmax"])
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er"],
+                    help="er: BASELINE config 4, gen_erdos_renyi(2^scale, avg_degree/(n-1), seed)")
+    ap.add_argument("--avg-degree", type=float, default=16.0)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slimwork", action="store_true")
@@ -178,7 +183,11 @@ def dist_env():
 # ---------------------------------------------------------------------------
 def build_graph(ssb, a, log):
     t0 = time.time()
-    g = ssb.gen_kronecker(a.scale, a.edgefactor, a.seed)
+    if a.graph == "er":
+        n = 1 << a.scale
+        g = ssb.gen_erdos_renyi(n, a.avg_degree / (n - 1), a.seed)
+    else:
+        g = ssb.gen_kronecker(a.scale, a.edgefactor, a.seed)
     t1 = time.time()
     r = ssb.build_slimsell(g, 32, g.num_vertices())
     t2 = time.time()
@@ -235,7 +244,9 @@ def main():
     variant_id = {"tropical": 0, "real": 1, "boolean": 2, "selmax": 3}[a.variant]
     slimwork = not a.no_slimwork
     cores = os.cpu_count() or 1
-    workload = (f"kronecker scale {a.scale} ef {a.edgefactor} seed {a.seed}, SlimSell C=32 sigma=n, "
+    gdesc = (f"erdos-renyi n=2^{a.scale} avg degree {a.avg_degree:g} seed {a.seed}" if a.graph == "er"
+             else f"kronecker scale {a.scale} ef {a.edgefactor} seed {a.seed}")
+    workload = (f"{gdesc}, SlimSell C=32 sigma=n, "
                 f"{a.variant}, slimwork={'on' if slimwork else 'off'}, slimchunk L={a.slimchunk}, "
                 f"{a.roots} Graph500 roots/step")
 
@@ -390,9 +401,8 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(max_ms, 3),
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic (device Kronecker generator, "
-        "bit-identical to the reference gen_kronecker)",
-        "config": {"workload": workload, "scale": a.scale, "edgefactor": a.edgefactor,
+        "vs_baseline": None, "dtype": "int32", "data": DATA[a.graph],
+        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor,
                    "C": 32, "sigma": "n", "semiring": a.variant, "slimwork": slimwork,
                    "slimchunk_len": a.slimchunk, "roots_per_step": len(roots),
                    "root_rule": "pick_roots stream (cli.cpp:114-134) rejecting degree 0",
@@ -496,8 +506,8 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(max_ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic (device Kronecker generator, bit-identical to the reference gen_kronecker)",
-        "config": {"workload": workload, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
+        "data": DATA[a.graph],
+        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
                    "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
                    "roots_per_step": len(roots), "parallelism": f"chunk-range shards x{world}",
                    "l2": "inputs larger than L2"},
@@ -544,7 +554,7 @@ def main_reference(a, world, rank, local, log, variant_id, slimwork, cores, work
         "warmup": a.warmup, "ms_per_step": round(1e3 * float(np.mean(times)), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": workload, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
+        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
                    "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk},
         "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": cores, "kind": "reference",
                          "sample": sample},

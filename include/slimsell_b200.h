@@ -84,6 +84,11 @@ int ssb_edges_from_pairs(const int64_t* uv, int64_t count, int64_t n, ssb_edges*
  * device: counter-based SplitMix64 draws + from_pairs normalisation. */
 int ssb_gen_kronecker(int64_t scale, int64_t edgefactor, uint64_t seed,
                       const double initiator[4], ssb_edges** out);
+/* gen_erdos_renyi (generator.hpp:50, generator.cpp:15-58), bit-exact: the
+ * counter-based geometric skips are drawn by all host threads with the same
+ * libm as the reference, prefix-summed, and decoded to (u, v) on the device.
+ * EINVAL for n < 0 or p outside [0, 1]. */
+int ssb_gen_erdos_renyi(int64_t n, double p, uint64_t seed, ssb_edges** out);
 /* Graph::num_vertices / num_edges (graph.hpp:42-43). */
 int ssb_edges_info(const ssb_edges* e, int64_t* n, int64_t* m);
 /* Graph::edges() (graph.hpp:44): 2*m int64, sorted (u<v) pairs. */

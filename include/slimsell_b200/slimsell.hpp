@@ -136,6 +136,13 @@ inline Graph gen_kronecker(std::int64_t scale, std::int64_t edgefactor, std::uin
   return Graph(h);
 }
 
+/// generator.hpp:50 — bit-exact (host-drawn skips, device decode).
+inline Graph gen_erdos_renyi(vid_t n, double p, std::uint64_t seed) {
+  ssb_edges* h = nullptr;
+  detail::check(ssb_gen_erdos_renyi(n, p, seed, &h));
+  return Graph(h);
+}
+
 inline Graph gen_path(vid_t n) {  // generator.hpp:62
   if (n < 1) throw std::invalid_argument("path needs n >= 1");
   std::vector<std::pair<vid_t, vid_t>> p;

@@ -64,6 +64,7 @@ def lib() -> C.CDLL:
         "ssb_set_device": (C.c_int, [C.c_int]),
         "ssb_edges_from_pairs": (C.c_int, [i64p, C.c_int64, C.c_int64, pvp]),
         "ssb_gen_kronecker": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_double), pvp]),
+        "ssb_gen_erdos_renyi": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, pvp]),
         "ssb_edges_info": (C.c_int, [vp, i64p, i64p]),
         "ssb_edges_export": (C.c_int, [vp, i64p]),
         "ssb_to_csr": (C.c_int, [vp, i64p, i64p]),

@@ -179,6 +179,12 @@ def gen_kronecker(scale: int, edgefactor: int, seed: int,
     return Graph(h)
 
 
+def gen_erdos_renyi(n: int, p: float, seed: int) -> Graph:  # generator.hpp:50
+    h = C.c_void_p()
+    _check(_L.lib().ssb_gen_erdos_renyi(n, p, seed, C.byref(h)))
+    return Graph(h)
+
+
 def gen_path(n: int) -> Graph:  # generator.hpp:62
     if n < 1:
         raise InvalidArgument("path needs n >= 1")

@@ -176,6 +176,46 @@ struct Probe {
   __device__ __forceinline__ uint32_t exact(int32_t c) const {
     return (Fc[c >> 5] >> (c & 31)) & 1u;  // L1 is invalidated by every grid.sync fence
   }
+  // The four probes of one int4 as one batch: four shared loads issued back to
+  // back (one shared-memory round trip instead of four dependent ones).
+  __device__ __forceinline__ uint32_t vbits4(const int32_t (&c)[4]) const {
+    int32_t v[4];
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = min(c[q], (c[q] >> kSummaryShift) + Pt);
+    const uint32_t base = uint32_t(__cvta_generic_to_shared(sm));
+    asm volatile(
+        "ld.shared.u32 %0, [%4];\n\t"
+        "ld.shared.u32 %1, [%5];\n\t"
+        "ld.shared.u32 %2, [%6];\n\t"
+        "ld.shared.u32 %3, [%7];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+        : "r"(base + 4u * uint32_t(v[0] >> 5)), "r"(base + 4u * uint32_t(v[1] >> 5)),
+          "r"(base + 4u * uint32_t(v[2] >> 5)), "r"(base + 4u * uint32_t(v[3] >> 5)));
+    uint32_t b = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b |= (__funnelshift_r(w[q], w[q], v[q]) & 1u) << q;
+    return b;
+  }
+  // Exact frontier bits of the cells flagged in `need`, the four global loads
+  // in flight together (unflagged lanes re-read word 0: one shared sector).
+  __device__ __forceinline__ uint32_t exact4(const int32_t (&c)[4], uint32_t need) const {
+    uint32_t w[4];
+    const uint32_t* p[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) p[q] = Fc + (((need >> q) & 1u) ? (c[q] >> 5) : 0);
+    asm volatile(
+        "ld.global.u32 %0, [%4];\n\t"
+        "ld.global.u32 %1, [%5];\n\t"
+        "ld.global.u32 %2, [%6];\n\t"
+        "ld.global.u32 %3, [%7];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+        : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]));
+    uint32_t b = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b |= ((w[q] >> (c[q] & 31)) & 1u) << q;
+    return b & need;
+  }
 };
 
 // Four cells of one column (rows 4·lg .. 4·lg+3). `hit` bit q says row q is
@@ -195,10 +235,13 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
                                            int32_t (&best)[4]) {
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
   const uint32_t open = kEarly ? ~hit : 0xffffffffu;
+  // dense sweeps batch the four shared probes; sparse ones keep the shorter
+  // per-cell sequence (their cost is instruction issue, not latency)
+  const uint32_t vb = kEarly ? pr.vbits4(c) & open : 0u;
   uint32_t need = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t b = pr.vbit(c[q]) & (open >> q);
+    const uint32_t b = kEarly ? (vb >> q) & 1u : pr.vbit(c[q]);
     const bool def = b && c[q] < pr.P;
     if (kSelMax) best[q] = def ? c[q] : best[q];
     // sel-max without early exit derives its row mask from best afterwards
@@ -206,10 +249,17 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
     need |= uint32_t(b && c[q] >= pr.P) << q;
   }
   if (__any_sync(0xffffffffu, need)) {  // warp-uniform: no reconvergence bookkeeping
+    if (kEarly) {
+      const uint32_t e = pr.exact4(c, need);
+      hit |= e;
+      if (kSelMax) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if ((need >> q) & 1u) {
-        if (pr.exact(c[q])) {
+        for (int q = 0; q < 4; ++q) best[q] = ((e >> q) & 1u) ? c[q] : best[q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (((need >> q) & 1u) && pr.exact(c[q])) {
           hit |= 1u << q;
           if (kSelMax) best[q] = c[q];
         }
@@ -549,7 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         // within each 4-column step. Out-of-range indices re-read the lane's
         // own rows of the last column (idempotent).
         const int4* base = reinterpret_cast<const int4*>(a.col + a.cs[chunk] + int64_t(cb) * 32);
-        uint32_t hit = 0;
+        // early-exit sweeps start with the rows already settled (visited or
+        // padding) marked decided: their probes are skipped
+        uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
         sweep_long<kSelMax, kEarly>(base, len, lane, lg, pr, pol, hit, best);
         uint32_t m = hit << (4 * lg);
@@ -590,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
                                 : reinterpret_cast<const int4*>(g_pad_column) + (lg & 7);
         const int32_t jlast = len > 0 ? len - 1 : 0;
         const int64_t stride = len > 0 ? 8 : 0;
-        uint32_t hit = 0;
+        uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
         sweep_group<kSelMax, kEarly>(p, jlast, stride, maxlen, pr, pol, hit, best);
         // 32-bit row mask of the unit (rows 4*lg+q)
@@ -1161,9 +1213,11 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
 bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
            int64_t cap, std::vector<ssb_iter_stats>& stats) {
   Run32 r = prepare32(g, root_pos, root_code, o, 0, g.n_chunks);
+  // SSB_ITERS_PER_LAUNCH=1 (profiling): one cooperative launch per iteration
+  const int64_t per = std::max(1, std::min(kItersPerLaunch, env_int("SSB_ITERS_PER_LAUNCH", kItersPerLaunch)));
   while (r.k <= cap) {
     bool conv = false;
-    launch32(g, r, std::min<int64_t>(cap + 1, r.k + kItersPerLaunch), stats, conv);
+    launch32(g, r, std::min<int64_t>(cap + 1, r.k + per), stats, conv);
     if (conv) return true;
   }
   return false;

@@ -60,6 +60,13 @@ int ssb_gen_kronecker(int64_t scale, int64_t edgefactor, uint64_t seed,
   });
 }
 
+int ssb_gen_erdos_renyi(int64_t n, double p, uint64_t seed, ssb_edges** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = ssb::gen_erdos_renyi(n, p, seed);
+  });
+}
+
 int ssb_edges_info(const ssb_edges* e, int64_t* n, int64_t* m) {
   return guarded([&] {
     need(e, "edges");

@@ -10,6 +10,8 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <thread>
+#include <vector>
 
 #include "ssb_internal.cuh"
 
@@ -229,6 +231,104 @@ ssb_edges* gen_kronecker(int64_t scale, int64_t ef, uint64_t seed, const double 
       unit_threshold(abc), e->bits, sentinel);
   SSB_CUDA(cudaGetLastError());
   normalise(*e, keys, cand, sentinel);
+  return e.release();
+}
+
+namespace {
+// Pair index t of the upper triangle (row-major, pairs (u, u+1+v)) -> key.
+// Row u starts at S(u) = u(n-1) - u(u-1)/2; exact integer binary search.
+__global__ void er_decode_kernel(const int64_t* __restrict__ t, int64_t count, int64_t n,
+                                 int bits, uint64_t* __restrict__ keys) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const int64_t x = t[i];
+    int64_t lo = 0, hi = n - 2;  // largest u with S(u) <= x
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      const int64_t s = mid * (n - 1) - mid * (mid - 1) / 2;
+      if (s <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t u = lo;
+    const int64_t v = u + 1 + (x - (u * (n - 1) - u * (u - 1) / 2));
+    keys[i] = (uint64_t(u) << bits) | uint64_t(v);
+  }
+}
+}  // namespace
+
+// gen_erdos_renyi (generator.cpp:15-58). The reference walks the pair index
+// space [0, n(n-1)/2) with geometric skips drawn from ONE SplitMix64 stream
+// (split(0xe5)); the stream is counter-based, so the skips are computed by all
+// host threads at once with the same libm log/log1p as the reference
+// (bit-exact — a device log could differ in the last ulp and move a floor),
+// their prefix sums give the pair indices, and the device decodes them to
+// (u, v). The pairs come out sorted and unique, i.e. already normalised.
+ssb_edges* gen_erdos_renyi(int64_t n, double p, uint64_t seed) {
+  if (n < 0) fail(SSB_EINVAL, "vertex count must be >= 0");
+  if (!(p >= 0.0 && p <= 1.0)) fail(SSB_EINVAL, "edge probability must be in [0, 1]");
+  if (n >= (int64_t{1} << 31)) fail(SSB_EINVAL, "device layout supports n < 2^31");
+  std::vector<int64_t> pos;  // pair indices, ascending
+  const int64_t total = n > 1 ? n * (n - 1) / 2 : 0;
+  if (p > 0.0 && n > 1) {
+    if (p == 1.0) {
+      pos.resize(size_t(total));
+      for (int64_t i = 0; i < total; ++i) pos[size_t(i)] = i;
+    } else {
+      const uint64_t s0 = mix64(seed ^ mix64(0xe5ULL + 0x6a09e667f3bcc909ULL));
+      const double denom = std::log1p(-p);
+      const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+      // draw i (0-based) -> geometric skip, generator.cpp:48-53
+      auto skip_of = [&](int64_t i) -> int64_t {
+        const uint64_t x = mix64(s0 + uint64_t(i + 1) * kGamma);
+        const double unit = 1.0 - double(x >> 11) * 0x1.0p-53;
+        return int64_t(std::floor(std::log(unit) / denom));
+      };
+      const double mean = double(total) * p;
+      int64_t drawn = 0, cursor = -1;  // cursor: last pair index (t_{-1} = -1)
+      bool first = true;
+      std::vector<int64_t> sk;
+      pos.reserve(size_t(std::min<double>(mean + 10.0 * std::sqrt(mean + 1.0) + 1024.0, double(total))));
+      while (true) {
+        // first batch: the expected pair count + 10 sigma; then 1M draws at a time
+        const int64_t batch = drawn == 0 ? int64_t(mean + 10.0 * std::sqrt(mean + 1.0)) + 1024
+                                         : int64_t{1} << 20;
+        sk.resize(size_t(std::max<int64_t>(batch, 1 << 16)));
+        const int64_t b = int64_t(sk.size());
+        std::vector<std::thread> th;
+        for (unsigned w = 0; w < nt; ++w)
+          th.emplace_back([&, w] {
+            for (int64_t i = b * w / nt; i < b * (w + 1) / nt; ++i) sk[size_t(i)] = skip_of(drawn + i);
+          });
+        for (auto& x : th) x.join();
+        bool done = false;
+        for (int64_t i = 0; i < b; ++i) {
+          // advance(first ? skip : 1 + skip) from the cursor (generator.cpp:35-53)
+          cursor += (first ? sk[size_t(i)] + 1 : 1 + sk[size_t(i)]);
+          first = false;
+          if (cursor >= total || cursor < 0) {
+            done = true;
+            break;
+          }
+          pos.push_back(cursor);
+        }
+        drawn += b;
+        if (done) break;
+      }
+    }
+  }
+  auto e = std::make_unique<ssb_edges>();
+  e->n = n;
+  e->bits = bits_for(std::max<int64_t>(n, 1));
+  const int64_t m = int64_t(pos.size());
+  e->m = m;
+  e->keys.alloc(size_t(std::max<int64_t>(m, 1)));
+  if (m) {
+    DevBuf<int64_t> dt{static_cast<size_t>(m)};
+    SSB_CUDA(cudaMemcpyAsync(dt.p, pos.data(), 8 * m, cudaMemcpyHostToDevice, e->sc.s));
+    er_decode_kernel<<<grid_for(m), 256, 0, e->sc.s>>>(dt.p, m, n, e->bits, e->keys.p);
+    SSB_CUDA(cudaGetLastError());
+    e->sc.sync();
+  }
   return e.release();
 }
 

@@ -167,6 +167,7 @@ ssb_graph* graph_from_host_layout(int64_t n, int64_t C, int64_t sigma, int64_t n
 // generator.cu
 ssb_edges* edges_from_pairs(const int64_t* uv, int64_t count, int64_t n);
 ssb_edges* gen_kronecker(int64_t scale, int64_t ef, uint64_t seed, const double init[4]);
+ssb_edges* gen_erdos_renyi(int64_t n, double p, uint64_t seed);
 void edges_to_csr(const ssb_edges& e, int64_t* row, int64_t* col);
 // spmv.cu
 void spmv_step(const ssb_graph& g, int variant, const int64_t* x_prev, int64_t* out,

@@ -9,8 +9,10 @@ ap.add_argument("--root", type=int, default=2564265)
 ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--variant", type=int, default=3)
 ap.add_argument("--L", type=int, default=128)
+ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er"])
 a = ap.parse_args()
-g = ssb.gen_kronecker(a.scale, 16, 1)
+g = (ssb.gen_erdos_renyi(1 << a.scale, 16 / ((1 << a.scale) - 1), 1) if a.graph == "er"
+     else ssb.gen_kronecker(a.scale, 16, 1))
 r = ssb.build_slimsell(g, 32, g.num_vertices())
 del g
 db = ssb.DeviceBfs(r)

@@ -338,3 +338,17 @@ def test_chunk_sharded_device_bfs_matches_single_gpu(ssb, port, monkeypatch, wor
             if v == 3:
                 assert np.array_equal(parent, b.parent), (root, v, world)
             assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
+
+
+def test_device_erdos_renyi_matches_oracle(ssb, port):
+    """gen_erdos_renyi (generator.cpp:15-58) bit-exact, incl. p = 0 / 1 and
+    the config-4 shape (average degree 16) at 2^18 and 2^20 vertices."""
+    cases = [(1, 0.5, 1), (2, 1.0, 3), (50, 0.0, 3), (40, 1.0, 2), (300, 0.05, 7), (5000, 0.003, 11),
+             (1 << 18, 16 / ((1 << 18) - 1), 1), (1 << 20, 16 / ((1 << 20) - 1), 1)]
+    for n, p, seed in cases:
+        g = ssb.gen_erdos_renyi(n, p, seed)
+        nn, uv = port.gen_erdos_renyi(n, p, seed)
+        assert g.num_vertices() == nn == n, (n, p, seed)
+        assert np.array_equal(g.edges(), uv), (n, p, seed)
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.gen_erdos_renyi(10, 1.5, 1)
