@@ -167,9 +167,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def b_alg(stats, C: int, n_padded: int) -> float:
-    """Algorithmic HBM bytes of one BFS."""
-    cols = sum(s.columns_processed for s in stats)
+def b_alg(stats, C: int, n_padded: int, swept=None) -> float:
+    """Algorithmic HBM bytes of one BFS: 4·C bytes per column
+    the sweeps needed — `swept` (ssb_bfs_columns_swept: early-exit sweeps stop
+    a unit once all its rows are decided) or, without it, Σ columns_processed —
+    plus three n/8 bitmaps per iteration and the level + parent rows."""
+    cols = swept if swept is not None else sum(s.columns_processed for s in stats)
     return 4.0 * C * cols + 3.0 * len(stats) * n_padded / 8.0 + 8.0 * n_padded
 
 
@@ -307,7 +310,7 @@ def main():
             kms, nl = db.last_timing()
             tot += ms
             launches += nl
-            balg_total += b_alg(stats, r.C, r.n_padded)
+            balg_total += b_alg(stats, r.C, r.n_padded, db.columns_swept())
             kernel_ms_total += kms
             n_bfs += 1
             per_root_ms.setdefault(root, []).append(ms)

@@ -151,6 +151,11 @@ int ssb_bfs_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent
 /* Timing of the last ssb_bfs_run: CUDA-event time of the main BFS kernel
  * launches alone (kernel_ms) and how many kernels the BFS launched. */
 int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches);
+/* Columns the last run actually streamed from HBM, summed over iterations:
+ * the early-exit sweeps stop a work unit once every row of it is decided, so
+ * this is <= Σ IterStats.columns_processed (the reference's counter). The
+ * roofline's algorithmic bytes are 4·C per swept column. */
+int ssb_bfs_columns_swept(ssb_graph* g, int64_t* swept);
 /* ---- multi-GPU: chunk-range shards -------------------
  * Each rank builds (or holds) the layout, owns chunks [chunk_begin, chunk_end)
  * (C = 32: chunk i <-> frontier word i) and the replicated 1-bit frontier.

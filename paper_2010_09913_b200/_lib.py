@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
                                   C.c_int64, i64p, C.POINTER(C.c_double)]),
         "ssb_bfs_fetch": (C.c_int, [vp, C.c_int, i64p, i64p, i64p]),
         "ssb_bfs_edges_traversed": (C.c_int, [vp, i64p]),
+        "ssb_bfs_columns_swept": (C.c_int, [vp, i64p]),
         "ssb_bfs_shard_begin": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.c_int64, C.c_int64]),
         "ssb_bfs_shard_step": (C.c_int, [vp, C.POINTER(IterStatsC), C.c_void_p]),
         "ssb_bfs_shard_exchange": (C.c_int, [vp, C.c_void_p, C.c_int64]),

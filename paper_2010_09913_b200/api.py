@@ -377,3 +377,9 @@ class DeviceBfs:
         m = np.zeros(1, np.int64)
         _check(_L.lib().ssb_bfs_edges_traversed(self.r._h, _p(m)))
         return int(m[0])
+
+    def columns_swept(self) -> int:
+        """Columns the last run streamed (<= Σ columns_processed: early exit)."""
+        m = np.zeros(1, np.int64)
+        _check(_L.lib().ssb_bfs_columns_swept(self.r._h, _p(m)))
+        return int(m[0])

@@ -349,20 +349,27 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
 // (rows) is fixed per lane and grp picks the column within each 4-column
 // step. Out-of-range indices re-read the lane's own rows of the last column
 // (idempotent). Loads run four steps ahead of the probes. On return `hit` and
-// `best` are combined over the four lanes that share rows.
+// `best` are combined over the four lanes that share rows. Early-exit sweeps
+// stop the unit once all 32 rows are decided (the semiring "plus" has
+// short-circuited for every row, so the remaining columns cannot change the
+// result). Returns the number of columns swept.
 template <bool kSelMax, bool kEarly>
-__device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int lane, int lg,
+__device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int lane, int lg,
                                            const Probe& pr, uint64_t pol, uint32_t& hit,
                                            int32_t (&best)[4]) {
   const int32_t nv = len * 8, imax = nv - 8 + lg;
   const int32_t nsteps = (nv + 31) >> 5;
   // lanes sharing rows exchange decided-row bits after every 4 steps
-  auto share = [&]() {
+  // ... and report whether every row of the unit is decided (warp-uniform)
+  auto share = [&]() -> bool {
     if (kEarly) {
       hit |= __shfl_xor_sync(0xffffffffu, hit, 8);
       hit |= __shfl_xor_sync(0xffffffffu, hit, 16);
+      return __all_sync(0xffffffffu, hit == 0xfu);
     }
+    return false;
   };
+  int32_t swept = len;
   if (!(kSelMax && kEarly)) {
     // forward sweep: step s = 0, 1, ...
     int4 v0 = ld_stream(base + min(lane, imax), pol);
@@ -373,6 +380,7 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
     // prefetch pointer then advances by 2 KB per 4 steps, offsets immediate.
     const int4* pf = base + 128 + lane;
     int32_t s = 0;
+    bool done = false;
     for (; s + 9 <= nsteps; s += 4, pf += 128) {
       take_cells<kSelMax, kEarly>(v0, pr, hit, best);
       v0 = ld_stream(pf, pol);
@@ -382,9 +390,13 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
       v2 = ld_stream(pf + 64, pol);
       take_cells<kSelMax, kEarly>(v3, pr, hit, best);
       v3 = ld_stream(pf + 96, pol);
-      share();
+      if (share()) {
+        done = true;
+        swept = 4 * (s + 4);
+        break;
+      }
     }
-    for (; s < nsteps; s += 4) {
+    for (; !done && s < nsteps; s += 4) {
       const bool more = s + 4 < nsteps;  // warp-uniform
       const int32_t i0 = (s + 4) * 32 + lane;
       take_cells<kSelMax, kEarly>(v0, pr, hit, best);
@@ -395,7 +407,10 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
       if (more) v2 = ld_stream(base + min(i0 + 64, imax), pol);
       take_cells<kSelMax, kEarly>(v3, pr, hit, best);
       if (more) v3 = ld_stream(base + min(i0 + 96, imax), pol);
-      share();
+      if (share()) {
+        swept = min(len, 4 * (s + 4));
+        break;
+      }
     }
   } else {
     // backward sweep (sel-max, early exit): steps nsteps-1 .. 0, clamped at 0
@@ -408,6 +423,9 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
     // steps top-r-4 .. top-r-7 are all full and >= 0 while r + 8 <= nsteps
     const int4* pf = base + 32 * (top - 4) + lane;
     int32_t r = 0;
+    bool done = false;
+    // columns in the top r steps (the top step may be partial)
+    auto cols_of = [&](int32_t st) { return max(0, len - 4 * (nsteps - st)); };
     for (; r + 8 <= nsteps; r += 4, pf -= 128) {
       take_cells<kSelMax, kEarly>(v0, pr, hit, best);
       v0 = ld_stream(pf, pol);
@@ -417,9 +435,13 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
       v2 = ld_stream(pf - 64, pol);
       take_cells<kSelMax, kEarly>(v3, pr, hit, best);
       v3 = ld_stream(pf - 96, pol);
-      share();
+      if (share()) {
+        done = true;
+        swept = cols_of(r + 4);
+        break;
+      }
     }
-    for (; r < nsteps; r += 4) {
+    for (; !done && r < nsteps; r += 4) {
       const bool more = r + 4 < nsteps;  // warp-uniform
       take_cells<kSelMax, kEarly>(v0, pr, hit, best);
       if (more) v0 = ld_stream(at(top - r - 4), pol);
@@ -429,7 +451,10 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
       if (more) v2 = ld_stream(at(top - r - 6), pol);
       take_cells<kSelMax, kEarly>(v3, pr, hit, best);
       if (more) v3 = ld_stream(at(top - r - 7), pol);
-      share();
+      if (share()) {
+        swept = cols_of(min(nsteps, r + 4));
+        break;
+      }
     }
   }
   // combine the four column groups
@@ -443,14 +468,17 @@ __device__ __forceinline__ void sweep_long(const int4* base, int32_t len, int la
   }
   hit |= __shfl_xor_sync(0xffffffffu, hit, 8);
   hit |= __shfl_xor_sync(0xffffffffu, hit, 16);
+  return swept;
 }
 
 // One short unit per 8-lane group: column j of the unit is int4 p[8j] (lane
 // lg: rows 4lg..4lg+3). Groups shorter than maxlen re-read their last (or,
 // backward, first) column — idempotent for both reductions; groups without a
 // unit read a padding column. Loads run 4 columns ahead of the probes.
+// Early-exit sweeps stop once every row of the four units is decided. Returns
+// the number of column steps run (the group's unit swept min(len, that)).
 template <bool kSelMax, bool kEarly>
-__device__ __forceinline__ void sweep_group(const int4* p, int32_t jlast, int64_t stride,
+__device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int64_t stride,
                                             int32_t maxlen, const Probe& pr, uint64_t pol,
                                             uint32_t& hit, int32_t (&best)[4]) {
   constexpr bool kBack = kSelMax && kEarly;
@@ -459,7 +487,8 @@ __device__ __forceinline__ void sweep_group(const int4* p, int32_t jlast, int64_
   int4 v1 = ld_stream(at(1), pol);
   int4 v2 = ld_stream(at(2), pol);
   int4 v3 = ld_stream(at(3), pol);
-  for (int32_t j = 0; j < maxlen; j += 4) {
+  int32_t j = 0;
+  while (j < maxlen) {
     const bool more = j + 4 < maxlen;  // warp-uniform
     take_cells<kSelMax, kEarly>(v0, pr, hit, best);
     if (more) v0 = ld_stream(at(j + 4), pol);
@@ -469,11 +498,14 @@ __device__ __forceinline__ void sweep_group(const int4* p, int32_t jlast, int64_
     if (more) v2 = ld_stream(at(j + 6), pol);
     take_cells<kSelMax, kEarly>(v3, pr, hit, best);
     if (more) v3 = ld_stream(at(j + 7), pol);
+    j += 4;
+    if (kEarly && __all_sync(0xffffffffu, hit == 0xfu)) break;
   }
   if (kSelMax) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) hit |= uint32_t(best[q] >= 0) << q;
   }
+  return min(j, maxlen);
 }
 
 template <bool kSelMax>
@@ -481,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   extern __shared__ uint4 smem_v4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem_v4);
   uint32_t* summ = sm + 4 + a.PW;
-  __shared__ unsigned long long blk[5];
+  __shared__ unsigned long long blk[6];  // stats slots 0-4 and 6
 
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
@@ -516,13 +548,13 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       // clear the summary buffer of iteration k+1 (last read at k-1)
       for (int i = blockIdx.x * kThreads + threadIdx.x; i < a.SW; i += gridDim.x * kThreads)
         Sx[i] = 0u;
-      if (threadIdx.x < 5) blk[threadIdx.x] = 0ull;
+      if (threadIdx.x < 6) blk[threadIdx.x] = 0ull;
     }
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
-    uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0;
+    uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0, c_swept = 0;
     const Probe pr{sm + 4, Fc, a.PW * 32, a.PW * 32 - ((a.PW * 32) >> kSummaryShift)};
 
     // Active task list: iteration 1 walks every task; later iterations only the
@@ -603,7 +635,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         // padding) marked decided: their probes are skipped
         uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
-        sweep_long<kSelMax, kEarly>(base, len, lane, lg, pr, pol, hit, best);
+        const int32_t sw = sweep_long<kSelMax, kEarly>(base, len, lane, lg, pr, pol, hit, best);
+        if (lane == 0) c_swept += uint32_t(sw);
         uint32_t m = hit << (4 * lg);
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
         m |= __shfl_xor_sync(0xffffffffu, m, 2);
@@ -642,9 +675,11 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
                                 : reinterpret_cast<const int4*>(g_pad_column) + (lg & 7);
         const int32_t jlast = len > 0 ? len - 1 : 0;
         const int64_t stride = len > 0 ? 8 : 0;
-        uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
+        // (a group without a unit counts as decided)
+        uint32_t hit = kEarly ? (src < 0 ? 0xfu : ((uvis | ~ureal) >> (4 * lg)) & 0xfu) : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
-        sweep_group<kSelMax, kEarly>(p, jlast, stride, maxlen, pr, pol, hit, best);
+        const int32_t ran = sweep_group<kSelMax, kEarly>(p, jlast, stride, maxlen, pr, pol, hit, best);
+        if (lg == 0) c_swept += uint32_t(min(len, ran));
         // 32-bit row mask of the unit (rows 4*lg+q)
         uint32_t m = hit << (4 * lg);
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
@@ -667,6 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       c_skip += __shfl_xor_sync(0xffffffffu, c_skip, o);
       c_sub += __shfl_xor_sync(0xffffffffu, c_sub, o);
       c_cols += __shfl_xor_sync(0xffffffffu, c_cols, o);
+      c_swept += __shfl_xor_sync(0xffffffffu, c_swept, o);
     }
     if (lane == 0) {
       atomicAdd(&blk[0], (unsigned long long)c_front);
@@ -674,10 +710,12 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       atomicAdd(&blk[2], (unsigned long long)c_skip);
       atomicAdd(&blk[3], (unsigned long long)c_sub);
       atomicAdd(&blk[4], (unsigned long long)c_cols);
+      atomicAdd(&blk[5], (unsigned long long)c_swept);
     }
     __syncthreads();
-    if (threadIdx.x < 5)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[rec * kStatW + threadIdx.x]),
+    if (threadIdx.x < 6)
+      atomicAdd(reinterpret_cast<unsigned long long*>(
+                    &a.stats[rec * kStatW + (threadIdx.x < 5 ? threadIdx.x : 6)]),
                 blk[threadIdx.x]);
     if (threadIdx.x == 0 && a.trace) atomicAdd(&a.trace[2], 1);
     grid.sync();
@@ -1188,6 +1226,7 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
     }
   }
   collect_stats(r.rec, r.k, ran, stats);
+  for (int64_t i = 0; i < ran; ++i) g.last_swept += r.rec[size_t(i) * kStatW + 6];
   for (size_t i = stats.size() - size_t(ran); i < stats.size(); ++i) {
     stats[i].chunks_processed += g.plan.empty_chunks - (r.z_skip ? 1 : 0);
     stats[i].chunks_skipped += r.z_skip ? 1 : 0;
@@ -1277,6 +1316,7 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
     float ms = 0;
     SSB_CUDA(cudaEventElapsedTime(&ms, g.sc.e0, g.sc.e1));
     rec[5] = int64_t(double(ms) * 1e6);
+    g.last_swept += rec[4];  // the generic engine streams every processed column
     g.last_kernel_ms += ms;
     g.last_launches += g.n_chunks ? 2 : 0;
     collect_stats(rec, k, 1, stats);
@@ -1322,6 +1362,7 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
   std::vector<ssb_iter_stats> st;
   g.last_kernel_ms = 0;
   g.last_launches = 0;
+  g.last_swept = 0;
   cudaEvent_t t0, t1;
   SSB_CUDA(cudaEventCreate(&t0));
   SSB_CUDA(cudaEventCreate(&t1));
@@ -1444,6 +1485,7 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
   auto st = std::make_shared<ShardState>();
   g.last_kernel_ms = 0;
   g.last_launches = 0;
+  g.last_swept = 0;
   st->r = prepare32(g, root_pos, root_code, o, cb, ce);
   st->r.stepping = true;
   st->r.cb = cb;

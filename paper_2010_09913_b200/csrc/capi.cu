@@ -253,6 +253,15 @@ int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches) {
   });
 }
 
+int ssb_bfs_columns_swept(ssb_graph* g, int64_t* swept) {
+  return guarded([&] {
+    need(g, "graph");
+    need(swept, "swept");
+    if (!g->last_valid) ssb::fail(SSB_EINVAL, "no BFS result on this graph");
+    *swept = g->last_swept;
+  });
+}
+
 int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
                         int64_t chunk_begin, int64_t chunk_end) {
   return guarded([&] {

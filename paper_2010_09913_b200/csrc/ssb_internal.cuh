@@ -153,6 +153,7 @@ struct ssb_graph {
   bool last_valid = false;
   double last_kernel_ms = 0;  // CUDA-event time of the main BFS kernel launches
   int64_t last_launches = 0;  // kernels launched by the last BFS
+  int64_t last_swept = 0;     // columns the last BFS actually streamed (Σ over iterations)
   std::shared_ptr<void> shard;  // state of a sharded (multi-GPU) BFS in progress
 
   ssb::StreamCtx sc;

@@ -19,5 +19,5 @@ db = ssb.DeviceBfs(r)
 o = ssb.BfsOptions(variant=ssb.Variant(a.variant), slimwork=True, slimchunk_len=a.L, max_iterations=a.iters)
 for _ in range(2):
     k, ms, st, rc = db.run(a.root, o)
-    print(f"iters={k} device_ms={ms:.3f} kernel_ms={db.last_timing()[0]:.3f}",
+    print(f"iters={k} device_ms={ms:.3f} kernel_ms={db.last_timing()[0]:.3f} swept={db.columns_swept()}",
           [(s.iteration, round(s.elapsed_ns / 1e6, 3), s.columns_processed, s.frontier_size) for s in st])
