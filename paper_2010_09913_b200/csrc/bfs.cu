@@ -168,10 +168,12 @@ struct Probe {
   int32_t P;           // prefix vertices (multiple of 2^S)
   int32_t Pt;          // P - (P >> S)
 
-  __device__ __forceinline__ uint32_t vbit(int32_t c) const {
+  __device__ __forceinline__ uint32_t vbit(int32_t c) const { return vrot(c) & 1u; }
+  // the probe's word rotated so that its bit sits at bit 0
+  __device__ __forceinline__ uint32_t vrot(int32_t c) const {
     const int32_t v = min(c, (c >> kSummaryShift) + Pt);
     const uint32_t word = sm[v >> 5];
-    return __funnelshift_r(word, word, v) & 1u;  // bit (v mod 32)
+    return __funnelshift_r(word, word, v);  // bit (v mod 32) -> bit 0
   }
   __device__ __forceinline__ uint32_t exact(int32_t c) const {
     return (Fc[c >> 5] >> (c & 31)) & 1u;  // L1 is invalidated by every grid.sync fence
@@ -235,13 +237,20 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
                                            int32_t (&best)[4]) {
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
   const uint32_t open = kEarly ? ~hit : 0xffffffffu;
-  // dense sweeps batch the four shared probes; sparse ones keep the shorter
-  // per-cell sequence (their cost is instruction issue, not latency)
+  // Sparse sweeps are instruction-issue bound and their probes almost always
+  // miss: test the four probe bits together and leave the per-cell bookkeeping
+  // to the (warp-uniform) rare path. Dense sweeps batch the four shared loads.
+  uint32_t rot[4];
+  if (!kEarly) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rot[q] = pr.vrot(c[q]);
+    if (!__any_sync(0xffffffffu, (rot[0] | rot[1] | rot[2] | rot[3]) & 1u)) return;
+  }
   const uint32_t vb = kEarly ? pr.vbits4(c) & open : 0u;
   uint32_t need = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint32_t b = kEarly ? (vb >> q) & 1u : pr.vbit(c[q]);
+    const uint32_t b = kEarly ? (vb >> q) & 1u : rot[q] & 1u;
     const bool def = b && c[q] < pr.P;
     if (kSelMax) best[q] = def ? c[q] : best[q];
     // sel-max without early exit derives its row mask from best afterwards
