@@ -98,6 +98,21 @@ __device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
   return v;
 }
 
+// Bulk L2 prefetch (no registers, no completion tracking): keeps more of the
+// col stream in flight than the four-step register ring alone can. bytes is a
+// multiple of 16, p 16-byte aligned.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+#ifndef SSB_PF_AHEAD
+#define SSB_PF_AHEAD 1  // in-loop prefetch distance, in 2 KB loop iterations (A/B: 1 best)
+#endif
+constexpr int32_t kPfAhead = SSB_PF_AHEAD;
+#ifndef SSB_PF_HEAD
+#define SSB_PF_HEAD 0  // steps (512 B) of each unit prefetched when its task starts
+#endif
+constexpr int32_t kPfHeadSteps = SSB_PF_HEAD;
+
 struct Args32 {
   const int32_t* col;
   const int64_t* cs;
@@ -168,7 +183,6 @@ struct Probe {
   int32_t P;           // prefix vertices (multiple of 2^S)
   int32_t Pt;          // P - (P >> S)
 
-  __device__ __forceinline__ uint32_t vbit(int32_t c) const { return vrot(c) & 1u; }
   // the probe's word rotated so that its bit sits at bit 0
   __device__ __forceinline__ uint32_t vrot(int32_t c) const {
     const int32_t v = min(c, (c >> kSummaryShift) + Pt);
@@ -391,6 +405,8 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     int32_t s = 0;
     bool done = false;
     for (; s + 9 <= nsteps; s += 4, pf += 128) {
+      if (kPfAhead > 0 && lane == 0 && s + 9 + 4 * kPfAhead <= nsteps)
+        prefetch_l2(pf - lane + 128 * kPfAhead, 2048);
       take_cells<kSelMax, kEarly>(v0, pr, hit, best);
       v0 = ld_stream(pf, pol);
       take_cells<kSelMax, kEarly>(v1, pr, hit, best);
@@ -436,6 +452,9 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     // columns in the top r steps (the top step may be partial)
     auto cols_of = [&](int32_t st) { return max(0, len - 4 * (nsteps - st)); };
     for (; r + 8 <= nsteps; r += 4, pf -= 128) {
+      // steps top-r-4-4A .. top-r-7-4A: int4 [32(top-r-7-4A), +128)
+      if (kPfAhead > 0 && lane == 0 && r + 8 + 4 * kPfAhead <= nsteps)
+        prefetch_l2(pf - lane - 96 - 128 * kPfAhead, 2048);
       take_cells<kSelMax, kEarly>(v0, pr, hit, best);
       v0 = ld_stream(pf, pol);
       take_cells<kSelMax, kEarly>(v1, pr, hit, best);
@@ -607,6 +626,12 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
             if (a.L > 0 && len > 0) c_sub += uint32_t((len + a.L - 1) / a.L);
           }
         }
+      }
+      // every lane prefetches the head (in sweep order) of its unit into L2
+      if (kPfHeadSteps > 0 && has && !skip && U.col_len > 0) {
+        const int32_t hc = min(U.col_len, 4 * kPfHeadSteps);  // columns
+        const int32_t first = (kSelMax && kEarly) ? U.col_len - hc : 0;
+        prefetch_l2(a.col + a.cs[U.chunk] + int64_t(U.col_begin + first) * 32, uint32_t(hc) * 128u);
       }
       // Long units (≥ kWarpUnitCols columns) are swept by the whole warp as one
       // contiguous 128-bit stream; short ones four at a time, one per group.
