@@ -21,3 +21,5 @@ for _ in range(2):
     k, ms, st, rc = db.run(a.root, o)
     print(f"iters={k} device_ms={ms:.3f} kernel_ms={db.last_timing()[0]:.3f} swept={db.columns_swept()}",
           [(s.iteration, round(s.elapsed_ns / 1e6, 3), s.columns_processed, s.frontier_size) for s in st])
+balg = 4.0 * 32 * db.columns_swept() + 3.0 * len(st) * r.n_padded / 8.0 + 8.0 * r.n_padded
+print(f"algorithmic_bytes_last_launch={int(balg)} (bench.py b_alg: 128 B per swept column + 3 bitmaps/iter + 8 B/row)")
