@@ -67,14 +67,17 @@ struct DevBuf {
 struct StreamCtx {
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e_end = nullptr;  // end of the last BFS launch's device work (before any host sync)
   StreamCtx() {
     SSB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     SSB_CUDA(cudaEventCreate(&e0));
     SSB_CUDA(cudaEventCreate(&e1));
+    SSB_CUDA(cudaEventCreate(&e_end));
   }
   ~StreamCtx() {
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
+    if (e_end) cudaEventDestroy(e_end);
     if (s) cudaStreamDestroy(s);
   }
   void sync() { SSB_CUDA(cudaStreamSynchronize(s)); }
