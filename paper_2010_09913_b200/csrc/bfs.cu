@@ -104,6 +104,36 @@ __device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// TMA bulk copy global -> this CTA's shared memory in <= 32 KB pieces
+// (bytes and both addresses 16-byte aligned), completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  for (uint32_t off = 0; off < bytes; off += 32768u) {
+    const uint32_t sz = min(32768u, bytes - off);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(static_cast<char*>(dst) + off)),
+        "l"(static_cast<const char*>(src) + off), "r"(sz), "r"(smem_u32(bar))
+        : "memory");
+  }
+}
+
 #ifndef SSB_PF_AHEAD
 #define SSB_PF_AHEAD 1  // in-loop prefetch distance, in 2 KB loop iterations (A/B: 1 best)
 #endif
@@ -297,7 +327,10 @@ __device__ __align__(16) int32_t g_pad_column[32] = {
     -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
     -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
-constexpr int32_t kWarpUnitCols = 16;  // units at least this long use the warp-wide sweep
+#ifndef SSB_WARP_UNIT_COLS
+#define SSB_WARP_UNIT_COLS 16
+#endif
+constexpr int32_t kWarpUnitCols = SSB_WARP_UNIT_COLS;  // units at least this long use the warp-wide sweep
 
 // Completes one work unit; called by all 32 lanes, `valid` per 8-lane group.
 // m = the unit's 32-row hit mask, best[q] = last hit of row 4·lg+q (sel-max).
@@ -541,6 +574,14 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   extern __shared__ uint4 smem_v4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem_v4);
   uint32_t* summ = sm + 4 + a.PW;
+  __shared__ __align__(8) unsigned long long stage_bar_storage;
+  unsigned long long* stage_bar = &stage_bar_storage;
+  uint32_t stage_phase = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(stage_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   __shared__ unsigned long long blk[6];  // stats slots 0-4 and 6
 
   cg::grid_group grid = cg::this_grid();
@@ -565,19 +606,27 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     uint32_t* Sx = ((k + 1) % 3) == 0 ? a.S0 : (((k + 1) % 3) == 1 ? a.S1 : a.S2);
 
     // -- stage the frontier prefix and the summary into shared memory -------
+    // One thread issues TMA bulk copies (global -> shared, completion on an
+    // mbarrier); everyone else goes on to the per-iteration setup and then
+    // waits on the barrier's phase.
     {
-      const uint4* src = reinterpret_cast<const uint4*>(Fc);
-      uint4* dst = smem_v4 + 1;  // words [4, 4 + PW)
-      if (threadIdx.x == 0) smem_v4[0] = make_uint4(0u, 0u, 0u, 0u);
-      for (int i = threadIdx.x; i < (a.PW >> 2); i += kThreads) dst[i] = src[i];
-      const uint4* ssrc = reinterpret_cast<const uint4*>(Sc);
-      uint4* sdst = reinterpret_cast<uint4*>(summ);
-      for (int i = threadIdx.x; i < (a.SW >> 2); i += kThreads) sdst[i] = ssrc[i];
+      if (threadIdx.x == 0) {
+        smem_v4[0] = make_uint4(0u, 0u, 0u, 0u);
+        // prior generic accesses (reads of the previous image, other CTAs'
+        // frontier stores ordered by grid.sync) before the async-proxy copies
+        asm volatile("fence.proxy.async;" ::: "memory");
+        const uint32_t bytes_p = uint32_t(a.PW) * 4u, bytes_s = uint32_t(a.SW) * 4u;
+        mbar_arrive_expect_tx(stage_bar, bytes_p + bytes_s);
+        bulk_g2s(sm + 4, Fc, bytes_p, stage_bar);
+        bulk_g2s(summ, Sc, bytes_s, stage_bar);
+      }
       // clear the summary buffer of iteration k+1 (last read at k-1)
       for (int i = blockIdx.x * kThreads + threadIdx.x; i < a.SW; i += gridDim.x * kThreads)
         Sx[i] = 0u;
       if (threadIdx.x < 6) blk[threadIdx.x] = 0ull;
     }
+    mbar_wait(stage_bar, stage_phase);
+    stage_phase ^= 1u;
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
 
@@ -596,10 +645,17 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     const bool dense = front_in > a.dense_thr;
     auto run_tasks = [&](auto early_tag) {
     constexpr bool kEarly = decltype(early_tag)::value;
+    // each warp's first task is its global warp id; the rest come from the
+    // atomic counter (late iterations with few tasks then cost no atomics)
+    const int32_t n_warps = int32_t(gridDim.x) * (kThreads / 32);
+    int32_t t_first = int32_t(blockIdx.x) * (kThreads / 32) + int32_t(threadIdx.x >> 5);
     for (;;) {
-      int32_t t = 0;
-      if (lane == 0) t = int32_t(atomicAdd(&a.task_ctr[rec], 1u));
-      t = __shfl_sync(0xffffffffu, t, 0);
+      int32_t t = t_first;
+      if (t < 0) {
+        if (lane == 0) t = int32_t(atomicAdd(&a.task_ctr[rec], 1u)) + n_warps;
+        t = __shfl_sync(0xffffffffu, t, 0);
+      }
+      t_first = -1;
       if (t >= n_in) break;
       if (k > 1) t = list_in[t];
       const int32_t ub = a.task_begin[t], ue = a.task_begin[t + 1];
