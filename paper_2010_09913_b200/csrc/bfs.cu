@@ -201,12 +201,10 @@ struct Args32 {
 // 2^S and x - (x >> S) is monotone, so the min picks the right branch) — so
 // every probe is the same shared load; only a set summary bit needs the exact
 // word from global memory (L2-resident).
-#ifndef SSB_SUMMARY_SHIFT
-#define SSB_SUMMARY_SHIFT 8
-#endif
-constexpr int kSummaryShift = SSB_SUMMARY_SHIFT;  // 2^S vertices per summary bit
-constexpr int kSummaryWordShift = kSummaryShift - 5;
-
+// S is chosen per graph (geometry32): 8 when the prefix holds most cell
+// targets (hub-heavy graphs), 6 — a 4x finer summary at the cost of prefix —
+// when it does not (low-skew graphs such as Erdős–Rényi).
+template <int kS>
 struct Probe {
   const uint32_t* sm;  // word 0 = first prefix word; sm[-4..-1] are zero
   const uint32_t* Fc;  // the full frontier in global memory
@@ -215,7 +213,7 @@ struct Probe {
 
   // the probe's word rotated so that its bit sits at bit 0
   __device__ __forceinline__ uint32_t vrot(int32_t c) const {
-    const int32_t v = min(c, (c >> kSummaryShift) + Pt);
+    const int32_t v = min(c, (c >> kS) + Pt);
     const uint32_t word = sm[v >> 5];
     return __funnelshift_r(word, word, v);  // bit (v mod 32) -> bit 0
   }
@@ -228,7 +226,7 @@ struct Probe {
     int32_t v[4];
     uint32_t w[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = min(c[q], (c[q] >> kSummaryShift) + Pt);
+    for (int q = 0; q < 4; ++q) v[q] = min(c[q], (c[q] >> kS) + Pt);
     const uint32_t base = uint32_t(__cvta_generic_to_shared(sm));
     asm volatile(
         "ld.shared.u32 %0, [%4];\n\t"
@@ -276,7 +274,7 @@ struct Probe {
 // column is probed in ascending order and sel-max keeps the LAST hit — the
 // cheapest instruction stream. kEarly = true (dense frontiers, where the exact
 // lookups dominate): decided rows are masked out as described above.
-template <bool kSelMax, bool kEarly>
+template <bool kSelMax, bool kEarly, class Probe>
 __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32_t& hit,
                                            int32_t (&best)[4]) {
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
@@ -409,7 +407,7 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
 // stop the unit once all 32 rows are decided (the semiring "plus" has
 // short-circuited for every row, so the remaining columns cannot change the
 // result). Returns the number of columns swept.
-template <bool kSelMax, bool kEarly>
+template <bool kSelMax, bool kEarly, class Probe>
 __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int lane, int lg,
                                            const Probe& pr, uint64_t pol, uint32_t& hit,
                                            int32_t (&best)[4]) {
@@ -538,7 +536,7 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
 // unit read a padding column. Loads run 4 columns ahead of the probes.
 // Early-exit sweeps stop once every row of the four units is decided. Returns
 // the number of column steps run (the group's unit swept min(len, that)).
-template <bool kSelMax, bool kEarly>
+template <bool kSelMax, bool kEarly, class Probe>
 __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int64_t stride,
                                             int32_t maxlen, const Probe& pr, uint64_t pol,
                                             uint32_t& hit, int32_t (&best)[4]) {
@@ -569,7 +567,7 @@ __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int
   return min(j, maxlen);
 }
 
-template <bool kSelMax>
+template <bool kSelMax, int kS>
 __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   extern __shared__ uint4 smem_v4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem_v4);
@@ -632,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0, c_swept = 0;
-    const Probe pr{sm + 4, Fc, a.PW * 32, a.PW * 32 - ((a.PW * 32) >> kSummaryShift)};
+    const Probe<kS> pr{sm + 4, Fc, a.PW * 32, a.PW * 32 - ((a.PW * 32) >> kS)};
 
     // Active task list: iteration 1 walks every task; later iterations only the
     // tasks kept by the previous one. A task whose units were all skipped in
@@ -1006,15 +1004,24 @@ __global__ void reached_degree_kernel(const uint32_t* __restrict__ visited,
 struct Geometry {
   int64_t NW = 0;  // bitmap words
   int32_t PW = 0, SW = 0, gshift = 0;
+  int32_t S = 8;  // log2 vertices per summary bit (Probe<kS>)
   size_t smem = 0;
 };
 
-Geometry geometry32(const ssb_graph& g) {
+// Summary granularities the kernel is instantiated for.
+using Bfs32Fn = void (*)(const Args32);
+Bfs32Fn bfs32_fn(bool sel, int S) {
+  if (S == 6) return sel ? bfs32_kernel<true, 6> : bfs32_kernel<false, 6>;
+  return sel ? bfs32_kernel<true, 8> : bfs32_kernel<false, 8>;
+}
+
+Geometry geometry32_for(const ssb_graph& g, int S) {
   Geometry G;
   G.NW = (g.n_padded + 31) / 32;
   const int64_t budget_words = int64_t(env_int("SSB_SMEM_KB", 200)) * 1024 / 4 - 4;
   const int64_t nw4 = (G.NW + 3) & ~int64_t(3);
-  G.gshift = kSummaryWordShift;  // summary bit = 2^gshift frontier words
+  G.S = S;
+  G.gshift = S - 5;  // summary bit = 2^gshift frontier words
   if (nw4 <= budget_words) {
     G.PW = int32_t(nw4);
     G.SW = 0;
@@ -1028,6 +1035,26 @@ Geometry geometry32(const ssb_graph& g) {
   }
   G.smem = size_t(4 + G.PW + G.SW) * 4;  // + 4 zero words for padding cells
   return G;
+}
+
+// The prefix's share of the cells' targets: vertex v is the target of deg(v)
+// cells and a chunk's rows have degree <= cl, so the cells of the first PW
+// chunks estimate it (exactly the cells of those rows' chunks for σ = n).
+double prefix_coverage(const ssb_graph& g, int64_t PW) {
+  if (g.n_cells <= 0) return 1.0;
+  int64_t c = 0;
+  for (int64_t i = 0; i < std::min<int64_t>(PW, g.n_chunks); ++i) c += int64_t(g.cl_host[size_t(i)]) * 32;
+  return double(c) / double(g.n_cells);
+}
+
+Geometry geometry32(const ssb_graph& g) {
+  const int forced = env_int("SSB_SUMMARY_SHIFT", 0);
+  if (forced == 6 || forced == 8) return geometry32_for(g, forced);
+  Geometry G8 = geometry32_for(g, 8);
+  // hub-heavy: the prefix catches most probes, keep it large; otherwise most
+  // probes fall in the tail, where a finer summary saves exact lookups
+  if (G8.SW == 0 || prefix_coverage(g, G8.PW) >= 0.5) return G8;
+  return geometry32_for(g, 6);
 }
 
 // Work units + tasks for the C=32 engine. A unit is a SlimChunk segment of at
@@ -1139,17 +1166,15 @@ void collect_stats(const std::vector<int64_t>& rec, int64_t k0, int64_t count,
   }
 }
 
-template <bool kSel>
-void configure32(size_t dyn_smem) {
+void configure32(Bfs32Fn fn, size_t dyn_smem) {
   int dev = 0, optin = 0;
   SSB_CUDA(cudaGetDevice(&dev));
   SSB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   cudaFuncAttributes fa;
-  SSB_CUDA(cudaFuncGetAttributes(&fa, bfs32_kernel<kSel>));
+  SSB_CUDA(cudaFuncGetAttributes(&fa, fn));
   if (dyn_smem + fa.sharedSizeBytes > size_t(optin))
     fail(SSB_EINVAL, "frontier staging exceeds shared memory (SSB_SMEM_KB too large)");
-  SSB_CUDA(cudaFuncSetAttribute(bfs32_kernel<kSel>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(dyn_smem)));
+  SSB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn_smem)));
 }
 
 // One C=32 BFS in flight: the kernel arguments and the host-side carry between
@@ -1200,11 +1225,10 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   SSB_CUDA(cudaGetLastError());
   g.last_launches += 1;  // set_root_kernel
 
-  if (r.sel) configure32<true>(G.smem); else configure32<false>(G.smem);
+  configure32(bfs32_fn(r.sel, G.S), G.smem);
   int per_sm = 0;
   SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, r.sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>,
-      kThreads, G.smem));
+      &per_sm, (const void*)bfs32_fn(r.sel, G.S), kThreads, G.smem));
   if (per_sm < 1) fail(SSB_ECUDA, "bfs32 kernel does not fit on an SM");
   r.grid = num_sms();
 
@@ -1281,7 +1305,7 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
   void* params[] = {&a};
   SSB_CUDA(cudaEventRecord(g.sc.e0, s));
   SSB_CUDA(cudaLaunchCooperativeKernel(
-      r.sel ? (const void*)bfs32_kernel<true> : (const void*)bfs32_kernel<false>, dim3(r.grid),
+      (const void*)bfs32_fn(r.sel, r.G.S), dim3(r.grid),
       dim3(kThreads), params, r.G.smem, s));
   SSB_CUDA(cudaGetLastError());
   SSB_CUDA(cudaEventRecord(g.sc.e1, s));

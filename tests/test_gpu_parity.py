@@ -289,6 +289,8 @@ def test_errors(ssb):
     {"SSB_DENSE_DIV": "1000000000"},   # always the sparse sweep
     {"SSB_DENSE_DIV": "1"},            # early-exit sweeps whenever |F| > 1
     {"SSB_DENSE_DIV": "4096"},         # the default switch point
+    {"SSB_DENSE_DIV": "1000000000", "SSB_SUMMARY_SHIFT": "6"},  # 64-vertex summary, sparse
+    {"SSB_DENSE_DIV": "1", "SSB_SUMMARY_SHIFT": "6"},           # 64-vertex summary, early exit
 ])
 def test_sweep_modes_with_small_shared_image(ssb, port, monkeypatch, mode_env):
     """Both sweep modes (sparse / early-exit) with a tiny shared-memory
@@ -352,3 +354,24 @@ def test_device_erdos_renyi_matches_oracle(ssb, port):
         assert np.array_equal(g.edges(), uv), (n, p, seed)
     with pytest.raises(ssb.InvalidArgument):
         ssb.gen_erdos_renyi(10, 1.5, 1)
+
+
+def test_erdos_renyi_bfs_matches_oracle(ssb, port, monkeypatch):
+    """A low-skew graph (config 4 shape at 2^16, with a 4 KB shared image so
+    the prefix holds few cell targets): the engine picks the fine 64-vertex
+    summary there; all semirings equal the oracle."""
+    monkeypatch.setenv("SSB_SMEM_KB", "4")
+    n = 1 << 16
+    g = ssb.gen_erdos_renyi(n, 16 / (n - 1), 5)
+    nn, uv = port.gen_erdos_renyi(n, 16 / (n - 1), 5)
+    row, col = port.to_csr(nn, uv)
+    r = ssb.build_slimsell(g, 32, n)
+    L = port.build_slimsell(n, row, col, 32, n)
+    csr = ssb.to_csr(g)
+    for root in (0, 12345):
+        for v in range(4):
+            a = ssb.bfs_spmv(r, root, opts(ssb, v, True, 64), csr)
+            b = port.bfs_spmv(L, root, v, True, 64, csr=(row, col))
+            assert np.array_equal(a.dist, b.dist), (root, v)
+            assert np.array_equal(a.parent, b.parent), (root, v)
+            assert dev_rows(a) == port_rows(b.stats), (root, v)
