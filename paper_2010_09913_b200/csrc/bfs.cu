@@ -1261,7 +1261,11 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.gone_base = 0;
   a.front_in = 1;  // F_0 = {root}
   {
-    const int div = std::max(1, env_int("SSB_DENSE_DIV", 4096));
+    // Early-exit sweeps pay off once rows get decided quickly: on hub-heavy
+    // graphs (most probes land in the shared prefix) from |F| > n/4096 on; on
+    // low-skew graphs only for dense frontiers (A/B on config 3 and config 4).
+    const bool hubby = G.S == 8;
+    const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 4096 : 16));
     a.dense_thr = std::max<int64_t>(1, g.n / div);
   }
   a.n_chunks = int32_t(g.n_chunks);
