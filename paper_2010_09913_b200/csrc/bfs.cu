@@ -300,7 +300,7 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
     need |= uint32_t(b && c[q] >= pr.P) << q;
   }
   if (__any_sync(0xffffffffu, need)) {  // warp-uniform: no reconvergence bookkeeping
-    if (kEarly) {
+    if (kEarly) {  // (A/B: the batched form does not help the sparse sweeps)
       const uint32_t e = pr.exact4(c, need);
       hit |= e;
       if (kSelMax) {
