@@ -61,6 +61,7 @@ def args_():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slimwork", action="store_true")
+    ap.add_argument("--no-validate", action="store_true")
     ap.add_argument("--shard", default="roots", choices=["roots", "chunks"],
                     help="multi-GPU decomposition: independent roots per rank (default) or "
                          "chunk-range shards with a per-iteration NCCL frontier all-gather")
@@ -195,9 +196,8 @@ def build_graph(ssb, a, log):
     r = ssb.build_slimsell(g, 32, g.num_vertices())
     t2 = time.time()
     m = g.num_edges()
-    del g
     log(f"graph S{a.scale}: n={r.n} m={m} cells={r.n_cells} gen {t1 - t0:.2f}s build {t2 - t1:.2f}s")
-    return r, m, t1 - t0, t2 - t1
+    return g, r, m, t1 - t0, t2 - t1
 
 
 def reference_repr(ssb, r, log):
@@ -274,7 +274,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    r, m, t_gen, t_build = build_graph(ssb, a, log)
+    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
     deg = r.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
     mine = roots[rank::world]
@@ -378,6 +378,31 @@ def main():
            "h2d_bytes_per_step": 8 * len(roots), "d2h_bytes_per_step": 16 * n * len(roots),
            "note": "ssb_bfs_spmv per root: root in, dist+parent int64[n] out to pinned host memory"}
 
+    # ---- Graph500-style validation of every root (device, untimed) ----------
+    validation = None
+    if not a.no_validate:
+        t0 = time.time()
+        bad, first = 0, None
+        compat = variant_id == 3  # the bench runs the reference's sel-max encoding
+        for root in mine:
+            db.run(root, opts)
+            dd, pp = db.fetch(True, pin_d, pin_p)
+            rep = ssb.validate_bfs(g, root, dd, pp if len(pp) else None, selmax_compat=compat)
+            if rep is not None:
+                bad += 1
+                first = first or f"root {root}: {rep}"
+        # the device queue BFS (independent of the SlimSell path) for the first root
+        t = ssb.bfs_traditional(g, mine[0])
+        db.run(mine[0], opts)
+        dd, _ = db.fetch(False, pin_d, pin_p)
+        validation = {"roots": len(mine), "roots_failed": bad, "first_failure": first,
+                      "checks": "ssb_validate_bfs: Graph500 edge checks + parent-tree checks "
+                                "(cli.cpp:73-112)" + (", sel-max compat parents of levels 0-1 skipped"
+                                                       if compat else ""),
+                      "dist_equal_queue_bfs_first_root": bool(np.array_equal(dd, t.dist)),
+                      "seconds": round(time.time() - t0, 2)}
+        log(f"validation: {validation}")
+
     # ---- CPU baseline: the reference library on this host, one root ---------
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -403,7 +428,7 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(max_ms, 3),
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": DATA[a.graph],
         "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor,
                    "C": 32, "sigma": "n", "semiring": a.variant, "slimwork": slimwork,
@@ -413,6 +438,7 @@ def main():
                    "l2": "inputs larger than L2 (col = %.2f GB int32 >> 126 MB)" % (4 * r.n_cells / 1e9),
                    "n": r.n, "m": m, "n_cells": r.n_cells, "iterations": len(last_stats)},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "validation": validation,
         "gpu_launches": int(launches),
         "graph500": {"harmonic_mean_gteps": round(hmean, 3), "median_gteps": round(float(np.median(teps)), 3),
                      "m_cc_first_root": mcc[mine[0]]},
@@ -450,7 +476,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
             dist.barrier()
         torch.cuda.synchronize()
 
-    r, m, t_gen, t_build = build_graph(ssb, a, log)
+    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
     deg = r.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
     ranges = partition_chunks(r.cl, 32, world)
@@ -535,7 +561,7 @@ def main_reference(a, world, rank, local, log, variant_id, slimwork, cores, work
     import paper_2010_09913_b200 as ssb
 
     ssb.set_device(local)
-    r, m, t_gen, t_build = build_graph(ssb, a, log)
+    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
     deg = r.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
     ref, rr = reference_repr(ssb, r, log)

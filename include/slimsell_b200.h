@@ -171,6 +171,26 @@ int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
 int ssb_bfs_shard_step(ssb_graph* g, ssb_iter_stats* local, uint32_t* owned_words);
 int ssb_bfs_shard_exchange(ssb_graph* g, const uint32_t* frontier_words, int64_t newly_total);
 int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent);
+/* ---- checking at scale --------------------------------
+ * bfs_traditional (bfs.hpp:83, bfs.cpp:248-286) on the device: an independent
+ * level-synchronous queue BFS over the CSR of original ids; parent = the
+ * smallest neighbour one level closer, root self-parented, unreached -1 /
+ * INT64_MAX. stats: per level {iteration, elapsed_ns, frontier_size}, as the
+ * reference fills them. ERANGE for a bad root. */
+int ssb_bfs_traditional(ssb_edges* e, int64_t root, int64_t* dist, int64_t* parent,
+                        ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations);
+/* The parent-tree checks of verify_against_oracle (cli.cpp:73-112: unreached
+ * => parent -1, root self-parented, parent a neighbour one level closer) plus
+ * the Graph500 edge checks that replace the oracle's distances (edges join
+ * levels at most 1 apart, never a reached and an unreached vertex; only the
+ * root at level 0), on the device. parent may be NULL (distances only).
+ * *violations = number of failed checks; report (NUL-terminated, up to
+ * report_cap bytes, may be NULL) lists the first few. flags:
+ * SSB_VALIDATE_SELMAX_COMPAT skips the parents of levels 0 and 1, which the
+ * reference's sel-max encoding sets to perm[root]. */
+#define SSB_VALIDATE_SELMAX_COMPAT 1
+int ssb_validate_bfs(ssb_edges* e, int64_t root, const int64_t* dist, const int64_t* parent,
+                     int flags, int64_t* violations, char* report, int64_t report_cap);
 /* m_cc of the last run: Σ_{reached v} deg(v) / 2 (the GTEPS numerator). */
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc);
 

@@ -458,5 +458,49 @@ inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& o
   return res;
 }
 
+/// bfs.hpp:86 (bfs.cpp:248-291) — the reference's queue BFS, run on the
+/// device over the graph's CSR: dist, parent = smallest neighbour one level
+/// closer (root self-parented), per_iter {iteration, elapsed_ns,
+/// frontier_size}.
+inline BfsResult bfs_traditional(const Graph& g, vid_t root) {
+  BfsResult res;
+  res.dist.resize(g.num_vertices());
+  res.parent.resize(g.num_vertices());
+  std::vector<ssb_iter_stats> st(std::min<std::int64_t>(g.num_vertices() + 2, 1 << 16));
+  std::int64_t iters = 0;
+  int rc = ssb_bfs_traditional(g.handle(), root, res.dist.data(), res.parent.data(), st.data(),
+                               static_cast<std::int64_t>(st.size()), &iters);
+  if (rc == SSB_OK && iters > static_cast<std::int64_t>(st.size())) {
+    st.resize(iters);
+    rc = ssb_bfs_traditional(g.handle(), root, res.dist.data(), res.parent.data(), st.data(),
+                             static_cast<std::int64_t>(st.size()), &iters);
+  }
+  if (rc != SSB_OK) detail::raise(rc);
+  res.iterations = iters;
+  for (std::int64_t i = 0; i < iters; ++i) {
+    IterStats s;
+    s.iteration = st[i].iteration;
+    s.elapsed_ns = st[i].elapsed_ns;
+    s.frontier_size = st[i].frontier_size;
+    res.per_iter.push_back(s);
+  }
+  return res;
+}
+
+/// cli.cpp:73-112 (verify_against_oracle's tree checks) + Graph500 edge
+/// checks, on the device. Empty optional = valid, else a diff report.
+inline std::optional<std::string> validate_bfs(const Graph& g, vid_t root, const BfsResult& run,
+                                               bool selmax_compat = false) {
+  std::int64_t bad = 0;
+  char report[1024];
+  const int rc = ssb_validate_bfs(g.handle(), root, run.dist.data(),
+                                  run.parent.empty() ? nullptr : run.parent.data(),
+                                  selmax_compat ? SSB_VALIDATE_SELMAX_COMPAT : 0, &bad, report,
+                                  static_cast<std::int64_t>(sizeof report));
+  if (rc != SSB_OK) detail::raise(rc);
+  if (bad == 0) return std::nullopt;
+  return std::to_string(bad) + " violation(s):\n" + report;
+}
+
 }  // namespace b200
 }  // namespace slimsell

@@ -341,6 +341,42 @@ def bfs_spmv(r: SlimSellRepr, root: int, opts: BfsOptions | None = None,
     return res
 
 
+def bfs_traditional(g: Graph, root: int) -> BfsResult:  # bfs.hpp:86, bfs.cpp:248-291
+    """The reference's queue BFS, on the device over the graph's CSR: parent =
+    smallest neighbour one level closer, root self-parented."""
+    n = g.num_vertices()
+    dist = np.empty(max(n, 1), np.int64)
+    parent = np.empty(max(n, 1), np.int64)
+    cap = min(n + 2, 4096)
+    st = (_L.IterStatsC * cap)()
+    it = np.zeros(1, np.int64)
+    _check(_L.lib().ssb_bfs_traditional(g._h, root, _p(dist), _p(parent), st, cap, _p(it)))
+    k = int(it[0])
+    if k > cap:
+        st = (_L.IterStatsC * k)()
+        _check(_L.lib().ssb_bfs_traditional(g._h, root, _p(dist), _p(parent), st, k, _p(it)))
+    per = [IterStats(iteration=s.iteration, elapsed_ns=s.elapsed_ns, frontier_size=s.frontier_size)
+           for s in st[:k]]
+    return BfsResult(dist[:n], parent[:n], k, per)
+
+
+def validate_bfs(g: Graph, root: int, dist, parent=None, selmax_compat: bool = False):
+    """cli.cpp:73-112 (the parent-tree checks of verify_against_oracle) plus the
+    Graph500 edge checks, on the device. Returns None when valid, else a report
+    (the first few violations) — the reference's optional<string>."""
+    dist = np.ascontiguousarray(dist, dtype=np.int64)
+    par = None if parent is None or len(parent) == 0 else np.ascontiguousarray(parent, dtype=np.int64)
+    if dist.shape[0] != g.num_vertices() or (par is not None and par.shape[0] != g.num_vertices()):
+        raise InvalidArgument("dist/parent length must equal the vertex count")
+    bad = np.zeros(1, np.int64)
+    buf = C.create_string_buffer(1024)
+    _check(_L.lib().ssb_validate_bfs(g._h, root, _p(dist), _p(par), 1 if selmax_compat else 0,
+                                     _p(bad), buf, 1024))
+    if int(bad[0]) == 0:
+        return None
+    return f"{int(bad[0])} violation(s):\n" + buf.value.decode()
+
+
 class DeviceBfs:
     """Benchmark-facing form: BFS results stay on the device (ssb_bfs_run)."""
 

@@ -262,6 +262,35 @@ int ssb_bfs_columns_swept(ssb_graph* g, int64_t* swept) {
   });
 }
 
+int ssb_bfs_traditional(ssb_edges* e, int64_t root, int64_t* dist, int64_t* parent,
+                        ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations) {
+  return guarded([&] {
+    need(e, "edges");
+    need(dist, "dist");
+    std::vector<ssb_iter_stats> st;
+    const int64_t k = ssb::bfs_traditional(*e, root, dist, parent, st);
+    if (iterations) *iterations = k;
+    if (stats)
+      for (int64_t i = 0; i < std::min<int64_t>(stats_cap, int64_t(st.size())); ++i) stats[i] = st[size_t(i)];
+  });
+}
+
+int ssb_validate_bfs(ssb_edges* e, int64_t root, const int64_t* dist, const int64_t* parent,
+                     int flags, int64_t* violations, char* report, int64_t report_cap) {
+  return guarded([&] {
+    need(e, "edges");
+    need(dist, "dist");
+    need(violations, "violations");
+    std::string text;
+    *violations = ssb::validate_bfs(*e, root, dist, parent, flags, text);
+    if (report && report_cap > 0) {
+      const size_t k = std::min<size_t>(text.size(), size_t(report_cap - 1));
+      std::memcpy(report, text.data(), k);
+      report[k] = 0;
+    }
+  });
+}
+
 int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
                         int64_t chunk_begin, int64_t chunk_end) {
   return guarded([&] {

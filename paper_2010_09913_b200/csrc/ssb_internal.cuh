@@ -96,6 +96,7 @@ struct ssb_edges {
   int64_t m = 0;
   int bits = 1;  // bits per endpoint in a key
   ssb::DevBuf<uint64_t> keys;
+  std::shared_ptr<void> csr;  // device CSR (validate.cu), built on first use
   ssb::StreamCtx sc;
 };
 
@@ -186,4 +187,9 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
 void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);
 void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total);
 void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent);
+// validate.cu
+int64_t bfs_traditional(ssb_edges& e, int64_t root, int64_t* dist, int64_t* parent,
+                        std::vector<ssb_iter_stats>& per_iter);
+int64_t validate_bfs(ssb_edges& e, int64_t root, const int64_t* dist, const int64_t* parent,
+                     int flags, std::string& report_text);
 }  // namespace ssb

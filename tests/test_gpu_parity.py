@@ -375,3 +375,55 @@ def test_erdos_renyi_bfs_matches_oracle(ssb, port, monkeypatch):
             assert np.array_equal(a.dist, b.dist), (root, v)
             assert np.array_equal(a.parent, b.parent), (root, v)
             assert dev_rows(a) == port_rows(b.stats), (root, v)
+
+
+def test_device_bfs_traditional_matches_oracle(ssb, port):
+    """The device queue BFS (bfs.cpp:248-291) equals the oracle's bfs_traditional:
+    dist, smallest-id parents and per-level frontier sizes."""
+    for make, roots in ((lambda: port.gen_kronecker(14, 16, 3), (0, 5, 4000)),
+                        (lambda: (2000, port.gen_path(2000)[1]), (0, 1999, 777)),
+                        (lambda: port.gen_erdos_renyi(3000, 0.002, 4), (1, 2999))):
+        n, uv = make()
+        g = ssb.Graph.from_pairs(uv, n)
+        row, col = port.to_csr(n, uv)
+        for root in roots:
+            a = ssb.bfs_traditional(g, root)
+            bd, bp, bk = port.bfs_traditional(n, row, col, root)
+            assert np.array_equal(a.dist, bd), root
+            assert np.array_equal(a.parent, bp), root
+            assert a.iterations == bk, root
+    with pytest.raises(ssb.OutOfRange):
+        ssb.bfs_traditional(g, -1)
+
+
+def test_device_validator(ssb, port):
+    """validate_bfs accepts correct BFS trees (device queue BFS, SpMV BFS with
+    corrected sel-max parents, compat parents with the compat flag) and reports
+    every kind of corruption."""
+    n, uv = port.gen_kronecker(14, 16, 5)
+    g = ssb.Graph.from_pairs(uv, n)
+    r = ssb.build_slimsell(g, 32, n)
+    deg = np.bincount(uv.ravel(), minlength=n)
+    deg[0] = 0  # vertex 0 sits at position 0: the sel-max quirk would be invisible
+    root = int(np.argmax(deg))
+    t = ssb.bfs_traditional(g, root)
+    assert ssb.validate_bfs(g, root, t.dist, t.parent) is None
+    s = ssb.bfs_spmv(r, root, opts(ssb, 3, True, 64, compat=False))
+    assert ssb.validate_bfs(g, root, s.dist, s.parent) is None
+    c = ssb.bfs_spmv(r, root, opts(ssb, 3, True, 64, compat=True))
+    assert ssb.validate_bfs(g, root, c.dist, c.parent, selmax_compat=True) is None
+    rep = ssb.validate_bfs(g, root, c.dist, c.parent)  # the reference's own selftest failure
+    assert rep is not None and "self-parented" in rep
+    assert ssb.validate_bfs(g, root, t.dist) is None  # distances only
+    reached = np.nonzero((t.dist != ssb.KINF) & (t.dist > 1))[0]
+    v = int(reached[0])
+    bad = t.parent.copy(); bad[v] = v
+    assert "not a neighbor" in ssb.validate_bfs(g, root, t.dist, bad)
+    d2 = t.dist.copy(); d2[v] += 2
+    assert ssb.validate_bfs(g, root, d2, None) is not None
+    un = np.nonzero(t.dist == ssb.KINF)[0]
+    if len(un):
+        p2 = t.parent.copy(); p2[int(un[0])] = root
+        assert "unreached but parent set" in ssb.validate_bfs(g, root, t.dist, p2)
+    d3 = t.dist.copy(); d3[v] = ssb.KINF
+    assert "reached and an unreached" in ssb.validate_bfs(g, root, d3, None)
