@@ -16,7 +16,7 @@
  * Status -> reference exception (bfs.hpp / repr.hpp / semiring.hpp):
  *   SSB_EINVAL -> std::invalid_argument, SSB_ERANGE -> std::out_of_range,
  *   SSB_ECAP -> BfsCapError (partial dist still written),
- *   SSB_ECUDA / SSB_ENOMEM -> std::runtime_error.
+ *   SSB_EPARSE -> ParseError, SSB_ECUDA / SSB_ENOMEM -> std::runtime_error.
  */
 #ifndef SLIMSELL_B200_H
 #define SLIMSELL_B200_H
@@ -33,6 +33,7 @@ extern "C" {
 #define SSB_ECAP 3
 #define SSB_ECUDA 4
 #define SSB_ENOMEM 5
+#define SSB_EPARSE 6 /* slimsell::ParseError (graph.hpp:15-21): "line N: ..." */
 
 #define SSB_ABI_VERSION 1
 
@@ -89,6 +90,24 @@ int ssb_gen_kronecker(int64_t scale, int64_t edgefactor, uint64_t seed,
  * libm as the reference, prefix-summed, and decoded to (u, v) on the device.
  * EINVAL for n < 0 or p outside [0, 1]. */
 int ssb_gen_erdos_renyi(int64_t n, double p, uint64_t seed, ssb_edges** out);
+/* from_edge_list (graph.hpp:50-56, graph.cpp:94-133): whitespace-separated
+ * "u v" records, '#'/'%' comment lines, an optional leading "H n m" header that
+ * pins n. SSB_REJECT_ASYMMETRIC requires the reverse of every non-loop record.
+ * The text is parsed on the host; normalisation runs on the device. */
+#define SSB_SYMMETRIZE 0
+#define SSB_REJECT_ASYMMETRIC 1
+int ssb_edges_from_edge_list(const char* text, int64_t len, int directive, ssb_edges** out);
+/* from_matrix_market (graph.hpp:58-59, graph.cpp:135-210): coordinate
+ * pattern|real, general|symmetric, square, 1-based entries. */
+int ssb_edges_from_matrix_market(const char* text, int64_t len, ssb_edges** out);
+/* The parsers alone (host only, no device work): *uv receives 2*count int64
+ * (the records before normalisation, 0-based), release it with ssb_free;
+ * *n = the declared vertex count (-1 when an edge list has no header). */
+int ssb_parse_edge_list(const char* text, int64_t len, int directive, int64_t** uv,
+                        int64_t* count, int64_t* n);
+int ssb_parse_matrix_market(const char* text, int64_t len, int64_t** uv, int64_t* count,
+                            int64_t* n);
+void ssb_free(void* p);
 /* Graph::num_vertices / num_edges (graph.hpp:42-43). */
 int ssb_edges_info(const ssb_edges* e, int64_t* n, int64_t* m);
 /* Graph::edges() (graph.hpp:44): 2*m int64, sorted (u<v) pairs. */

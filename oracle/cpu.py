@@ -311,6 +311,8 @@ class Reference:
         L.ref_gen_erdos_renyi.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.POINTER(vp)]
         L.ref_gen_named.argtypes = [C.c_int, C.c_int64, C.POINTER(vp)]
         L.ref_graph_from_pairs.argtypes = [_i64p, C.c_int64, C.c_int64, C.POINTER(vp)]
+        L.ref_from_edge_list.argtypes = [C.c_char_p, C.c_int64, C.c_int, C.POINTER(vp)]
+        L.ref_from_matrix_market.argtypes = [C.c_char_p, C.c_int64, C.POINTER(vp)]
         L.ref_graph_n.argtypes = [vp]
         L.ref_graph_n.restype = C.c_int64
         L.ref_graph_m.argtypes = [vp]
@@ -360,6 +362,12 @@ class Reference:
     def from_pairs(self, pairs, n=-1) -> RefGraph:
         uv = np.ascontiguousarray(pairs, dtype=np.int64).reshape(-1, 2)
         return self._graph(self.lib.ref_graph_from_pairs, _p(uv), uv.shape[0], n)
+
+    def from_edge_list(self, text: bytes, reject_asymmetric=False) -> RefGraph:
+        return self._graph(self.lib.ref_from_edge_list, text, len(text), int(reject_asymmetric))
+
+    def from_matrix_market(self, text: bytes) -> RefGraph:
+        return self._graph(self.lib.ref_from_matrix_market, text, len(text))
 
     def build_slimsell(self, g: RefGraph, Cc, sigma) -> RefRepr:
         h = C.c_void_p()

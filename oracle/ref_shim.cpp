@@ -28,7 +28,7 @@ using namespace slimsell;
 namespace {
 thread_local std::string g_err;
 
-enum : int { kOk = 0, kEInval = 1, kERange = 2, kECap = 3, kEOther = 4 };
+enum : int { kOk = 0, kEInval = 1, kERange = 2, kECap = 3, kEOther = 4, kEParse = 6 };
 
 template <typename F>
 int guarded(F&& f) {
@@ -41,6 +41,9 @@ int guarded(F&& f) {
   } catch (const std::out_of_range& e) {
     g_err = e.what();
     return kERange;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return kEParse;
   } catch (const std::exception& e) {
     g_err = e.what();
     return kEOther;
@@ -132,6 +135,22 @@ void ref_graph_csr(void* g, int64_t* row, int64_t* col) {
 }
 
 void ref_graph_free(void* g) { delete static_cast<RefGraph*>(g); }
+
+// graph.hpp:55-59 from_edge_list / from_matrix_market
+int ref_from_edge_list(const char* text, int64_t len, int directive, void** out) {
+  return guarded([&] {
+    *out = new RefGraph{from_edge_list(std::string_view(text, size_t(len)),
+                                       directive ? InputDirective::reject_asymmetric
+                                                 : InputDirective::symmetrize),
+                        nullptr};
+  });
+}
+
+int ref_from_matrix_market(const char* text, int64_t len, void** out) {
+  return guarded([&] {
+    *out = new RefGraph{from_matrix_market(std::string_view(text, size_t(len))), nullptr};
+  });
+}
 
 // repr.hpp:66 build_slimsell
 int ref_build_slimsell(void* g, int64_t C, int64_t sigma, void** out) {
@@ -261,6 +280,9 @@ int ref_bfs_spmv(void* r, int64_t root, int variant, int slimwork, int64_t L,
   } catch (const std::out_of_range& e) {
     g_err = e.what();
     return kERange;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return kEParse;
   } catch (const std::exception& e) {
     g_err = e.what();
     return kEOther;

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SSB_LIB", os.path.join(HERE, "libslimsell_b200.so"))  # override: experiments
 CSRC = os.path.join(HERE, "csrc")
 
-SSB_OK, SSB_EINVAL, SSB_ERANGE, SSB_ECAP, SSB_ECUDA, SSB_ENOMEM = range(6)
+SSB_OK, SSB_EINVAL, SSB_ERANGE, SSB_ECAP, SSB_ECUDA, SSB_ENOMEM, SSB_EPARSE = range(7)
 
 i64p = C.POINTER(C.c_int64)
 i32p = C.POINTER(C.c_int32)
@@ -65,6 +65,11 @@ def lib() -> C.CDLL:
         "ssb_edges_from_pairs": (C.c_int, [i64p, C.c_int64, C.c_int64, pvp]),
         "ssb_gen_kronecker": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_double), pvp]),
         "ssb_gen_erdos_renyi": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, pvp]),
+        "ssb_edges_from_edge_list": (C.c_int, [C.c_char_p, C.c_int64, C.c_int, pvp]),
+        "ssb_edges_from_matrix_market": (C.c_int, [C.c_char_p, C.c_int64, pvp]),
+        "ssb_parse_edge_list": (C.c_int, [C.c_char_p, C.c_int64, C.c_int, C.POINTER(i64p), i64p, i64p]),
+        "ssb_parse_matrix_market": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(i64p), i64p, i64p]),
+        "ssb_free": (None, [vp]),
         "ssb_edges_info": (C.c_int, [vp, i64p, i64p]),
         "ssb_edges_export": (C.c_int, [vp, i64p]),
         "ssb_to_csr": (C.c_int, [vp, i64p, i64p]),

@@ -56,6 +56,17 @@ class DeviceError(SlimSellError):
     pass
 
 
+class ParseError(SlimSellError):  # graph.hpp:15-21
+    """Malformed input text; `line` is the 1-based line of the error."""
+
+    def __init__(self, what: str):
+        super().__init__(what)
+        try:
+            self.line = int(what.split(":", 1)[0].split()[1])
+        except (IndexError, ValueError):
+            self.line = 0
+
+
 @dataclass
 class IterStats:  # bfs.hpp:26-34
     iteration: int = 0
@@ -112,6 +123,8 @@ def _raise(rc: int):
         raise InvalidArgument(msg)
     if rc == _L.SSB_ERANGE:
         raise OutOfRange(msg)
+    if rc == _L.SSB_EPARSE:
+        raise ParseError(msg)
     raise DeviceError(f"status {rc}: {msg}")
 
 
@@ -153,6 +166,20 @@ class Graph:
         _check(_L.lib().ssb_edges_from_pairs(_p(uv) if uv.size else None, uv.shape[0], n, C.byref(h)))
         return Graph(h)
 
+    @staticmethod
+    def from_edge_list(text, reject_asymmetric: bool = False) -> "Graph":  # graph.hpp:55
+        t = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        _check(_L.lib().ssb_edges_from_edge_list(t, len(t), int(reject_asymmetric), C.byref(h)))
+        return Graph(h)
+
+    @staticmethod
+    def from_matrix_market(text) -> "Graph":  # graph.hpp:59
+        t = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        _check(_L.lib().ssb_edges_from_matrix_market(t, len(t), C.byref(h)))
+        return Graph(h)
+
     def num_vertices(self) -> int:
         return self._n
 
@@ -170,6 +197,29 @@ class Graph:
         if h is not None and h.value and _L._lib is not None:
             _L._lib.ssb_edges_destroy(h)
             self._h = None
+
+
+def _parsed(fn, *args):
+    ptr, cnt, n = _L.i64p(), np.zeros(1, np.int64), np.zeros(1, np.int64)
+    _check(fn(*args, C.byref(ptr), _p(cnt), _p(n)))
+    try:
+        k = int(cnt[0])
+        uv = np.ctypeslib.as_array(ptr, shape=(max(2 * k, 1),))[: 2 * k].copy().reshape(-1, 2)
+    finally:
+        _L.lib().ssb_free(ptr)
+    return int(n[0]), uv
+
+
+def parse_edge_list(text, reject_asymmetric: bool = False):
+    """The edge-list parser alone (host only): (declared n or -1, raw records)."""
+    t = text.encode() if isinstance(text, str) else bytes(text)
+    return _parsed(_L.lib().ssb_parse_edge_list, t, len(t), int(reject_asymmetric))
+
+
+def parse_matrix_market(text):
+    """The MatrixMarket parser alone (host only): (n, 0-based records)."""
+    t = text.encode() if isinstance(text, str) else bytes(text)
+    return _parsed(_L.lib().ssb_parse_matrix_market, t, len(t))
 
 
 def gen_kronecker(scale: int, edgefactor: int, seed: int,

@@ -67,6 +67,71 @@ int ssb_gen_erdos_renyi(int64_t n, double p, uint64_t seed, ssb_edges** out) {
   });
 }
 
+namespace {
+int64_t* copy_out(const std::vector<int64_t>& v) {
+  auto* p = static_cast<int64_t*>(std::malloc(std::max<size_t>(v.size(), 1) * sizeof(int64_t)));
+  if (!p) throw std::bad_alloc();
+  if (!v.empty()) std::memcpy(p, v.data(), v.size() * sizeof(int64_t));
+  return p;
+}
+}  // namespace
+
+int ssb_parse_edge_list(const char* text, int64_t len, int directive, int64_t** uv,
+                        int64_t* count, int64_t* n) {
+  return guarded([&] {
+    need(uv, "uv");
+    need(count, "count");
+    need(n, "n");
+    if (len > 0) need(text, "text");
+    std::vector<int64_t> v;
+    ssb::parse_edge_list(std::string_view(text ? text : "", size_t(std::max<int64_t>(len, 0))),
+                         directive, v, *n);
+    *uv = copy_out(v);
+    *count = int64_t(v.size() / 2);
+  });
+}
+
+int ssb_parse_matrix_market(const char* text, int64_t len, int64_t** uv, int64_t* count,
+                            int64_t* n) {
+  return guarded([&] {
+    need(uv, "uv");
+    need(count, "count");
+    need(n, "n");
+    if (len > 0) need(text, "text");
+    std::vector<int64_t> v;
+    ssb::parse_matrix_market(std::string_view(text ? text : "", size_t(std::max<int64_t>(len, 0))),
+                             v, *n);
+    *uv = copy_out(v);
+    *count = int64_t(v.size() / 2);
+  });
+}
+
+void ssb_free(void* p) { std::free(p); }
+
+int ssb_edges_from_edge_list(const char* text, int64_t len, int directive, ssb_edges** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (len > 0) need(text, "text");
+    std::vector<int64_t> v;
+    int64_t n = -1;
+    ssb::parse_edge_list(std::string_view(text ? text : "", size_t(std::max<int64_t>(len, 0))),
+                         directive, v, n);
+    *out = ssb::edges_from_pairs(v.data(), int64_t(v.size() / 2), n);
+  });
+}
+
+int ssb_edges_from_matrix_market(const char* text, int64_t len, ssb_edges** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (len > 0) need(text, "text");
+    std::vector<int64_t> v;
+    int64_t n = 0;
+    ssb::parse_matrix_market(std::string_view(text ? text : "", size_t(std::max<int64_t>(len, 0))),
+                             v, n);
+    *out = ssb::edges_from_pairs(v.data(), int64_t(v.size() / 2), n);
+  });
+}
+
 int ssb_edges_info(const ssb_edges* e, int64_t* n, int64_t* m) {
   return guarded([&] {
     need(e, "edges");

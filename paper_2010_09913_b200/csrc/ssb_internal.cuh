@@ -9,6 +9,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "slimsell_b200.h"
@@ -187,6 +188,9 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
 void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);
 void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total);
 void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent);
+// ingest.cu
+void parse_edge_list(std::string_view text, int directive, std::vector<int64_t>& uv, int64_t& n);
+void parse_matrix_market(std::string_view text, std::vector<int64_t>& uv, int64_t& n);
 // validate.cu
 int64_t bfs_traditional(ssb_edges& e, int64_t root, int64_t* dist, int64_t* parent,
                         std::vector<ssb_iter_stats>& per_iter);

@@ -427,3 +427,29 @@ def test_device_validator(ssb, port):
         assert "unreached but parent set" in ssb.validate_bfs(g, root, t.dist, p2)
     d3 = t.dist.copy(); d3[v] = ssb.KINF
     assert "reached and an unreached" in ssb.validate_bfs(g, root, d3, None)
+
+
+def test_ingest_to_device_graph(ssb, port):
+    """Graph.from_edge_list / from_matrix_market: host parse + device
+    normalisation equal the oracle's from_pairs of the same records; errors
+    surface as the reference's exception kinds."""
+    rng = np.random.default_rng(3)
+    uv = rng.integers(0, 500, size=(3000, 2))
+    text = "H 600 3000\n" + "\n".join(f"{u} {v}" for u, v in uv) + "\n"
+    g = ssb.Graph.from_edge_list(text)
+    n, ref_uv = port.from_pairs(uv, 600)
+    assert g.num_vertices() == n == 600 and np.array_equal(g.edges(), ref_uv)
+    mm = "%%MatrixMarket matrix coordinate pattern symmetric\n500 500 3000\n" + \
+         "\n".join(f"{u + 1} {v + 1}" for u, v in uv) + "\n"
+    g2 = ssb.Graph.from_matrix_market(mm)
+    n2, ref2 = port.from_pairs(np.concatenate([uv, uv[:, ::-1]]), 500)
+    assert g2.num_vertices() == n2 and np.array_equal(g2.edges(), ref2)
+    r = ssb.build_slimsell(g2, 32, n2)
+    assert ssb.bfs_spmv(r, int(uv[0, 0]), opts(ssb, 3, True, 16)).dist[int(uv[0, 0])] == 0
+    with pytest.raises(ssb.ParseError) as e:
+        ssb.Graph.from_edge_list("0 1\n1 2 3\n")
+    assert e.value.line == 2
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.Graph.from_edge_list("0 1\n", reject_asymmetric=True)
+    with pytest.raises(ssb.OutOfRange):
+        ssb.Graph.from_edge_list("H 2 1\n0 5\n")
