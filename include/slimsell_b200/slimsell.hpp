@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <cstdlib>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -42,12 +43,28 @@ inline namespace b200 {
 // ---- graph.hpp ----------------------------------------------------------
 using vid_t = std::int64_t;
 
+/// graph.hpp:15-21 — malformed input text, with its 1-based line.
+class ParseError : public std::runtime_error {
+ public:
+  ParseError(std::int64_t line, const std::string& what_with_line)
+      : std::runtime_error(what_with_line), line_(line) {}
+  std::int64_t line() const { return line_; }
+
+ private:
+  std::int64_t line_;
+};
+
 namespace detail {
 [[noreturn]] inline void raise(int rc) {
   const std::string msg = ssb_last_error();
   switch (rc) {
     case SSB_EINVAL: throw std::invalid_argument(msg);
     case SSB_ERANGE: throw std::out_of_range(msg);
+    case SSB_EPARSE: {  // "line N: ..."
+      std::int64_t line = 0;
+      if (msg.rfind("line ", 0) == 0) line = std::strtoll(msg.c_str() + 5, nullptr, 10);
+      throw ParseError(line, msg);
+    }
     default: throw std::runtime_error("slimsell_b200: " + msg);
   }
 }
@@ -117,6 +134,29 @@ struct CsrView {
     return std::binary_search(col.begin() + row[u], col.begin() + row[u + 1], v);
   }
 };
+
+/// graph.hpp:50
+enum class InputDirective { symmetrize, reject_asymmetric };
+
+/// graph.hpp:55-56 (graph.cpp:94-133) — parsed on the host, normalised on the device.
+inline Graph from_edge_list(std::string_view text,
+                            InputDirective directive = InputDirective::symmetrize) {
+  ssb_edges* h = nullptr;
+  detail::check(ssb_edges_from_edge_list(text.data(), static_cast<std::int64_t>(text.size()),
+                                         directive == InputDirective::reject_asymmetric
+                                             ? SSB_REJECT_ASYMMETRIC
+                                             : SSB_SYMMETRIZE,
+                                         &h));
+  return Graph(h);
+}
+
+/// graph.hpp:58-59 (graph.cpp:135-210).
+inline Graph from_matrix_market(std::string_view text) {
+  ssb_edges* h = nullptr;
+  detail::check(
+      ssb_edges_from_matrix_market(text.data(), static_cast<std::int64_t>(text.size()), &h));
+  return Graph(h);
+}
 
 /// graph.hpp:71 (graph.cpp:212-232), on the device.
 inline CsrView to_csr(const Graph& g) {

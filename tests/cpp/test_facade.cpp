@@ -163,7 +163,38 @@ TEST_CASE(kronecker_matches_oracle) {
   }
 }
 
+// graph.hpp:55-59 readers, bfs.hpp:86 bfs_traditional, and the validator.
+void ingest_and_checks() {
+  Graph g = from_edge_list("# path 0-1-2-3 plus 5-6\nH 7 4\n0 1\n2 1\n3 2\n5 6\n");
+  CHECK(g.num_vertices() == 7 && g.num_edges() == 4);
+  Graph h = from_matrix_market(
+      "%%MatrixMarket matrix coordinate pattern symmetric\n7 7 4\n2 1\n3 2\n4 3\n7 6\n");
+  CHECK(h.edges() == g.edges());
+  bool threw = false;
+  try {
+    from_edge_list("0 1\n1 x\n");
+  } catch (const ParseError& e) {
+    threw = e.line() == 2;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    from_edge_list("0 1\n", InputDirective::reject_asymmetric);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  BfsResult t = bfs_traditional(g, 1);
+  CHECK(t.dist[0] == 1 && t.dist[3] == 2 && t.parent[3] == 2 && t.parent[1] == 1);
+  CHECK(t.dist[5] == kInf && t.parent[5] == kNoParent);
+  CHECK(!validate_bfs(g, 1, t).has_value());
+  BfsResult bad = t;
+  bad.parent[3] = 0;  // not a neighbour of 3
+  CHECK(validate_bfs(g, 1, bad).has_value());
+}
+
 int main() {
+  ingest_and_checks();
   csr_layout_of_path4();
   from_pairs_normalises();
   spec_layout_kats();
