@@ -177,6 +177,27 @@ def b_alg(stats, C: int, n_padded: int, swept=None) -> float:
     return 4.0 * C * cols + 3.0 * len(stats) * n_padded / 8.0 + 8.0 * n_padded
 
 
+RED_DEV = "cuda"  # device of the small reduction tensors (cpu under gloo)
+
+
+def init_dist(torch, ssb, world, local):
+    """One process per GPU (NCCL). SSB_BENCH_BACKEND=gloo runs the multi-rank
+    control flow where ranks share a GPU (functional check only)."""
+    global RED_DEV
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    ssb.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        backend = os.environ.get("SSB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+            RED_DEV = "cpu"
+    return dev
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -262,11 +283,7 @@ def main():
 
     import paper_2010_09913_b200 as ssb
 
-    torch.cuda.set_device(local)
-    ssb.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = init_dist(torch, ssb, world, local)
 
     def barrier():
         if world > 1:
@@ -326,7 +343,7 @@ def main():
     tot_edges, max_ms = my_edges, my_ms
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([float(my_edges), my_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([float(my_edges), my_ms], dtype=torch.float64, device=RED_DEV)
         e = t[:1].clone()
         dist.all_reduce(e, op=dist.ReduceOp.SUM)
         mx = t[1:].clone()
@@ -369,9 +386,9 @@ def main():
     e2e_tot, e2e_max = float(e2e_edges), e2e_s
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device=RED_DEV)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        mx = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        mx = torch.tensor([e2e_s], dtype=torch.float64, device=RED_DEV)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         e2e_tot, e2e_max = float(t.item()), float(mx.item())
     e2e = {"value": round(e2e_tot / e2e_max / 1e9, 3) if e2e_tot else None, "unit": "GTEPS",
@@ -464,11 +481,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
     import paper_2010_09913_b200 as ssb
     from paper_2010_09913_b200.sharding import DeviceShard, TorchComm, partition_chunks, run_sharded_bfs
 
-    torch.cuda.set_device(local)
-    ssb.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = init_dist(torch, ssb, world, local)
 
     def barrier():
         if world > 1:
@@ -494,7 +507,10 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
         dist_, parent_, per_iter = run_sharded_bfs([shard], comm, root, opts)
         e1.record()
         torch.cuda.synchronize()
+        launches[0] += shard.launches()
         return e0.elapsed_time(e1), per_iter
+
+    launches = [0]
 
     for _ in range(a.warmup):
         for root in roots:
@@ -504,6 +520,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
     barrier()
     sampler.start()
     step_ms = []
+    launches[0] = 0
     for s in range(a.steps):
         tot = 0.0
         for root in roots:
@@ -527,7 +544,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
     max_ms = my_ms
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([my_ms], dtype=torch.float64, device=RED_DEV)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         max_ms = float(t.item())
     value = sum(mcc.values()) / (max_ms * 1e-3) / 1e9
@@ -543,7 +560,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "chunk-sharded mode reports device time only"},
-        "clocks": clocks, "gpu_launches": None,
+        "clocks": clocks, "gpu_launches": int(launches[0]),
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
                    "build_s": round(t_build, 3)},
     }

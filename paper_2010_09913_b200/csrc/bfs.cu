@@ -1666,6 +1666,7 @@ void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_
     summary_from_words_kernel<<<grid_for(r.G.SW), 256, 0, s>>>(Fn, r.G.PW, g.n_chunks, Sn, r.G.SW,
                                                                r.G.gshift);
     SSB_CUDA(cudaGetLastError());
+    g.last_launches += 1;
   }
   r.a.front_in = newly_total;
   g.sc.sync();

@@ -312,7 +312,7 @@ int ssb_bfs_spmv(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, int64_
 int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches) {
   return guarded([&] {
     need(g, "graph");
-    if (!g->last_valid) ssb::fail(SSB_EINVAL, "no BFS result on this graph");
+    if (!g->last_valid && !g->shard) ssb::fail(SSB_EINVAL, "no BFS result on this graph");
     if (kernel_ms) *kernel_ms = g->last_kernel_ms;
     if (launches) *launches = g->last_launches;
   });

@@ -128,6 +128,17 @@ class DeviceShard:
                       st.subchunks_processed, st.columns_processed, st.frontier_size)
         return s, self.owned[: self.ce - self.cb]
 
+    def launches(self) -> int:
+        """Kernels the current/last sharded BFS launched on this rank."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        ms = C.c_double()
+        n = np.zeros(1, np.int64)
+        _check(L.lib().ssb_bfs_last_timing(self.r._h, C.byref(ms), n.ctypes.data_as(L.i64p)))
+        return int(n[0])
+
     def exchange(self, full_words, newly_total: int) -> None:
         import ctypes as C
 
@@ -163,26 +174,37 @@ class TorchComm:
     counters."""
 
     def __init__(self, ranges, group=None):
+        import torch.distributed as dist
         self.ranges = ranges
         self.group = group
         self.slot = max(1, max(e - b for b, e in ranges))
+        # gloo (functional runs with ranks sharing a GPU) exchanges host tensors
+        self.host = dist.get_backend(group) == "gloo"
 
     def allgather_frontier(self, owned_list):
         import torch
         import torch.distributed as dist
         (owned,) = owned_list
-        send = torch.zeros(self.slot, dtype=torch.int32, device=owned.device)
-        send[: owned.shape[0]] = owned
-        recv = torch.empty(self.slot * len(self.ranges), dtype=torch.int32, device=owned.device)
-        dist.all_gather_into_tensor(recv, send, group=self.group)
-        return torch.cat([recv[r * self.slot: r * self.slot + (e - b)]
-                          for r, (b, e) in enumerate(self.ranges)]).contiguous()
+        dev = "cpu" if self.host else owned.device
+        send = torch.zeros(self.slot, dtype=torch.int32, device=dev)
+        send[: owned.shape[0]] = owned.to(dev)
+        recv = torch.empty(self.slot * len(self.ranges), dtype=torch.int32, device=dev)
+        if self.host:
+            parts = list(recv.split(self.slot))
+            dist.all_gather(parts, send, group=self.group)
+        else:
+            dist.all_gather_into_tensor(recv, send, group=self.group)
+        out = torch.cat([recv[r * self.slot: r * self.slot + (e - b)]
+                         for r, (b, e) in enumerate(self.ranges)]).contiguous()
+        return out.to(owned.device)
 
     def allreduce_sum(self, arrays):
         import torch
         import torch.distributed as dist
         (a,) = arrays
-        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).cuda()
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64))
+        if not self.host:
+            t = t.cuda()
         dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
 
