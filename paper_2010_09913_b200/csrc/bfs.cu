@@ -567,6 +567,10 @@ __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int
   return min(j, maxlen);
 }
 
+#ifdef SSB_PHASES
+__device__ unsigned long long g_phase[4];  // debug: staging, tasks, barrier ns; iterations
+#endif
+
 template <bool kSelMax, int kS>
 __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   extern __shared__ uint4 smem_v4[];
@@ -596,6 +600,10 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
 
   for (int32_t k = a.k_begin; k < a.k_end; ++k) {
     const int32_t rec = k - a.k_begin;
+#ifdef SSB_PHASES
+    uint64_t ph0 = 0, ph1 = 0, ph2 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ph0 = globaltimer();
+#endif
     const uint32_t* Fc = ((k - 1) & 1) ? a.F1 : a.F0;
     uint32_t* Fn = (k & 1) ? a.F1 : a.F0;
     const int32_t km3 = (k - 1) % 3;
@@ -626,6 +634,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     mbar_wait(stage_bar, stage_phase);
     stage_phase ^= 1u;
     __syncthreads();
+#ifdef SSB_PHASES
+    if (blockIdx.x == 0 && threadIdx.x == 0) ph1 = globaltimer();
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
@@ -663,9 +674,11 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       const bool has = u < ue;
       ssb_unit U = {0, 0, 0, -1};
       uint32_t vis = 0, realm = 0;
+      int64_t ubase = 0;  // the unit's first cell in col (loaded once per task)
       bool skip = false;
       if (has) {
         U = a.units[u];
+        ubase = a.cs[U.chunk] + int64_t(U.col_begin) * 32;
         vis = a.visited[U.chunk];
         realm = U.chunk == a.n_chunks - 1 ? a.last_real : 0xffffffffu;
         skip = a.slimwork && vis == realm;  // should_skip_chunk
@@ -687,6 +700,14 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         const int32_t first = (kSelMax && kEarly) ? U.col_len - hc : 0;
         prefetch_l2(a.col + a.cs[U.chunk] + int64_t(U.col_begin + first) * 32, uint32_t(hc) * 128u);
       }
+#ifndef SSB_PF_SHORT
+#define SSB_PF_SHORT 1
+#endif
+      // short units are swept four at a time, up to eight rounds per task, each
+      // round paying a memory round trip: their whole columns (< 2 KB each) are
+      // prefetched into L2 when the task starts, so the later rounds hit L2
+      if (SSB_PF_SHORT && has && !skip && U.col_len > 0 && U.col_len < kWarpUnitCols)
+        prefetch_l2(a.col + ubase, uint32_t(U.col_len) * 128u);
       // Long units (≥ kWarpUnitCols columns) are swept by the whole warp as one
       // contiguous 128-bit stream; short ones four at a time, one per group.
       const bool is_long = has && !skip && U.col_len >= kWarpUnitCols;
@@ -709,7 +730,6 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         const int32_t sl = __ffs(longs) - 1;
         longs &= longs - 1;
         const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
-        const int32_t cb = __shfl_sync(0xffffffffu, U.col_begin, sl);
         const int32_t len = __shfl_sync(0xffffffffu, U.col_len, sl);
         const int32_t split = __shfl_sync(0xffffffffu, U.split, sl);
         const uint32_t uvis = __shfl_sync(0xffffffffu, vis, sl);
@@ -718,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         // i = 32s + l, so lg (rows) is fixed per lane and grp picks the column
         // within each 4-column step. Out-of-range indices re-read the lane's
         // own rows of the last column (idempotent).
-        const int4* base = reinterpret_cast<const int4*>(a.col + a.cs[chunk] + int64_t(cb) * 32);
+        const int4* base = reinterpret_cast<const int4*>(a.col + __shfl_sync(0xffffffffu, ubase, sl));
         // early-exit sweeps start with the rows already settled (visited or
         // padding) marked decided: their probes are skipped
         uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
@@ -744,7 +764,6 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         }
         const int32_t sl = src < 0 ? 0 : src;
         const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
-        const int32_t cb = __shfl_sync(0xffffffffu, U.col_begin, sl);
         const int32_t ulen = __shfl_sync(0xffffffffu, U.col_len, sl);  // all lanes shuffle
         const int32_t len = src < 0 ? 0 : ulen;
         const int32_t split = __shfl_sync(0xffffffffu, U.split, sl);
@@ -758,8 +777,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         // shorter than maxlen re-read their last column (idempotent for both
         // the "any" and the "last hit" reduction); groups without a unit read
         // a padding column. Loads run 4 columns ahead of the probes.
-        const int4* p = len > 0 ? reinterpret_cast<const int4*>(a.col + a.cs[chunk] +
-                                                                 int64_t(cb) * 32) + lg
+        const int64_t gbase = __shfl_sync(0xffffffffu, ubase, sl);  // all lanes shuffle
+        const int4* p = len > 0 ? reinterpret_cast<const int4*>(a.col + gbase) + lg
                                 : reinterpret_cast<const int4*>(g_pad_column) + (lg & 7);
         const int32_t jlast = len > 0 ? len - 1 : 0;
         const int64_t stride = len > 0 ? 8 : 0;
@@ -806,7 +825,19 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
                     &a.stats[rec * kStatW + (threadIdx.x < 5 ? threadIdx.x : 6)]),
                 blk[threadIdx.x]);
     if (threadIdx.x == 0 && a.trace) atomicAdd(&a.trace[2], 1);
+#ifdef SSB_PHASES
+    if (blockIdx.x == 0 && threadIdx.x == 0) ph2 = globaltimer();
+#endif
     grid.sync();
+#ifdef SSB_PHASES
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const uint64_t ph3 = globaltimer();
+      g_phase[0] += ph1 - ph0;
+      g_phase[1] += ph2 - ph1;
+      g_phase[2] += ph3 - ph2;
+      g_phase[3] += 1;
+    }
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(1, 4);
     const int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
     front_in = front;
@@ -1325,6 +1356,18 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
     }
     cudaEventDestroy(done);
   }
+#ifdef SSB_PHASES
+  {
+    unsigned long long ph[4];
+    g.sc.sync();
+    SSB_CUDA(cudaMemcpyFromSymbol(ph, g_phase, sizeof ph));
+    if (ph[3])
+      fprintf(stderr, "[ssb phases] iterations %llu: staging %.2f us, sweep %.2f us, barrier %.2f us\n",
+              ph[3], ph[0] / 1e3 / ph[3], ph[1] / 1e3 / ph[3], ph[2] / 1e3 / ph[3]);
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    SSB_CUDA(cudaMemcpyToSymbol(g_phase, z, sizeof z));
+  }
+#endif
   // the records of the first 64 iterations come back with the launch (a BFS
   // rarely needs more); the rest only when the launch got that far
   const int64_t nrec = kend - r.k;

@@ -8,6 +8,6 @@ make -s >/dev/null
 tmp=$(mktemp -d)
 nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -I../../include \
   --expt-relaxed-constexpr $defs -c bfs.cu -o $tmp/bfs.o
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" build/capi.o build/generator.o build/builder.o \
-  build/spmv.o $tmp/bfs.o -lcudart
+objs=$(ls build/*.o | grep -v '/bfs.o$')
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" $objs $tmp/bfs.o -lcudart
 rm -rf $tmp
