@@ -35,6 +35,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
+#include <mutex>
 #include <climits>
 #include <cstdlib>
 #include <memory>
@@ -920,18 +922,46 @@ __global__ void gen_sweep_kernel(ArgsG a) {
 
 // ---- shared init / epilogue kernels ---------------------------------------
 
-__global__ void set_root_kernel(uint32_t* visited, uint32_t* F0, uint32_t* S0, int32_t* level,
-                                int32_t* parent, int32_t root_pos, int32_t root_code, int32_t PW,
-                                int32_t gshift) {
-  const int32_t w = root_pos >> 5;
-  visited[w] |= 1u << (root_pos & 31);
-  F0[w] |= 1u << (root_pos & 31);
-  if (S0 && w >= PW) {
-    const int32_t gi = (w - PW) >> gshift;
-    S0[gi >> 5] |= 1u << (gi & 31);
+// init_state for the C=32 engine in ONE launch (one host call instead of five):
+// zero the 16-byte-aligned regions (visited+F0, the summaries, the stats and
+// control words), the per-task skip flags, and set the root's bits; the
+// thread that zeroes the root's words writes them with the root bit instead.
+struct ResetArgs {
+  uint4* reg[4];
+  int64_t n16[4];
+  uint8_t* tskip;
+  int64_t n_tasks;
+  uint32_t* visited;  // region 0 starts with visited, F0 follows at +NW4 words
+  int64_t NW4;
+  uint32_t* S0;       // null without a summary
+  int32_t root_pos, root_code, PW, gshift;
+  int32_t* level;
+  int32_t* parent;
+};
+
+__global__ void reset32_kernel(const ResetArgs r) {
+  const int32_t rw = r.root_pos >> 5;
+  const uint32_t rbit = 1u << (r.root_pos & 31);
+  const int32_t sgi = r.S0 && rw >= r.PW ? (rw - r.PW) >> r.gshift : -1;
+  for (int q = 0; q < 4; ++q) {
+    uint4* p = r.reg[q];
+    GRID_STRIDE(i, r.n16[q]) {
+      uint4 z = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t* zw = reinterpret_cast<uint32_t*>(&z);
+      uint32_t* base = reinterpret_cast<uint32_t*>(p + i);
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t* w = base + t;
+        if (w == r.visited + rw || w == r.visited + r.NW4 + rw) zw[t] = rbit;
+        if (sgi >= 0 && w == r.S0 + (sgi >> 5)) zw[t] = 1u << (sgi & 31);
+      }
+      p[i] = z;
+    }
   }
-  level[root_pos] = 0;
-  parent[root_pos] = root_code;
+  GRID_STRIDE(i, r.n_tasks) r.tskip[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    r.level[r.root_pos] = 0;
+    r.parent[r.root_pos] = r.root_code;
+  }
 }
 
 __global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_padded,
@@ -1224,6 +1254,7 @@ struct Run32 {
   unsigned long long* gone = nullptr;
   std::vector<int64_t> rec;
   bool stepping = false;         // shard mode: always carry state to the next launch
+  bool zeroed = false;           // stats/control words already clear for the next launch
   int64_t cb = 0, ce = 0;        // owned chunk range
 };
 
@@ -1236,7 +1267,18 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   r.sel = o.variant == SSB_SELMAX;
   r.root_pos = root_pos;
   build_plan32(g, o.slimchunk_len, cb, ce);
-  r.G = geometry32(g);
+  {
+    // the shared-memory image geometry depends on the layout and the SSB_*
+    // knobs only: computed once per graph and knob setting
+    const std::string key = std::to_string(env_int("SSB_SMEM_KB", 200)) + "/" +
+                            std::to_string(env_int("SSB_SUMMARY_SHIFT", 0));
+    auto* cached = static_cast<std::pair<std::string, Geometry>*>(g.geom.get());
+    if (!cached || cached->first != key) {
+      g.geom = std::make_shared<std::pair<std::string, Geometry>>(key, geometry32(g));
+      cached = static_cast<std::pair<std::string, Geometry>*>(g.geom.get());
+    }
+    r.G = cached->second;
+  }
   const Geometry& G = r.G;
   BitRegions R = bit_regions(g, G.SW);
   g.level.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
@@ -1248,19 +1290,61 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   r.task_out = task_ctr + kItersPerLaunch;
   r.gone = reinterpret_cast<unsigned long long*>(r.task_out + kItersPerLaunch);
 
-  SSB_CUDA(cudaMemsetAsync(R.visited, 0, size_t(R.NW4) * 4 * 2, s));  // visited + F0
-  SSB_CUDA(cudaMemsetAsync(R.S0, 0, size_t(R.SW4) * 4 * 3, s));
-  SSB_CUDA(cudaMemsetAsync(g.plan.tskip.p, 0, g.plan.tskip.bytes(), s));
-  set_root_kernel<<<1, 1, 0, s>>>(R.visited, R.F0, G.SW ? R.S0 : nullptr, g.level.p, g.parent.p,
-                                  root_pos, root_code, G.PW, G.gshift);
-  SSB_CUDA(cudaGetLastError());
-  g.last_launches += 1;  // set_root_kernel
+  {
+    ResetArgs ra{};
+    ra.reg[0] = reinterpret_cast<uint4*>(R.visited);  // visited + F0
+    ra.n16[0] = 2 * R.NW4 / 4;
+    ra.reg[1] = reinterpret_cast<uint4*>(R.S0);       // S0..S2
+    ra.n16[1] = 3 * R.SW4 / 4;
+    ra.reg[2] = reinterpret_cast<uint4*>(g.dstats.p);  // the first launch's records
+    ra.n16[2] = int64_t(g.dstats.bytes() / 16);
+    ra.reg[3] = reinterpret_cast<uint4*>(g.dctrl.p);   // and control words
+    ra.n16[3] = int64_t(g.dctrl.bytes() / 16);
+    ra.tskip = g.plan.tskip.p;
+    ra.n_tasks = int64_t(g.plan.tskip.bytes());
+    ra.visited = R.visited;
+    ra.NW4 = R.NW4;
+    ra.S0 = G.SW ? R.S0 : nullptr;
+    ra.root_pos = root_pos;
+    ra.root_code = root_code;
+    ra.PW = G.PW;
+    ra.gshift = G.gshift;
+    ra.level = g.level.p;
+    ra.parent = g.parent.p;
+    reset32_kernel<<<num_sms() * 4, 256, 0, s>>>(ra);
+    SSB_CUDA(cudaGetLastError());
+    g.last_launches += 1;  // reset32_kernel
+    r.zeroed = true;       // the first launch's stats/control words are clear
+  }
 
-  configure32(bfs32_fn(r.sel, G.S), G.smem);
-  int per_sm = 0;
-  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, (const void*)bfs32_fn(r.sel, G.S), kThreads, G.smem));
-  if (per_sm < 1) fail(SSB_ECUDA, "bfs32 kernel does not fit on an SM");
+  {
+    // The kernel's dynamic shared-memory attribute is set (and the fit
+    // checked) only when it differs from what the kernel is configured for on
+    // this device: the driver calls are host time on every BFS.
+    struct Cfg {
+      int dev;
+      Bfs32Fn fn;
+      size_t smem;
+    };
+    static std::mutex mu;
+    static std::vector<Cfg> current;
+    int dev = 0;
+    SSB_CUDA(cudaGetDevice(&dev));
+    const Bfs32Fn fn = bfs32_fn(r.sel, G.S);
+    std::lock_guard<std::mutex> lock(mu);
+    Cfg* c = nullptr;
+    for (Cfg& x : current)
+      if (x.dev == dev && x.fn == fn) c = &x;
+    if (!c || c->smem != G.smem) {
+      configure32(fn, G.smem);
+      int per_sm = 0;
+      SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads,
+                                                             G.smem));
+      if (per_sm < 1) fail(SSB_ECUDA, "bfs32 kernel does not fit on an SM");
+      if (c) c->smem = G.smem;
+      else current.push_back({dev, fn, G.smem});
+    }
+  }
   r.grid = num_sms();
 
   Args32& a = r.a;
@@ -1335,8 +1419,11 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
   Args32& a = r.a;
   a.k_begin = int32_t(r.k);
   a.k_end = int32_t(kend);
-  SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, g.dstats.bytes(), s));
-  SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
+  if (!r.zeroed) {
+    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, g.dstats.bytes(), s));
+    SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
+  }
+  r.zeroed = false;
   void* params[] = {&a};
   SSB_CUDA(cudaEventRecord(g.sc.e0, s));
   SSB_CUDA(cudaLaunchCooperativeKernel(
@@ -1422,7 +1509,11 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
 // Returns true when converged; appends per-iteration stats.
 bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
            int64_t cap, std::vector<ssb_iter_stats>& stats) {
+  const auto h0 = std::chrono::steady_clock::now();
   Run32 r = prepare32(g, root_pos, root_code, o, 0, g.n_chunks);
+  if (std::getenv("SSB_GAPS"))
+    fprintf(stderr, "[ssb gaps] host prepare32 %.1f us\n",
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
   // SSB_ITERS_PER_LAUNCH=1 (profiling): one cooperative launch per iteration
   const int64_t per = std::max(1, std::min(kItersPerLaunch, env_int("SSB_ITERS_PER_LAUNCH", kItersPerLaunch)));
   while (r.k <= cap) {
@@ -1559,6 +1650,13 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
     float ms1 = 0;
     SSB_CUDA(cudaEventElapsedTime(&ms1, t0, t1));
     if (ms <= 0.f || ms > ms1) ms = ms1;
+  }
+  if (std::getenv("SSB_GAPS") && g.C == 32) {  // debug: where the time outside the kernel goes
+    float pre = 0, post = 0;
+    SSB_CUDA(cudaEventElapsedTime(&pre, t0, g.sc.e0));
+    SSB_CUDA(cudaEventElapsedTime(&post, g.sc.e1, g.sc.e_end));
+    fprintf(stderr, "[ssb gaps] before last launch %.1f us, after it %.1f us, device %.3f ms\n",
+            pre * 1e3, post * 1e3, ms);
   }
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);

@@ -160,6 +160,7 @@ struct ssb_graph {
   int64_t last_launches = 0;  // kernels launched by the last BFS
   int64_t last_swept = 0;     // columns the last BFS actually streamed (Σ over iterations)
   std::shared_ptr<void> shard;  // state of a sharded (multi-GPU) BFS in progress
+  std::shared_ptr<void> geom;   // cached shared-memory image geometry (bfs.cu)
 
   ssb::StreamCtx sc;
 };
