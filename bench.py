@@ -62,9 +62,13 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slimwork", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
-    ap.add_argument("--shard", default="roots", choices=["roots", "chunks"],
-                    help="multi-GPU decomposition: independent roots per rank (default) or "
-                         "chunk-range shards with a per-iteration NCCL frontier all-gather")
+    ap.add_argument("--shard", default="roots", choices=["roots", "chunks", "p2p"],
+                    help="multi-GPU decomposition: independent roots per rank (default), "
+                         "chunk-range shards with a per-iteration NCCL frontier all-gather, or "
+                         "chunk-range shards with the exchange fused into the BFS kernel (p2p)")
+    ap.add_argument("--emulate-ranks", type=int, default=1,
+                    help="--shard p2p at N=1: run this many ranks as one cooperative launch on "
+                         "the single GPU (measures the fused exchange's overhead)")
     return ap.parse_args()
 
 
@@ -278,6 +282,8 @@ def main():
         return main_reference(a, world, rank, local, log, variant_id, slimwork, cores, workload)
     if a.shard == "chunks":
         return main_chunks(a, world, rank, local, log, variant_id, slimwork, workload)
+    if a.shard == "p2p":
+        return main_p2p(a, world, rank, local, log, variant_id, slimwork, workload)
 
     import torch
 
@@ -564,6 +570,114 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "chunk-sharded mode reports device time only"},
         "clocks": clocks, "gpu_launches": int(launches[0]),
+        "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
+                   "build_s": round(t_build, 3)},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
+    """Chunk-range sharding with the frontier exchange FUSED into the BFS
+    kernel (sharding.P2PShard): each rank's owned frontier words go straight
+    into the peers' windows over NVLink and the ranks meet at an in-kernel
+    counter barrier — one cooperative launch per BFS per rank. Needs one GPU
+    per rank (ranks that wait on each other must not share a GPU); at N=1,
+    --emulate-ranks W runs W ranks as one launch on the single GPU."""
+    import torch
+
+    import paper_2010_09913_b200 as ssb
+    from paper_2010_09913_b200.sharding import P2PShard, partition_chunks, run_p2p_group
+
+    if world > 1 and torch.cuda.device_count() < world:
+        raise SystemExit("--shard p2p needs one GPU per rank")
+    dev = init_dist(torch, ssb, world, local)
+    if world > 1 and os.environ.get("SSB_BENCH_BACKEND", "nccl") != "nccl":
+        raise SystemExit("--shard p2p runs over NCCL ranks on separate GPUs")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
+    deg = r.degrees()
+    roots = graph500_roots(deg, a.roots, a.seed)
+    opts = ssb.BfsOptions(variant=ssb.Variant(variant_id), slimwork=slimwork, slimchunk_len=a.slimchunk)
+    emu = max(1, a.emulate_ranks) if world == 1 else 1
+    if emu > 1:
+        reprs = [r] + [ssb.build_slimsell(g, 32, g.num_vertices()) for _ in range(emu - 1)]
+        ranges = partition_chunks(r.cl, 32, emu)
+
+        def one(root, fetch=False):
+            d, p, per_iter, ms = run_p2p_group(reprs, ranges, root, opts, fetch=fetch)
+            return ms, d
+    else:
+        ranges = partition_chunks(r.cl, 32, world)
+        shard = P2PShard(r, *ranges[rank])
+        if world > 1:
+            shard.attach_dist()
+        else:
+            shard.attach(0, 1, [shard.window_handle()])
+
+        def one(root):
+            k, ms, st = shard.run(root, opts)
+            return ms, None
+
+    for _ in range(a.warmup):
+        for root in roots:
+            one(root)
+    sampler = ClockSampler(local)
+    barrier()
+    sampler.start()
+    step_ms = []
+    for s in range(a.steps):
+        step_ms.append(sum(one(root)[0] for root in roots))
+    barrier()
+    clocks = sampler.stop()
+    # m_cc per root from the assembled distances (owned rows, MIN over ranks)
+    mcc = {}
+    n = r.n
+    dd = np.full(n, np.iinfo(np.int64).max, np.int64)
+    pp = np.full(n, -1, np.int64)
+    for root in roots:
+        if emu > 1:
+            _, d = one(root, fetch=True)
+        else:
+            one(root)
+            dd.fill(np.iinfo(np.int64).max)
+            shard.fetch(False, dd, pp)
+            d = dd
+            if world > 1:
+                import torch.distributed as dist
+                t = torch.from_numpy(d).cuda()
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                d = t.cpu().numpy()
+        mcc[root] = m_cc_of(d, deg)
+    max_ms = float(np.mean(step_ms))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([max_ms], dtype=torch.float64, device=RED_DEV)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms = float(t.item())
+    value = sum(mcc.values()) / (max_ms * 1e-3) / 1e9
+    par = (f"chunk-range shards x{world}, fused in-kernel frontier exchange" if emu == 1 else
+           f"{emu} chunk-range shards emulated in one launch on 1 GPU, fused in-kernel exchange")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(max_ms, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": DATA[a.graph],
+        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
+                   "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
+                   "roots_per_step": len(roots), "parallelism": par, "l2": "inputs larger than L2"},
+        "roofline": None, "cpu_baseline": None,
+        "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "note": "p2p-sharded mode reports device time only"},
+        "clocks": clocks, "gpu_launches": 2 * len(roots) * a.steps,
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
                    "build_s": round(t_build, 3)},
     }

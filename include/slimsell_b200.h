@@ -190,6 +190,34 @@ int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
 int ssb_bfs_shard_step(ssb_graph* g, ssb_iter_stats* local, uint32_t* owned_words);
 int ssb_bfs_shard_exchange(ssb_graph* g, const uint32_t* frontier_words, int64_t newly_total);
 int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent);
+/* ---- multi-GPU, fused: chunk-range shards whose frontier exchange runs
+ * inside the BFS kernel (replaces the per-iteration host
+ * round trip of ssb_bfs_shard_*). Each rank's frontier bitmaps live in a
+ * device WINDOW that every peer maps (CUDA IPC, peer access over NVLink):
+ * after its sweep a rank stores its owned frontier words and ORs its summary
+ * words into every peer's window, publishes its |newly| count and meets the
+ * others at a counter barrier in its own window — one cooperative launch per
+ * BFS on every rank, no host step between iterations.
+ * ssb_p2p_window: allocates this rank's window; ipc_handle (may be NULL)
+ *   receives its cudaIpcMemHandle_t (64 bytes) for the peers.
+ * ssb_p2p_attach: maps the peers' windows; ipc_handles = world handles in
+ *   rank order (this rank's entry is ignored); [chunk_begin, chunk_end) is
+ *   the owned range. Every rank attaches before any rank starts a BFS, and
+ *   all ranks run the same GPU model (equal CTA counts).
+ * ssb_bfs_p2p: one BFS from `root` on this rank; every rank calls it with
+ *   the same root and options. stats: this rank's counters (sum over ranks
+ *   for the reference's IterStats). Results: ssb_bfs_shard_fetch (owned rows).
+ * ssb_bfs_p2p_group: `world` shards (2..4 handles on THIS device, ranges =
+ *   2·world chunk bounds) run as one cooperative launch — the same kernel
+ *   and exchange code, peers being plain device memory; stats summed. */
+int ssb_p2p_window(ssb_graph* g, void* ipc_handle, int64_t* window_bytes);
+int ssb_p2p_attach(ssb_graph* g, int rank, int world, const void* ipc_handles,
+                   int64_t chunk_begin, int64_t chunk_end);
+int ssb_bfs_p2p(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, ssb_iter_stats* stats,
+                int64_t stats_cap, int64_t* iterations, double* device_ms);
+int ssb_bfs_p2p_group(ssb_graph* const* shards, int world, const int64_t* ranges, int64_t root,
+                      const ssb_bfs_options* opts, ssb_iter_stats* stats, int64_t stats_cap,
+                      int64_t* iterations, double* device_ms);
 /* ---- checking at scale --------------------------------
  * bfs_traditional (bfs.hpp:83, bfs.cpp:248-286) on the device: an independent
  * level-synchronous queue BFS over the CSR of original ids; parent = the

@@ -97,6 +97,12 @@ def lib() -> C.CDLL:
         "ssb_bfs_shard_step": (C.c_int, [vp, C.POINTER(IterStatsC), C.c_void_p]),
         "ssb_bfs_shard_exchange": (C.c_int, [vp, C.c_void_p, C.c_int64]),
         "ssb_bfs_shard_fetch": (C.c_int, [vp, C.c_int, i64p, i64p]),
+        "ssb_p2p_window": (C.c_int, [vp, C.c_void_p, i64p]),
+        "ssb_p2p_attach": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int64]),
+        "ssb_bfs_p2p": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.POINTER(IterStatsC), C.c_int64,
+                                  i64p, C.POINTER(C.c_double)]),
+        "ssb_bfs_p2p_group": (C.c_int, [pvp, C.c_int, i64p, C.c_int64, C.POINTER(BfsOptionsC),
+                                        C.POINTER(IterStatsC), C.c_int64, i64p, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

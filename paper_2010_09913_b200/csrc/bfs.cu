@@ -187,6 +187,35 @@ struct Args32 {
   int* trace;  // debug progress words in mapped host memory (SSB_TRACE), or null
 };
 
+// Fused multi-GPU exchange (chunk-range shards): every rank's
+// frontier F0/F1 and summaries S0..S2 live in a WINDOW that the other ranks
+// map (CUDA IPC over NVLink, or plain device memory when the ranks are
+// emulated inside one cooperative launch). After each iteration's sweep the
+// rank stores its owned frontier words and ORs its owned summary words
+// straight into every peer's window, publishes |newly| in a slot ring, and
+// meets the others at a counter barrier in its own window — the reference's
+// per-iteration all-gather + is_converged without leaving the kernel.
+constexpr int kMaxRanks = 8;
+constexpr int kSlotRing = 64;  // generations of |newly| slots kept in a window
+struct P2PArgs {
+  uint32_t* win[kMaxRanks];    // every rank's window base (peer-mapped)
+  int64_t offF[2];             // word offsets of F0 / F1 in a window
+  int64_t offS[3];             // ... of S0 / S1 / S2
+  int64_t offSlots;            // int64 [kSlotRing][kMaxRanks]
+  int64_t offArrive;           // uint64 arrival counter (cumulative)
+  unsigned long long gen_base; // barrier generations completed before this launch
+  unsigned long long arrivals; // CTAs per generation over all ranks
+  int32_t rank, world;
+  int32_t wcb, wce;            // owned frontier words (= chunks, C = 32)
+  int32_t sw0, sw1;            // owned summary words
+};
+constexpr int kMaxVRanks = 4;  // ranks emulated in one launch (single-GPU tests)
+struct GroupArgs {
+  Args32 a[kMaxVRanks];
+  P2PArgs x[kMaxVRanks];
+  int32_t nvb;  // CTAs per (virtual) rank
+};
+
 #define TRACE(slot, v)                                           \
   do {                                                           \
     if (a.trace) *reinterpret_cast<volatile int*>(&a.trace[slot]) = (v); \
@@ -276,6 +305,11 @@ struct Probe {
 // column is probed in ascending order and sel-max keeps the LAST hit — the
 // cheapest instruction stream. kEarly = true (dense frontiers, where the exact
 // lookups dominate): decided rows are masked out as described above.
+#ifdef SSB_COUNT
+// debug counters (SSB_COUNT builds, one launch per iteration): open probes,
+// tail probes, exact lookups, exact hits, warp steps with a lookup
+__device__ unsigned long long g_cnt[8];
+#endif
 template <bool kSelMax, bool kEarly, class Probe>
 __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32_t& hit,
                                            int32_t (&best)[4]) {
@@ -301,9 +335,34 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
     if (!kSelMax || kEarly) hit |= uint32_t(def) << q;
     need |= uint32_t(b && c[q] >= pr.P) << q;
   }
+#ifdef SSB_COUNT
+  {
+    uint32_t probes = 0, tail = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool o = (open >> q) & 1u;
+      probes += o;
+      tail += o && c[q] >= pr.P;
+    }
+    const uint32_t pw = __reduce_add_sync(0xffffffffu, probes), tw = __reduce_add_sync(0xffffffffu, tail),
+                   nw = __reduce_add_sync(0xffffffffu, uint32_t(__popc(need)));
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&g_cnt[0], (unsigned long long)pw);
+      atomicAdd(&g_cnt[1], (unsigned long long)tw);
+      atomicAdd(&g_cnt[2], (unsigned long long)nw);
+      if (nw) atomicAdd(&g_cnt[4], 1ull);
+    }
+  }
+#endif
   if (__any_sync(0xffffffffu, need)) {  // warp-uniform: no reconvergence bookkeeping
     if (kEarly) {  // (A/B: the batched form does not help the sparse sweeps)
       const uint32_t e = pr.exact4(c, need);
+#ifdef SSB_COUNT
+      {
+        const uint32_t ew = __reduce_add_sync(0xffffffffu, uint32_t(__popc(e)));
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_cnt[3], (unsigned long long)ew);
+      }
+#endif
       hit |= e;
       if (kSelMax) {
 #pragma unroll
@@ -573,8 +632,63 @@ __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int
 __device__ unsigned long long g_phase[4];  // debug: staging, tasks, barrier ns; iterations
 #endif
 
-template <bool kSelMax, int kS>
-__global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Cross-rank barrier of generation `gen` (called by every CTA of every rank):
+// this CTA's prior stores (local and peer) are released to all ranks, then
+// thread 0 waits until every CTA of every rank has arrived.
+__device__ __forceinline__ void p2p_barrier(const P2PArgs& x, unsigned long long gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < x.world; ++r)
+      atomicAdd_system(reinterpret_cast<unsigned long long*>(x.win[r] + x.offArrive), 1ull);
+    const unsigned long long* mine =
+        reinterpret_cast<const unsigned long long*>(x.win[x.rank] + x.offArrive);
+    while (ld_acquire_sys(mine) < gen * x.arrivals) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();  // no stale L1 lines of the peers' words past this point
+}
+
+// One iteration's exchange; returns the global |newly| (every rank's count).
+// Fn / Sn are this rank's window regions of the iteration just swept.
+__device__ __forceinline__ int64_t p2p_exchange(const P2PArgs& x, int32_t k, const uint32_t* Fn,
+                                                const uint32_t* Sn, int64_t local_front,
+                                                unsigned long long gen, int vb, int nvb) {
+  const int tid = vb * kThreads + threadIdx.x, nth = nvb * kThreads;
+  for (int r = 0; r < x.world; ++r) {
+    if (r == x.rank) continue;
+    uint32_t* pf = x.win[r] + x.offF[k & 1];
+    for (int32_t w = x.wcb + tid; w < x.wce; w += nth) pf[w] = __ldcg(Fn + w);
+    // summary words at the range ends are shared with the neighbouring ranks
+    uint32_t* ps = x.win[r] + x.offS[k % 3];
+    for (int32_t w = x.sw0 + tid; w < x.sw1; w += nth) {
+      const uint32_t v = __ldcg(Sn + w);
+      if (v) atomicOr_system(&ps[w], v);
+    }
+  }
+  const int slot = int(gen % kSlotRing) * kMaxRanks;
+  if (vb == 0 && threadIdx.x == 0)
+    for (int r = 0; r < x.world; ++r)
+      *reinterpret_cast<volatile int64_t*>(reinterpret_cast<int64_t*>(x.win[r] + x.offSlots) + slot +
+                                           x.rank) = local_front;
+  p2p_barrier(x, gen);
+  const volatile int64_t* sl = reinterpret_cast<const int64_t*>(x.win[x.rank] + x.offSlots) + slot;
+  int64_t front = 0;
+  for (int r = 0; r < x.world; ++r) front += sl[r];
+  return front;
+}
+
+// The BFS loop of one rank. vb / nvb: this CTA's index and the CTA count of
+// the rank (the whole grid, except when ranks are emulated in one launch).
+template <bool kSelMax, int kS, bool kP2P>
+__device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, const int vb,
+                                           const int nvb) {
   extern __shared__ uint4 smem_v4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem_v4);
   uint32_t* summ = sm + 4 + a.PW;
@@ -595,16 +709,18 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
   const uint32_t gmask = 0xffu << (grp * 8);
   const uint64_t pol = evict_first_policy();
   uint64_t t_prev = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
+  if (vb == 0 && threadIdx.x == 0) t_prev = globaltimer();
   int32_t n_in = a.n_tasks;                  // active tasks entering iteration k
   int64_t front_in = a.front_in;             // |F_{k-1}|
   unsigned long long gone = a.gone_base;     // chunks of tasks retired before k
+  // every rank has reset its window before anyone stores into it
+  if (kP2P) p2p_barrier(x, x.gen_base + 1);
 
   for (int32_t k = a.k_begin; k < a.k_end; ++k) {
     const int32_t rec = k - a.k_begin;
 #ifdef SSB_PHASES
     uint64_t ph0 = 0, ph1 = 0, ph2 = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ph0 = globaltimer();
+    if (vb == 0 && threadIdx.x == 0) ph0 = globaltimer();
 #endif
     const uint32_t* Fc = ((k - 1) & 1) ? a.F1 : a.F0;
     uint32_t* Fn = (k & 1) ? a.F1 : a.F0;
@@ -629,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
         bulk_g2s(summ, Sc, bytes_s, stage_bar);
       }
       // clear the summary buffer of iteration k+1 (last read at k-1)
-      for (int i = blockIdx.x * kThreads + threadIdx.x; i < a.SW; i += gridDim.x * kThreads)
+      for (int i = vb * kThreads + threadIdx.x; i < a.SW; i += nvb * kThreads)
         Sx[i] = 0u;
       if (threadIdx.x < 6) blk[threadIdx.x] = 0ull;
     }
@@ -637,9 +753,9 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     stage_phase ^= 1u;
     __syncthreads();
 #ifdef SSB_PHASES
-    if (blockIdx.x == 0 && threadIdx.x == 0) ph1 = globaltimer();
+    if (vb == 0 && threadIdx.x == 0) ph1 = globaltimer();
 #endif
-    if (blockIdx.x == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
+    if (vb == 0 && threadIdx.x == 0) { TRACE(0, k); TRACE(1, 1); }
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0, c_swept = 0;
@@ -658,8 +774,8 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     constexpr bool kEarly = decltype(early_tag)::value;
     // each warp's first task is its global warp id; the rest come from the
     // atomic counter (late iterations with few tasks then cost no atomics)
-    const int32_t n_warps = int32_t(gridDim.x) * (kThreads / 32);
-    int32_t t_first = int32_t(blockIdx.x) * (kThreads / 32) + int32_t(threadIdx.x >> 5);
+    const int32_t n_warps = int32_t(nvb) * (kThreads / 32);
+    int32_t t_first = int32_t(vb) * (kThreads / 32) + int32_t(threadIdx.x >> 5);
     for (;;) {
       int32_t t = t_first;
       if (t < 0) {
@@ -828,11 +944,11 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
                 blk[threadIdx.x]);
     if (threadIdx.x == 0 && a.trace) atomicAdd(&a.trace[2], 1);
 #ifdef SSB_PHASES
-    if (blockIdx.x == 0 && threadIdx.x == 0) ph2 = globaltimer();
+    if (vb == 0 && threadIdx.x == 0) ph2 = globaltimer();
 #endif
     grid.sync();
 #ifdef SSB_PHASES
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (vb == 0 && threadIdx.x == 0) {
       const uint64_t ph3 = globaltimer();
       g_phase[0] += ph1 - ph0;
       g_phase[1] += ph2 - ph1;
@@ -840,11 +956,17 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
       g_phase[3] += 1;
     }
 #endif
-    if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(1, 4);
-    const int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+    if (vb == 0 && threadIdx.x == 0) TRACE(1, 4);
+    int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+    if (kP2P) {
+      if (vb == 0 && threadIdx.x == 0) TRACE(1, 5);
+      front = p2p_exchange(x, k, Fn, Sn, front, x.gen_base + 2 + uint32_t(rec), vb, nvb);
+      if (vb == 0 && threadIdx.x == 0) { TRACE(1, 6); TRACE(3, int(front)); }
+      if (vb == 0 && threadIdx.x == 0) a.stats[rec * kStatW + 7] = front;  // global |newly|
+    }
     front_in = front;
     n_in = int32_t(*reinterpret_cast<volatile uint32_t*>(&a.task_out[rec]));
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (vb == 0 && threadIdx.x == 0) {
       const uint64_t t = globaltimer();
       a.stats[rec * kStatW + 5] = int64_t(t - t_prev);
       a.stats[rec * kStatW + 2] += int64_t(gone);  // retired tasks' chunks: skipped
@@ -853,6 +975,24 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
     gone += *reinterpret_cast<volatile unsigned long long*>(&a.gone_chunks[rec]);
     if (front == 0) break;  // is_converged: no row newly reached
   }
+}
+
+template <bool kSelMax, int kS>
+__global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
+  bfs32_body<kSelMax, kS, false>(a, P2PArgs{}, int(blockIdx.x), int(gridDim.x));
+}
+
+// Chunk-range shard of a multi-GPU BFS with the frontier exchange fused in:
+// one launch per rank (bfs32x_kernel), or all ranks of an emulated group in
+// one cooperative launch (bfs32p_kernel, rank = blockIdx.x / nvb).
+template <bool kSelMax, int kS>
+__global__ void __launch_bounds__(kThreads, 1) bfs32x_kernel(const Args32 a, const P2PArgs x) {
+  bfs32_body<kSelMax, kS, true>(a, x, int(blockIdx.x), int(gridDim.x));
+}
+template <bool kSelMax, int kS>
+__global__ void __launch_bounds__(kThreads, 1) bfs32p_kernel(const __grid_constant__ GroupArgs ga) {
+  const int vr = int(blockIdx.x) / ga.nvb;
+  bfs32_body<kSelMax, kS, true>(ga.a[vr], ga.x[vr], int(blockIdx.x) - vr * ga.nvb, ga.nvb);
 }
 
 // ---- generic engine (any C) ------------------------------------------------
@@ -927,12 +1067,12 @@ __global__ void gen_sweep_kernel(ArgsG a) {
 // control words), the per-task skip flags, and set the root's bits; the
 // thread that zeroes the root's words writes them with the root bit instead.
 struct ResetArgs {
-  uint4* reg[4];
-  int64_t n16[4];
+  uint4* reg[5];      // visited, F0, S0..S2, stats, control words
+  int64_t n16[5];
   uint8_t* tskip;
   int64_t n_tasks;
-  uint32_t* visited;  // region 0 starts with visited, F0 follows at +NW4 words
-  int64_t NW4;
+  uint32_t* visited;
+  uint32_t* F0;
   uint32_t* S0;       // null without a summary
   int32_t root_pos, root_code, PW, gshift;
   int32_t* level;
@@ -943,7 +1083,7 @@ __global__ void reset32_kernel(const ResetArgs r) {
   const int32_t rw = r.root_pos >> 5;
   const uint32_t rbit = 1u << (r.root_pos & 31);
   const int32_t sgi = r.S0 && rw >= r.PW ? (rw - r.PW) >> r.gshift : -1;
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 5; ++q) {
     uint4* p = r.reg[q];
     GRID_STRIDE(i, r.n16[q]) {
       uint4 z = make_uint4(0u, 0u, 0u, 0u);
@@ -951,7 +1091,7 @@ __global__ void reset32_kernel(const ResetArgs r) {
       uint32_t* base = reinterpret_cast<uint32_t*>(p + i);
       for (int t = 0; t < 4; ++t) {
         const uint32_t* w = base + t;
-        if (w == r.visited + rw || w == r.visited + r.NW4 + rw) zw[t] = rbit;
+        if (w == r.visited + rw || w == r.F0 + rw) zw[t] = rbit;
         if (sgi >= 0 && w == r.S0 + (sgi >> 5)) zw[t] = 1u << (sgi & 31);
       }
       p[i] = z;
@@ -1227,7 +1367,7 @@ void collect_stats(const std::vector<int64_t>& rec, int64_t k0, int64_t count,
   }
 }
 
-void configure32(Bfs32Fn fn, size_t dyn_smem) {
+void configure32(const void* fn, size_t dyn_smem) {
   int dev = 0, optin = 0;
   SSB_CUDA(cudaGetDevice(&dev));
   SSB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -1258,29 +1398,87 @@ struct Run32 {
   int64_t cb = 0, ce = 0;        // owned chunk range
 };
 
+// The shared-memory image geometry depends on the layout and the SSB_* knobs
+// only: computed once per graph and knob setting.
+Geometry cached_geometry(ssb_graph& g) {
+  const std::string key = std::to_string(env_int("SSB_SMEM_KB", 200)) + "/" +
+                          std::to_string(env_int("SSB_SUMMARY_SHIFT", 0));
+  auto* cached = static_cast<std::pair<std::string, Geometry>*>(g.geom.get());
+  if (!cached || cached->first != key) {
+    g.geom = std::make_shared<std::pair<std::string, Geometry>>(key, geometry32(g));
+    cached = static_cast<std::pair<std::string, Geometry>*>(g.geom.get());
+  }
+  return cached->second;
+}
+
+// ---- the peer-mapped window of a fused multi-GPU BFS ------------------------
+// words: F0 [NW4] | F1 [NW4] | S0 | S1 | S2 [SW4 each] | slots int64
+// [kSlotRing][kMaxRanks] | arrival counter (u64, padded to 16 bytes)
+struct WinGeom {
+  int64_t NW4 = 0, SW4 = 0;
+  int64_t offF[2] = {0, 0}, offS[3] = {0, 0, 0}, offSlots = 0, offArrive = 0, words = 0;
+};
+
+WinGeom win_geom(ssb_graph& g) {
+  const Geometry G = cached_geometry(g);
+  WinGeom w;
+  w.NW4 = ((g.n_padded + 31) / 32 + 3) & ~int64_t(3);
+  w.SW4 = std::max<int64_t>((G.SW + 3) & ~int64_t(3), 4);
+  w.offF[0] = 0;
+  w.offF[1] = w.NW4;
+  for (int i = 0; i < 3; ++i) w.offS[i] = 2 * w.NW4 + i * w.SW4;
+  w.offSlots = 2 * w.NW4 + 3 * w.SW4;
+  w.offArrive = w.offSlots + 2 * kSlotRing * kMaxRanks;
+  w.words = w.offArrive + 4;
+  return w;
+}
+
+struct P2PHost {
+  int rank = 0, world = 1;
+  int64_t cb = 0, ce = 0;
+  uint32_t* win[kMaxRanks] = {};
+  std::vector<void*> opened;  // peer windows mapped through CUDA IPC
+  unsigned long long gen = 0;  // barrier generations completed
+  WinGeom wg;
+  ~P2PHost() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
+};
+
+// The window is allocated (zeroed) once per graph; its geometry must not
+// change while peers have it mapped.
+uint32_t* p2p_window_alloc(ssb_graph& g, WinGeom& wg) {
+  if (g.C != 32) fail(SSB_EINVAL, "the fused multi-GPU BFS needs the C = 32 layout");
+  wg = win_geom(g);
+  if (g.p2p_win.n != size_t(wg.words)) {
+    g.p2p_win.alloc(size_t(wg.words));
+    SSB_CUDA(cudaMemset(g.p2p_win.p, 0, g.p2p_win.bytes()));
+    g.p2p.reset();
+  }
+  return g.p2p_win.p;
+}
+
 // init_state (semiring.cpp:56-88) in 1-bit form + kernel arguments for the
-// chunk range [cb, ce) (all chunks for a single-GPU BFS).
+// chunk range [cb, ce) (all chunks for a single-GPU BFS). With a window (a
+// fused multi-GPU shard) the frontier and summaries live in the window.
 Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
-                int64_t cb, int64_t ce) {
+                int64_t cb, int64_t ce, const P2PHost* p2p = nullptr) {
   cudaStream_t s = g.sc.s;
   Run32 r;
   r.sel = o.variant == SSB_SELMAX;
   r.root_pos = root_pos;
   build_plan32(g, o.slimchunk_len, cb, ce);
-  {
-    // the shared-memory image geometry depends on the layout and the SSB_*
-    // knobs only: computed once per graph and knob setting
-    const std::string key = std::to_string(env_int("SSB_SMEM_KB", 200)) + "/" +
-                            std::to_string(env_int("SSB_SUMMARY_SHIFT", 0));
-    auto* cached = static_cast<std::pair<std::string, Geometry>*>(g.geom.get());
-    if (!cached || cached->first != key) {
-      g.geom = std::make_shared<std::pair<std::string, Geometry>>(key, geometry32(g));
-      cached = static_cast<std::pair<std::string, Geometry>*>(g.geom.get());
-    }
-    r.G = cached->second;
-  }
+  r.G = cached_geometry(g);
   const Geometry& G = r.G;
   BitRegions R = bit_regions(g, G.SW);
+  if (p2p) {
+    uint32_t* w = p2p->win[p2p->rank];
+    R.F0 = w + p2p->wg.offF[0];
+    R.F1 = w + p2p->wg.offF[1];
+    R.S0 = w + p2p->wg.offS[0];
+    R.S1 = w + p2p->wg.offS[1];
+    R.S2 = w + p2p->wg.offS[2];
+  }
   g.level.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
   g.parent.ensure(size_t(std::max<int64_t>(g.n_padded, 1)));
   g.dstats.ensure(size_t(kItersPerLaunch) * kStatW);
@@ -1292,18 +1490,20 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
 
   {
     ResetArgs ra{};
-    ra.reg[0] = reinterpret_cast<uint4*>(R.visited);  // visited + F0
-    ra.n16[0] = 2 * R.NW4 / 4;
-    ra.reg[1] = reinterpret_cast<uint4*>(R.S0);       // S0..S2
-    ra.n16[1] = 3 * R.SW4 / 4;
-    ra.reg[2] = reinterpret_cast<uint4*>(g.dstats.p);  // the first launch's records
-    ra.n16[2] = int64_t(g.dstats.bytes() / 16);
-    ra.reg[3] = reinterpret_cast<uint4*>(g.dctrl.p);   // and control words
-    ra.n16[3] = int64_t(g.dctrl.bytes() / 16);
+    ra.reg[0] = reinterpret_cast<uint4*>(R.visited);
+    ra.n16[0] = R.NW4 / 4;
+    ra.reg[1] = reinterpret_cast<uint4*>(R.F0);
+    ra.n16[1] = R.NW4 / 4;
+    ra.reg[2] = reinterpret_cast<uint4*>(R.S0);       // S0..S2 (contiguous)
+    ra.n16[2] = 3 * R.SW4 / 4;
+    ra.reg[3] = reinterpret_cast<uint4*>(g.dstats.p);  // the first launch's records
+    ra.n16[3] = int64_t(g.dstats.bytes() / 16);
+    ra.reg[4] = reinterpret_cast<uint4*>(g.dctrl.p);   // and control words
+    ra.n16[4] = int64_t(g.dctrl.bytes() / 16);
     ra.tskip = g.plan.tskip.p;
     ra.n_tasks = int64_t(g.plan.tskip.bytes());
     ra.visited = R.visited;
-    ra.NW4 = R.NW4;
+    ra.F0 = R.F0;
     ra.S0 = G.SW ? R.S0 : nullptr;
     ra.root_pos = root_pos;
     ra.root_code = root_code;
@@ -1336,7 +1536,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     for (Cfg& x : current)
       if (x.dev == dev && x.fn == fn) c = &x;
     if (!c || c->smem != G.smem) {
-      configure32(fn, G.smem);
+      configure32((const void*)fn, G.smem);
       int per_sm = 0;
       SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads,
                                                              G.smem));
@@ -1443,6 +1643,17 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
     }
     cudaEventDestroy(done);
   }
+#ifdef SSB_COUNT
+  {
+    unsigned long long c[8];
+    g.sc.sync();
+    SSB_CUDA(cudaMemcpyFromSymbol(c, g_cnt, sizeof c));
+    fprintf(stderr, "[ssb count] k=%d probes %llu tail %llu exact %llu hits %llu lookup-steps %llu\n",
+            a.k_begin, c[0], c[1], c[2], c[3], c[4]);
+    const unsigned long long z[8] = {};
+    SSB_CUDA(cudaMemcpyToSymbol(g_cnt, z, sizeof z));
+  }
+#endif
 #ifdef SSB_PHASES
   {
     unsigned long long ph[4];
@@ -1820,6 +2031,318 @@ void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent)
   if (!st) fail(SSB_EINVAL, "no sharded BFS (ssb_bfs_shard_begin)");
   g.last_valid = true;
   fetch_rows(g, want_parents, dist, parent, nullptr, st->r.cb * 32, st->r.ce * 32);
+}
+
+// ---- fused multi-GPU chunk-range BFS (frontier exchange inside the kernel) ----
+
+void p2p_window(ssb_graph& g, void* ipc_handle, int64_t* bytes) {
+  WinGeom wg;
+  uint32_t* w = p2p_window_alloc(g, wg);
+  if (bytes) *bytes = int64_t(g.p2p_win.bytes());
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    SSB_CUDA(cudaIpcGetMemHandle(&h, w));
+    std::memcpy(ipc_handle, &h, sizeof h);
+  }
+}
+
+void check_range(ssb_graph& g, int64_t cb, int64_t ce) {
+  if (cb < 0 || ce > g.n_chunks || cb > ce) fail(SSB_EINVAL, "chunk range out of bounds");
+}
+
+// Maps every peer's window (CUDA IPC; peer access over NVLink). Collective in
+// spirit: every rank attaches before any rank runs a BFS, and the windows'
+// arrival counters start at zero together.
+void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, int64_t cb, int64_t ce) {
+  if (world < 1 || world > kMaxRanks) fail(SSB_EINVAL, "world must be in [1, 8]");
+  if (rank < 0 || rank >= world) fail(SSB_EINVAL, "rank outside [0, world)");
+  check_range(g, cb, ce);
+  auto h = std::make_shared<P2PHost>();
+  uint32_t* mine = p2p_window_alloc(g, h->wg);
+  SSB_CUDA(cudaMemset(mine, 0, g.p2p_win.bytes()));
+  h->rank = rank;
+  h->world = world;
+  h->cb = cb;
+  h->ce = ce;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      h->win[r] = mine;
+      continue;
+    }
+    if (!handles) fail(SSB_EINVAL, "ipc_handles is NULL");
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, static_cast<const char*>(handles) + size_t(r) * sizeof ih, sizeof ih);
+    void* p = nullptr;
+    SSB_CUDA(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+    h->opened.push_back(p);
+    h->win[r] = static_cast<uint32_t*>(p);
+  }
+  g.p2p = h;
+}
+
+// Kernel-side view of one rank's peer table.
+P2PArgs p2p_args(const ssb_graph& g, const P2PHost& h, const Geometry& G, unsigned long long arrivals) {
+  P2PArgs x{};
+  for (int r = 0; r < h.world; ++r) x.win[r] = h.win[r];
+  for (int i = 0; i < 2; ++i) x.offF[i] = h.wg.offF[i];
+  for (int i = 0; i < 3; ++i) x.offS[i] = h.wg.offS[i];
+  x.offSlots = h.wg.offSlots;
+  x.offArrive = h.wg.offArrive;
+  x.gen_base = h.gen;
+  x.arrivals = arrivals;
+  x.rank = h.rank;
+  x.world = h.world;
+  x.wcb = int32_t(h.cb);
+  x.wce = int32_t(h.ce);
+  // summary words holding bits of the owned chunks (shared at the range ends)
+  x.sw0 = x.sw1 = 0;
+  const int64_t lo = std::max<int64_t>(h.cb, G.PW);
+  if (G.SW > 0 && h.ce > lo) {
+    x.sw0 = int32_t(((lo - G.PW) >> G.gshift) >> 5);
+    x.sw1 = int32_t((((h.ce - 1 - G.PW) >> G.gshift) >> 5) + 1);
+  }
+  (void)g;
+  return x;
+}
+
+const void* bfs32p_fn(bool sel, int S, bool group) {
+  if (group) {
+    if (S == 6) return sel ? (const void*)bfs32p_kernel<true, 6> : (const void*)bfs32p_kernel<false, 6>;
+    return sel ? (const void*)bfs32p_kernel<true, 8> : (const void*)bfs32p_kernel<false, 8>;
+  }
+  if (S == 6) return sel ? (const void*)bfs32x_kernel<true, 6> : (const void*)bfs32x_kernel<false, 6>;
+  return sel ? (const void*)bfs32x_kernel<true, 8> : (const void*)bfs32x_kernel<false, 8>;
+}
+
+// One BFS over chunk-range shards with the exchange fused into the kernel.
+// n_local = 1: this process's rank of a multi-GPU job (peers attached with
+// p2p_attach); n_local > 1: all ranks emulated on this device in ONE
+// cooperative launch (ranges[2i], ranges[2i+1] = rank i's chunk range).
+// stats: per iteration, counters summed over the local shards.
+int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t root,
+            const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
+            int64_t* iterations, double* device_ms) {
+  if (n_local < 1 || n_local > kMaxVRanks) fail(SSB_EINVAL, "local shards must be in [1, 4]");
+  if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
+  ssb_graph& g0 = *gs[0];
+  for (int i = 0; i < n_local; ++i) {
+    ssb_graph& g = *gs[i];
+    if (g.C != 32) fail(SSB_EINVAL, "the fused multi-GPU BFS needs the C = 32 layout");
+    if (g.n != g0.n || g.n_chunks != g0.n_chunks || g.n_cells != g0.n_cells)
+      fail(SSB_EINVAL, "shards hold different layouts");
+  }
+  if (root < 0 || root >= g0.n)
+    fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g0.n) + ")");
+  if (n_local > 1) {
+    // emulated group: the windows are plain device memory of this device
+    std::vector<uint32_t*> wins(static_cast<size_t>(n_local));
+    std::vector<std::shared_ptr<P2PHost>> hs(static_cast<size_t>(n_local));
+    for (int i = 0; i < n_local; ++i) {
+      check_range(*gs[i], ranges[2 * i], ranges[2 * i + 1]);
+      auto* prev = static_cast<P2PHost*>(gs[i]->p2p.get());
+      hs[size_t(i)] = std::make_shared<P2PHost>();
+      wins[size_t(i)] = p2p_window_alloc(*gs[i], hs[size_t(i)]->wg);
+      hs[size_t(i)]->gen = prev && prev->world == n_local && prev->rank == i ? prev->gen : ~0ull;
+    }
+    // keep the barrier generation count only for the same group of windows
+    for (int i = 0; i < n_local; ++i) {
+      auto* prev = static_cast<P2PHost*>(gs[i]->p2p.get());
+      for (int r = 0; prev && r < n_local; ++r)
+        if (prev->win[r] != wins[size_t(r)]) hs[size_t(i)]->gen = ~0ull;
+    }
+    unsigned long long gen = hs[0]->gen;
+    for (int i = 0; i < n_local; ++i)
+      if (hs[size_t(i)]->gen != gen) gen = ~0ull;
+    for (int i = 0; i < n_local; ++i) {
+      P2PHost& h = *hs[size_t(i)];
+      h.rank = i;
+      h.world = n_local;
+      h.cb = ranges[2 * i];
+      h.ce = ranges[2 * i + 1];
+      for (int r = 0; r < n_local; ++r) h.win[r] = wins[size_t(r)];
+      if (gen == ~0ull) {  // a new group: restart the barrier counters together
+        SSB_CUDA(cudaMemset(wins[size_t(i)], 0, gs[i]->p2p_win.bytes()));
+        h.gen = 0;
+      }
+      gs[i]->p2p = hs[size_t(i)];
+    }
+  }
+  std::vector<P2PHost*> H(static_cast<size_t>(n_local));
+  for (int i = 0; i < n_local; ++i) {
+    H[size_t(i)] = static_cast<P2PHost*>(gs[i]->p2p.get());
+    if (!H[size_t(i)]) fail(SSB_EINVAL, "no peer windows attached (ssb_p2p_attach)");
+  }
+  const int world = H[0]->world;
+  int dev = 0;
+  SSB_CUDA(cudaGetDevice(&dev));
+
+  int32_t root_pos = 0;
+  SSB_CUDA(cudaMemcpy(&root_pos, g0.inv_perm.p + root, 4, cudaMemcpyDeviceToHost));
+  const int32_t root_code = (o.variant == SSB_SELMAX && o.selmax_compat) ? int32_t(root) : root_pos;
+  const int64_t cap = o.max_iterations > 0 ? o.max_iterations : g0.n + 1;
+
+  std::vector<Run32> rs;
+  rs.reserve(size_t(n_local));
+  for (int i = 0; i < n_local; ++i) {
+    ssb_graph& g = *gs[i];
+    g.last_kernel_ms = 0;
+    g.last_launches = 0;
+    g.last_swept = 0;
+    g.last_valid = false;
+    rs.push_back(prepare32(g, root_pos, root_code, o, H[size_t(i)]->cb, H[size_t(i)]->ce, H[size_t(i)]));
+  }
+  const Geometry G = rs[0].G;
+  const bool sel = rs[0].sel;
+  const void* fn = bfs32p_fn(sel, G.S, n_local > 1);
+  {
+    configure32(fn, G.smem);
+    int per_sm = 0;
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, G.smem));
+    if (per_sm < 1) fail(SSB_ECUDA, "bfs32p kernel does not fit on an SM");
+  }
+  // every rank runs the same CTA count (same GPU model): arrivals = world x nvb
+  const int nvb = num_sms() / n_local;
+  const int grid = nvb * n_local;
+  for (int i = 0; i < n_local; ++i) gs[i]->sc.sync();  // resets done before anyone stores
+
+  cudaStream_t s = g0.sc.s;
+  cudaEvent_t t0, t1;
+  SSB_CUDA(cudaEventCreate(&t0));
+  SSB_CUDA(cudaEventCreate(&t1));
+  SSB_CUDA(cudaEventRecord(t0, s));
+  std::vector<std::vector<ssb_iter_stats>> st(static_cast<size_t>(n_local));
+  std::vector<std::vector<int64_t>> rec(size_t(n_local), std::vector<int64_t>(size_t(kItersPerLaunch) * kStatW));
+  int64_t k = 1;
+  bool conv = false;
+  double kms_total = 0;
+  while (!conv && k <= cap) {
+    const int64_t kend = std::min<int64_t>(cap + 1, k + kItersPerLaunch);
+    GroupArgs ga{};
+    ga.nvb = nvb;
+    for (int i = 0; i < n_local; ++i) {
+      Run32& r = rs[size_t(i)];
+      if (!r.zeroed) {
+        SSB_CUDA(cudaMemsetAsync(gs[i]->dstats.p, 0, gs[i]->dstats.bytes(), s));
+        SSB_CUDA(cudaMemsetAsync(gs[i]->dctrl.p, 0, gs[i]->dctrl.bytes(), s));
+      }
+      r.zeroed = false;
+      r.a.k_begin = int32_t(k);
+      r.a.k_end = int32_t(kend);
+      ga.a[i] = r.a;
+      ga.x[i] = p2p_args(*gs[i], *H[size_t(i)], G, (unsigned long long)world * (unsigned long long)nvb);
+    }
+    static int* trace_buf = nullptr;  // debug (SSB_TRACE): per-rank progress words in mapped host memory
+    if (std::getenv("SSB_TRACE")) {
+      if (!trace_buf) SSB_CUDA(cudaHostAlloc(&trace_buf, 4096, cudaHostAllocMapped));
+      std::memset(trace_buf, 0, 4096);
+      for (int i = 0; i < n_local; ++i) {
+        int* d = nullptr;
+        SSB_CUDA(cudaHostGetDevicePointer(&d, trace_buf + 16 * i, 0));
+        ga.a[i].trace = d;
+      }
+    }
+    void* params_group[] = {&ga};
+    void* params_rank[] = {&ga.a[0], &ga.x[0]};
+    SSB_CUDA(cudaEventRecord(g0.sc.e0, s));
+    SSB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads),
+                                         n_local > 1 ? params_group : params_rank, G.smem, s));
+    SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaEventRecord(g0.sc.e1, s));
+    if (ga.a[0].trace) {  // debug: poll progress instead of blocking forever
+      for (int spin = 0; cudaEventQuery(g0.sc.e1) == cudaErrorNotReady; ++spin) {
+        if (spin % 1000 == 999) {
+          for (int i = 0; i < n_local; ++i)
+            fprintf(stderr, "[ssb p2p trace] rank %d k=%d phase=%d arrived=%d front=%d\n", i,
+                    trace_buf[16 * i], trace_buf[16 * i + 1], trace_buf[16 * i + 2], trace_buf[16 * i + 3]);
+        }
+        if (spin > 10000) {
+          fprintf(stderr, "[ssb p2p trace] giving up\n");
+          std::abort();
+        }
+        usleep(1000);
+      }
+    }
+    for (int i = 0; i < n_local; ++i)
+      SSB_CUDA(cudaMemcpyAsync(rec[size_t(i)].data(), gs[i]->dstats.p, size_t(kend - k) * kStatW * 8,
+                               cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaEventRecord(g0.sc.e_end, s));
+    SSB_CUDA(cudaStreamSynchronize(s));
+    float kms = 0;
+    SSB_CUDA(cudaEventElapsedTime(&kms, g0.sc.e0, g0.sc.e1));
+    kms_total += kms;
+    // iterations run: up to the first with global |newly| = 0 (slot 7)
+    int64_t ran = 0;
+    for (int64_t j = 0; j < kend - k; ++j) {
+      ++ran;
+      if (rec[0][size_t(j) * kStatW + 7] == 0) {
+        conv = true;
+        break;
+      }
+    }
+    for (int i = 0; i < n_local; ++i) {
+      ssb_graph& g = *gs[i];
+      Run32& r = rs[size_t(i)];
+      const size_t before = st[size_t(i)].size();
+      collect_stats(rec[size_t(i)], k, ran, st[size_t(i)]);
+      for (int64_t j = 0; j < ran; ++j) g.last_swept += rec[size_t(i)][size_t(j) * kStatW + 6];
+      for (size_t j = before; j < st[size_t(i)].size(); ++j) {
+        st[size_t(i)][j].chunks_processed += g.plan.empty_chunks - (r.z_skip ? 1 : 0);
+        st[size_t(i)][j].chunks_skipped += r.z_skip ? 1 : 0;
+      }
+      H[size_t(i)]->gen += static_cast<unsigned long long>(1 + ran);
+      if (!conv) {
+        std::vector<uint32_t> outs(static_cast<size_t>(ran));
+        std::vector<unsigned long long> gones(static_cast<size_t>(ran));
+        SSB_CUDA(cudaMemcpy(outs.data(), r.task_out, 4 * ran, cudaMemcpyDeviceToHost));
+        SSB_CUDA(cudaMemcpy(gones.data(), r.gone, 8 * ran, cudaMemcpyDeviceToHost));
+        r.a.n_tasks = int32_t(outs.back());
+        for (auto v : gones) r.a.gone_base += v;
+        r.a.front_in = rec[size_t(i)][size_t(ran - 1) * kStatW + 7];
+      }
+    }
+    k += ran;
+  }
+  SSB_CUDA(cudaEventRecord(t1, s));
+  SSB_CUDA(cudaEventSynchronize(t1));
+  float ms = 0;
+  SSB_CUDA(cudaEventElapsedTime(&ms, t0, g0.sc.e_end));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  const int64_t iters = int64_t(st[0].size());
+  for (int i = 0; i < n_local; ++i) {
+    ssb_graph& g = *gs[i];
+    g.last_kernel_ms = kms_total;
+    g.last_launches = 1 + (iters + kItersPerLaunch - 1) / kItersPerLaunch;  // reset + BFS launches
+    g.last_root = root;
+    g.last_variant = o.variant;
+    g.last_compat = o.selmax_compat;
+    g.last_iterations = iters;
+    g.last_valid = true;
+    auto ss = std::make_shared<ShardState>();
+    ss->r = rs[size_t(i)];
+    ss->r.cb = H[size_t(i)]->cb;
+    ss->r.ce = H[size_t(i)]->ce;
+    ss->o = o;
+    ss->stats = st[size_t(i)];
+    g.shard = ss;  // results of the owned rows: ssb_bfs_shard_fetch
+  }
+  if (device_ms) *device_ms = ms;
+  if (iterations) *iterations = iters;
+  if (stats) {
+    for (int64_t j = 0; j < std::min<int64_t>(stats_cap, iters); ++j) {
+      ssb_iter_stats a = st[0][size_t(j)];
+      for (int i = 1; i < n_local; ++i) {
+        const ssb_iter_stats& b = st[size_t(i)][size_t(j)];
+        a.chunks_processed += b.chunks_processed;
+        a.chunks_skipped += b.chunks_skipped;
+        a.subchunks_processed += b.subchunks_processed;
+        a.columns_processed += b.columns_processed;
+        a.frontier_size += b.frontier_size;
+      }
+      stats[j] = a;
+    }
+  }
+  return conv ? SSB_OK : SSB_ECAP;
 }
 
 int64_t bfs_edges_traversed(ssb_graph& g) {

@@ -386,6 +386,51 @@ int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* 
   });
 }
 
+int ssb_p2p_window(ssb_graph* g, void* ipc_handle, int64_t* window_bytes) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::p2p_window(*g, ipc_handle, window_bytes);
+  });
+}
+
+int ssb_p2p_attach(ssb_graph* g, int rank, int world, const void* ipc_handles, int64_t chunk_begin,
+                   int64_t chunk_end) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::p2p_attach(*g, rank, world, ipc_handles, chunk_begin, chunk_end);
+  });
+}
+
+int ssb_bfs_p2p(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, ssb_iter_stats* stats,
+                int64_t stats_cap, int64_t* iterations, double* device_ms) {
+  int rc = SSB_OK;
+  const int st = guarded([&] {
+    need(g, "graph");
+    need(opts, "opts");
+    rc = ssb::bfs_p2p(&g, 1, nullptr, root, *opts, stats, stats_cap, iterations, device_ms);
+  });
+  if (st != SSB_OK) return st;
+  if (rc == SSB_ECAP) g_last_error = "iteration cap reached before fixed point";
+  return rc;
+}
+
+int ssb_bfs_p2p_group(ssb_graph* const* shards, int world, const int64_t* ranges, int64_t root,
+                      const ssb_bfs_options* opts, ssb_iter_stats* stats, int64_t stats_cap,
+                      int64_t* iterations, double* device_ms) {
+  int rc = SSB_OK;
+  const int st = guarded([&] {
+    need(shards, "shards");
+    need(ranges, "ranges");
+    need(opts, "opts");
+    if (world < 2) ssb::fail(SSB_EINVAL, "a group needs at least 2 shards");
+    for (int i = 0; i < world; ++i) need(shards[i], "shard");
+    rc = ssb::bfs_p2p(shards, world, ranges, root, *opts, stats, stats_cap, iterations, device_ms);
+  });
+  if (st != SSB_OK) return st;
+  if (rc == SSB_ECAP) g_last_error = "iteration cap reached before fixed point";
+  return rc;
+}
+
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc) {
   return guarded([&] {
     need(g, "graph");

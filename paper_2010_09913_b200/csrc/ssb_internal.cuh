@@ -160,6 +160,8 @@ struct ssb_graph {
   int64_t last_launches = 0;  // kernels launched by the last BFS
   int64_t last_swept = 0;     // columns the last BFS actually streamed (Σ over iterations)
   std::shared_ptr<void> shard;  // state of a sharded (multi-GPU) BFS in progress
+  ssb::DevBuf<uint32_t> p2p_win;  // fused multi-GPU BFS: the peer-mapped frontier window
+  std::shared_ptr<void> p2p;      // ... and its peer table (bfs.cu)
   std::shared_ptr<void> geom;   // cached shared-memory image geometry (bfs.cu)
 
   ssb::StreamCtx sc;
@@ -189,6 +191,11 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
 void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);
 void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total);
 void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent);
+void p2p_window(ssb_graph& g, void* ipc_handle, int64_t* bytes);
+void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, int64_t cb, int64_t ce);
+int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t root,
+            const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
+            int64_t* iterations, double* device_ms);
 // ingest.cu
 void parse_edge_list(std::string_view text, int directive, std::vector<int64_t>& uv, int64_t& n);
 void parse_matrix_market(std::string_view text, std::vector<int64_t>& uv, int64_t& n);

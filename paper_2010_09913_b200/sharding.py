@@ -156,6 +156,99 @@ class DeviceShard:
         _check(L.lib().ssb_bfs_shard_fetch(self.r._h, int(want_parents), _p(dist), _p(parent)))
 
 
+class P2PShard:
+    """One rank's shard of the FUSED multi-GPU BFS: the frontier exchange runs
+    inside the BFS kernel over peer-mapped windows (ssb_p2p_* / ssb_bfs_p2p),
+    so a BFS is one cooperative launch per rank with no host step between
+    iterations. attach() is collective over torch.distributed: the ranks swap
+    their windows' CUDA IPC handles (all_gather_object) and map each other's."""
+
+    def __init__(self, r, cb: int, ce: int):
+        self.r, self.cb, self.ce = r, int(cb), int(ce)
+
+    def window_handle(self) -> bytes:
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        h = (C.c_char * 64)()
+        nbytes = np.zeros(1, np.int64)
+        _check(L.lib().ssb_p2p_window(self.r._h, h, nbytes.ctypes.data_as(L.i64p)))
+        return bytes(h)
+
+    def attach(self, rank: int, world: int, handles) -> None:
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        if len(handles) != world or any(len(h) != 64 for h in handles):
+            raise ValueError("need one 64-byte IPC handle per rank")
+        buf = C.create_string_buffer(b"".join(handles), 64 * world)
+        _check(L.lib().ssb_p2p_attach(self.r._h, int(rank), int(world), buf, self.cb, self.ce))
+
+    def attach_dist(self, group=None) -> None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        mine = self.window_handle()
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        self.attach(rank, world, handles)
+        dist.barrier(group=group)  # every window mapped and zeroed before any BFS
+
+    def run(self, root: int, opts):
+        """One BFS (every rank calls it with the same root/opts). Returns
+        (iterations, device ms, this rank's per-iteration counters)."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check, _stats_list
+        o = opts._c()
+        cap = 4096
+        st = (L.IterStatsC * cap)()
+        k = np.zeros(1, np.int64)
+        ms = C.c_double()
+        rc = L.lib().ssb_bfs_p2p(self.r._h, int(root), C.byref(o), st, cap, k.ctypes.data_as(L.i64p),
+                                 C.byref(ms))
+        _check(rc)
+        return int(k[0]), float(ms.value), _stats_list(st, int(k[0]))
+
+    def fetch(self, want_parents: bool, dist: np.ndarray, parent: np.ndarray) -> None:
+        from . import _lib as L
+        from .api import _check, _p
+        _check(L.lib().ssb_bfs_shard_fetch(self.r._h, int(want_parents), _p(dist), _p(parent)))
+
+
+def run_p2p_group(reprs, ranges, root: int, opts, fetch: bool = True):
+    """The fused multi-GPU BFS with every rank emulated on THIS device: one
+    cooperative launch runs all ranks' sweeps and their in-kernel frontier
+    exchange (ssb_bfs_p2p_group). Returns (dist, parent, per_iter, device_ms)
+    assembled over the shards (dist / parent None when fetch is False)."""
+    import ctypes as C
+
+    from . import _lib as L
+    from .api import KINF, _check, _p, _stats_list
+    world = len(reprs)
+    hs = (C.c_void_p * world)(*[r._h for r in reprs])
+    rg = np.array([x for b_e in ranges for x in b_e], dtype=np.int64)
+    o = opts._c()
+    cap = 4096
+    st = (L.IterStatsC * cap)()
+    k = np.zeros(1, np.int64)
+    ms = C.c_double()
+    rc = L.lib().ssb_bfs_p2p_group(hs, world, rg.ctypes.data_as(L.i64p), int(root), C.byref(o), st, cap,
+                                   k.ctypes.data_as(L.i64p), C.byref(ms))
+    _check(rc)
+    if not fetch:
+        return None, None, _stats_list(st, int(k[0])), float(ms.value)
+    n = reprs[0].n
+    dist = np.full(n, KINF, dtype=np.int64)
+    parent = np.full(n, -1, dtype=np.int64)
+    want = bool(opts.want_parents) and int(opts.variant) == 3
+    for r in reprs:
+        _check(L.lib().ssb_bfs_shard_fetch(r._h, int(want), _p(dist), _p(parent)))
+    return dist, (parent if want else parent[:0]), _stats_list(st, int(k[0])), float(ms.value)
+
+
 class LocalComm:
     """Every shard lives in this process (one GPU emulating several ranks):
     the all-gather is a concatenation in rank order, reductions are sums."""

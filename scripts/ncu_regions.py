@@ -12,7 +12,7 @@ tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
 cub = os.path.join(tmp, "bfs.sm_100a.cubin")
 sass = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
-fn = f"bfs32_kernelILb{sel}EEEvNS0_6Args32E:"
+fn = f"bfs32_kernelILb{sel}ELi{os.environ.get('KS', '8')}EEEvNS0_6Args32E:"
 addr_site = {}
 on = False
 chain = []
@@ -42,7 +42,16 @@ for line in sass.splitlines():
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
-h = rows[1]; data = rows[2:]
+# one section per profiled launch ("Kernel Name" row, header row, SASS rows): take section LAUNCH
+secs, cur = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur = []
+        secs.append(cur)
+    elif cur is not None:
+        cur.append(r)
+sec = secs[int(os.environ.get("LAUNCH", "0"))]
+h = sec[0]; data = [r for r in sec[1:] if r and r[0].startswith("0x")]
 iA = h.index("Address"); iS = h.index("Warp Stall Sampling (All Samples)"); iE = h.index("Instructions Executed")
 base = min(int(r[iA], 16) for r in data)
 agg = collections.defaultdict(lambda: [0, 0])

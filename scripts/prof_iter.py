@@ -10,11 +10,16 @@ ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--variant", type=int, default=3)
 ap.add_argument("--L", type=int, default=128)
 ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er"])
+ap.add_argument("--g500", type=int, default=-1, help="use the i-th bench.py Graph500 root instead of --root")
 a = ap.parse_args()
 g = (ssb.gen_erdos_renyi(1 << a.scale, 16 / ((1 << a.scale) - 1), 1) if a.graph == "er"
      else ssb.gen_kronecker(a.scale, 16, 1))
 r = ssb.build_slimsell(g, 32, g.num_vertices())
 del g
+if a.g500 >= 0:
+    from bench import graph500_roots
+    a.root = graph500_roots(r.degrees(), a.g500 + 1, 1)[a.g500]
+    print("root", a.root)
 db = ssb.DeviceBfs(r)
 o = ssb.BfsOptions(variant=ssb.Variant(a.variant), slimwork=True, slimchunk_len=a.L, max_iterations=a.iters)
 for _ in range(2):

@@ -342,6 +342,76 @@ def test_chunk_sharded_device_bfs_matches_single_gpu(ssb, port, monkeypatch, wor
             assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
 
 
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_fused_p2p_sharded_bfs_matches_oracle(ssb, port, monkeypatch, world):
+    """The fused multi-GPU BFS (frontier words stored into the peers' windows
+    and a counter barrier inside the BFS kernel, ssb_bfs_p2p*) with `world`
+    ranks emulated in ONE cooperative launch on this device — the same kernel
+    and exchange code a multi-GPU job runs, peers being plain device memory —
+    equals the reference (oracle) in dist, sel-max parents and counters, over
+    repeated BFS on the same windows (barrier generations carry over)."""
+    from paper_2010_09913_b200.sharding import partition_chunks, run_p2p_group
+    monkeypatch.setenv("SSB_SMEM_KB", "4")  # prefix + summary + exact lookups; summary words shared at range ends
+    n, uv = port.gen_kronecker(15, 16, 2)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    reprs = [ssb.build_slimsell(g, 32, n) for _ in range(world)]
+    ranges = partition_chunks(reprs[0].cl, 32, world)
+    for root in (0, 5, 2000, 31000):
+        for v, sw, Lc in ((3, True, 64), (0, True, 0), (3, False, 0), (1, True, 16), (2, True, 2048)):
+            o = opts(ssb, v, sw, Lc)
+            dist, parent, per_iter, ms = run_p2p_group(reprs, ranges, root, o)
+            b = port.bfs_spmv(L, root, v, sw, Lc)
+            assert np.array_equal(dist, b.dist), (root, v, world)
+            if v == 3:
+                assert np.array_equal(parent, b.parent), (root, v, world)
+            assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
+    # an uneven split (one rank owns a single chunk) and the iteration cap
+    nc = reprs[0].n_chunks
+    odd = [(0, 1), (1, nc)] + [(nc, nc)] * (world - 2)
+    o = opts(ssb, 3, True, 64)
+    dist, parent, _, _ = run_p2p_group(reprs, odd, 5, o)
+    b = port.bfs_spmv(L, 5, 3, True, 64)
+    assert np.array_equal(dist, b.dist) and np.array_equal(parent, b.parent)
+    o.max_iterations = 2
+    with pytest.raises(ssb.DeviceError):
+        run_p2p_group(reprs, ranges, 5, o)
+    o.max_iterations = 0
+    dist, _, _, _ = run_p2p_group(reprs, ranges, 5, o)  # usable after a capped BFS
+    assert np.array_equal(dist, b.dist)
+
+
+def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
+    """The per-rank entry points a multi-GPU job uses (ssb_p2p_window → IPC
+    handle, ssb_p2p_attach, ssb_bfs_p2p with the one-launch-per-rank kernel,
+    ssb_bfs_shard_fetch) at world 1: the exchange has no peers but the kernel,
+    its barrier generations and the window reset run exactly as on a rank."""
+    from paper_2010_09913_b200.sharding import P2PShard
+    monkeypatch.setenv("SSB_SMEM_KB", "4")
+    n, uv = port.gen_kronecker(14, 16, 5)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    r = ssb.build_slimsell(g, 32, n)
+    sh = P2PShard(r, 0, r.n_chunks)
+    h = sh.window_handle()
+    assert len(h) == 64
+    sh.attach(0, 1, [h])
+    for root in (0, 17, 9000):
+        for v in (3, 0):
+            o = opts(ssb, v, True, 64)
+            k, ms, st = sh.run(root, o)
+            dist = np.full(n, ssb.KINF, np.int64)
+            parent = np.full(n, -1, np.int64)
+            sh.fetch(v == 3, dist, parent)
+            b = port.bfs_spmv(L, root, v, True, 64)
+            assert np.array_equal(dist, b.dist), (root, v)
+            if v == 3:
+                assert np.array_equal(parent, b.parent), (root, v)
+            assert dev_rows(ssb.BfsResult(dist, parent, k, st)) == port_rows(b.stats)
+
+
 def test_device_erdos_renyi_matches_oracle(ssb, port):
     """gen_erdos_renyi (generator.cpp:15-58) bit-exact, incl. p = 0 / 1 and
     the config-4 shape (average degree 16) at 2^18 and 2^20 vertices."""
