@@ -398,11 +398,15 @@ def main():
         mx = torch.tensor([e2e_s], dtype=torch.float64, device=RED_DEV)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         e2e_tot, e2e_max = float(t.item()), float(mx.item())
+    wire = os.environ.get("SSB_WIRE", "1") != "0" and n >= 1 << 16  # fetch_rows' wire-format rule
     e2e = {"value": round(e2e_tot / e2e_max / 1e9, 3) if e2e_tot else None, "unit": "GTEPS",
            "h2d_bytes_per_step": 8 * len(roots),
-           "d2h_bytes_per_step": (16 if parents_out else 8) * n * len(roots),
+           "d2h_bytes_per_step": ((5 if parents_out else 1) if wire else (16 if parents_out else 8)) *
+                                 n * len(roots),
            "note": "ssb_bfs_spmv per root: root in, dist" + ("+parent" if parents_out else "") +
-                   " int64[n] out to pinned host memory"}
+                   " int64[n] out to pinned host memory" +
+                   (" (PCIe carries uint8 levels + int32 parents, widened to int64 by host threads)"
+                    if wire else "")}
 
     # ---- Graph500-style validation of every root (device, untimed) ----------
     validation = None

@@ -1156,13 +1156,14 @@ __global__ void unpermute_kernel(const uint32_t* __restrict__ visited,
 
 // dp_transform (semiring.cpp:159-187) on the layout: the smallest ORIGINAL id
 // among the row's neighbours one level closer; root self-parented.
+template <class T>
 __global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t* __restrict__ cs,
                                  const int32_t* __restrict__ cl, int64_t C,
                                  const uint32_t* __restrict__ visited,
                                  const int32_t* __restrict__ level,
                                  const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ inv_perm, int64_t n,
-                                 int64_t* __restrict__ par, int* __restrict__ bad, int64_t pb,
+                                 T* __restrict__ par, int* __restrict__ bad, int64_t pb,
                                  int64_t pe) {
   GRID_STRIDE(o, n) {
     const int32_t p = inv_perm[o];
@@ -1185,7 +1186,24 @@ __global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t*
       if (((visited[c >> 5] >> (c & 31)) & 1u) && level[c] == lv - 1) bestp = min(bestp, perm[c]);
     }
     if (bestp == INT_MAX) atomicOr(bad, 1);
-    par[o] = bestp == INT_MAX ? -1 : bestp;
+    par[o] = bestp == INT_MAX ? T(-1) : T(bestp);
+  }
+}
+
+// The result in original ids as the PCIe wire format of the fetch: uint8
+// levels (255 = unreached) and int32 sel-max parents (-1 = unreached);
+// hostio.cpp widens them into the caller's int64 arrays.
+__global__ void pack_wire_kernel(const uint32_t* __restrict__ visited,
+                                 const int32_t* __restrict__ level,
+                                 const int32_t* __restrict__ parent,
+                                 const int32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ inv_perm, int64_t n,
+                                 uint8_t* __restrict__ lev8, int32_t* __restrict__ par32) {
+  GRID_STRIDE(o, n) {
+    const int32_t p = inv_perm[o];
+    const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
+    if (lev8) lev8[o] = reached ? uint8_t(level[p]) : uint8_t(255);
+    if (par32) par32[o] = reached ? perm[parent[p]] : -1;
   }
 }
 
@@ -1891,6 +1909,79 @@ void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
   fetch_rows(g, want_parents, dist, parent, parent_len, 0, g.n_padded);
 }
 
+// Pinned host copy of the wire buffer and the per-chunk completion events.
+struct WireHost {
+  uint8_t* p = nullptr;
+  size_t bytes = 0;
+  std::vector<cudaEvent_t> ev;
+  ~WireHost() {
+    if (p) cudaFreeHost(p);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+// Whole-result fetch through the narrow wire format: pack (device) -> chunked
+// D2H into pinned staging -> host threads widen chunk c while c+1 is in
+// flight. 5 bytes per vertex cross PCIe instead of 16.
+void fetch_wire(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent, int64_t* parent_len) {
+  cudaStream_t s = g.sc.s;
+  const int64_t n = g.n;
+  const bool sel = g.last_variant == SSB_SELMAX;
+  const bool want_p = want_parents && parent != nullptr;
+  const size_t poff = (size_t(n) + 255) & ~size_t(255);
+  const size_t bytes = poff + 4 * size_t(n);
+  g.wire.ensure(bytes);
+  auto* H = static_cast<WireHost*>(g.wire_host.get());
+  if (!H || H->bytes < bytes) {
+    auto h = std::make_shared<WireHost>();
+    SSB_CUDA(cudaHostAlloc(&h->p, bytes, cudaHostAllocDefault));
+    h->bytes = bytes;
+    g.wire_host = h;
+    H = h.get();
+  }
+  const int K = std::max(1, std::min(64, env_int("SSB_WIRE_CHUNKS", 16)));
+  while (int(H->ev.size()) < K) {
+    cudaEvent_t e;
+    SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
+    H->ev.push_back(e);
+  }
+  uint8_t* lev8 = g.wire.p;
+  int32_t* par32 = reinterpret_cast<int32_t*>(g.wire.p + poff);
+  uint8_t* hlev = H->p;
+  int32_t* hpar = reinterpret_cast<int32_t*>(H->p + poff);
+  BitRegions R = bit_regions(g, 0);
+  pack_wire_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p, g.inv_perm.p, n,
+                                               dist ? lev8 : nullptr, want_p && sel ? par32 : nullptr);
+  SSB_CUDA(cudaGetLastError());
+  int hbad = 0;
+  if (want_parents && !sel) {
+    g.flag.ensure(1);
+    SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, 4, s));
+    if (want_p)
+      dp_parent_kernel<int32_t><<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
+                                                            g.level.p, g.perm.p, g.inv_perm.p, n, par32,
+                                                            g.flag.p, 0, g.n_padded);
+    SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<int64_t> bounds(size_t(K) + 1);
+  for (int c = 0; c <= K; ++c) bounds[size_t(c)] = (n * c / K + 63) / 64 * 64 < n ? (n * c / K + 63) / 64 * 64 : n;
+  bounds[0] = 0;
+  std::vector<cudaEvent_t> ready(H->ev.begin(), H->ev.begin() + K);
+  for (int c = 0; c < K; ++c) {
+    const int64_t b = bounds[size_t(c)], len = bounds[size_t(c) + 1] - b;
+    if (len > 0 && dist)
+      SSB_CUDA(cudaMemcpyAsync(hlev + b, lev8 + b, size_t(len), cudaMemcpyDeviceToHost, s));
+    if (len > 0 && want_p)
+      SSB_CUDA(cudaMemcpyAsync(hpar + b, par32 + b, 4 * size_t(len), cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaEventRecord(ready[size_t(c)], s));
+  }
+  widen_chunks(bounds, ready, hlev, hpar, dist, want_p ? parent : nullptr);
+  g.sc.sync();
+  if (hbad) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
+  if (parent_len) *parent_len = want_parents ? n : 0;
+}
+
 // Results of the rows at positions [pb, pe) only (a shard), original ids.
 void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
                 int64_t* parent_len, int64_t pb, int64_t pe) {
@@ -1899,6 +1990,14 @@ void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
   const int64_t n = g.n;
   if (n == 0) {
     if (parent_len) *parent_len = 0;
+    return;
+  }
+  // whole results of shallow BFS (levels fit a byte) of graphs worth it take
+  // the narrow wire format (SSB_WIRE=0: the direct int64 path below)
+  const bool whole = pb <= 0 && pe >= g.n_padded;
+  if (whole && g.last_iterations <= 254 && n >= env_int("SSB_WIRE_MIN", 1 << 16) &&
+      env_int("SSB_WIRE", 1) != 0) {
+    fetch_wire(g, want_parents, dist, parent, parent_len);
     return;
   }
   BitRegions R = bit_regions(g, 0);  // visited is the first region for both engines
@@ -1933,7 +2032,7 @@ void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
     g.flag.ensure(1);
     SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, 4, s));
     if (p_out)
-      dp_parent_kernel<<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
+      dp_parent_kernel<int64_t><<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
                                                    g.level.p, g.perm.p, g.inv_perm.p, n, p_out,
                                                    g.flag.p, pb, pe);
     SSB_CUDA(cudaGetLastError());

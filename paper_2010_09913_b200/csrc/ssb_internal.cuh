@@ -160,6 +160,8 @@ struct ssb_graph {
   int64_t last_launches = 0;  // kernels launched by the last BFS
   int64_t last_swept = 0;     // columns the last BFS actually streamed (Σ over iterations)
   std::shared_ptr<void> shard;  // state of a sharded (multi-GPU) BFS in progress
+  ssb::DevBuf<uint8_t> wire;       // result fetch: uint8 levels | int32 parents (original ids)
+  std::shared_ptr<void> wire_host; // ... its pinned host copy and chunk events (bfs.cu)
   ssb::DevBuf<uint32_t> p2p_win;  // fused multi-GPU BFS: the peer-mapped frontier window
   std::shared_ptr<void> p2p;      // ... and its peer table (bfs.cu)
   std::shared_ptr<void> geom;   // cached shared-memory image geometry (bfs.cu)
@@ -196,6 +198,11 @@ void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, int64_t 
 int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t root,
             const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
             int64_t* iterations, double* device_ms);
+// hostio.cpp: widen the uint8 / int32 wire chunks into int64 host arrays on a
+// persistent host thread pool, chunk c once ready[c] has completed
+void widen_chunks(const std::vector<int64_t>& bounds, const std::vector<cudaEvent_t>& ready,
+                  const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent);
+int host_threads();
 // ingest.cu
 void parse_edge_list(std::string_view text, int directive, std::vector<int64_t>& uv, int64_t& n);
 void parse_matrix_market(std::string_view text, std::vector<int64_t>& uv, int64_t& n);

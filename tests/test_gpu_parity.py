@@ -412,6 +412,39 @@ def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
             assert dev_rows(ssb.BfsResult(dist, parent, k, st)) == port_rows(b.stats)
 
 
+def test_fetch_wire_format_equals_direct_path(ssb, port, monkeypatch):
+    """Whole-result fetches go through the narrow wire format (uint8 levels +
+    int32 parents over PCIe, widened to int64 by host threads); it must equal
+    the direct int64 path (SSB_WIRE=0) and the oracle, into pageable and
+    pinned outputs, for sel-max parents and dp_transform parents, and with the
+    chunking pushed to odd sizes."""
+    import torch
+    n, uv = port.gen_kronecker(17, 16, 3)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    r = ssb.build_slimsell(g, 32, n)
+    csr = ssb.to_csr(g)
+    pin_d = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    pin_p = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    for root in (0, 4242):
+        for v in (3, 0, 2):
+            o = opts(ssb, v, True, 64)
+            b = port.bfs_spmv(L, root, v, True, 64, csr=(row, col))
+            outs = []
+            for wire, chunks in (("1", "16"), ("1", "7"), ("0", "16")):
+                monkeypatch.setenv("SSB_WIRE", wire)
+                monkeypatch.setenv("SSB_WIRE_CHUNKS", chunks)
+                a = ssb.bfs_spmv(r, root, o, csr)
+                pin_d.fill(-7)
+                pin_p.fill(-7)
+                c = ssb.bfs_spmv(r, root, o, csr, pin_d, pin_p)
+                outs.append((a.dist.copy(), a.parent.copy(), c.dist.copy(), c.parent.copy()))
+            for d1, p1, d2, p2 in outs:
+                assert np.array_equal(d1, b.dist) and np.array_equal(d2, b.dist), (root, v)
+                assert np.array_equal(p1, b.parent) and np.array_equal(p2, b.parent), (root, v)
+
+
 def test_device_erdos_renyi_matches_oracle(ssb, port):
     """gen_erdos_renyi (generator.cpp:15-58) bit-exact, incl. p = 0 / 1 and
     the config-4 shape (average degree 16) at 2^18 and 2^20 vertices."""
