@@ -1164,8 +1164,9 @@ __global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t*
                                  const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ inv_perm, int64_t n,
                                  T* __restrict__ par, int* __restrict__ bad, int64_t pb,
-                                 int64_t pe) {
-  GRID_STRIDE(o, n) {
+                                 int64_t pe, int64_t o0 = 0) {
+  GRID_STRIDE(i, n - o0) {
+    const int64_t o = o0 + i;
     const int32_t p = inv_perm[o];
     if (p < pb || p >= pe) continue;  // another shard's row
     if (!((visited[p >> 5] >> (p & 31)) & 1u)) {
@@ -1197,9 +1198,10 @@ __global__ void pack_wire_kernel(const uint32_t* __restrict__ visited,
                                  const int32_t* __restrict__ level,
                                  const int32_t* __restrict__ parent,
                                  const int32_t* __restrict__ perm,
-                                 const int32_t* __restrict__ inv_perm, int64_t n,
+                                 const int32_t* __restrict__ inv_perm, int64_t o0, int64_t o1,
                                  uint8_t* __restrict__ lev8, int32_t* __restrict__ par32) {
-  GRID_STRIDE(o, n) {
+  GRID_STRIDE(i, o1 - o0) {
+    const int64_t o = o0 + i;
     const int32_t p = inv_perm[o];
     const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
     if (lev8) lev8[o] = reached ? uint8_t(level[p]) : uint8_t(255);
@@ -1950,32 +1952,35 @@ void fetch_wire(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent, 
   uint8_t* hlev = H->p;
   int32_t* hpar = reinterpret_cast<int32_t*>(H->p + poff);
   BitRegions R = bit_regions(g, 0);
-  pack_wire_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p, g.inv_perm.p, n,
-                                               dist ? lev8 : nullptr, want_p && sel ? par32 : nullptr);
-  SSB_CUDA(cudaGetLastError());
   int hbad = 0;
-  if (want_parents && !sel) {
+  const bool dp = want_parents && !sel;
+  if (dp) {
     g.flag.ensure(1);
     SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, 4, s));
-    if (want_p)
-      dp_parent_kernel<int32_t><<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
-                                                            g.level.p, g.perm.p, g.inv_perm.p, n, par32,
-                                                            g.flag.p, 0, g.n_padded);
-    SSB_CUDA(cudaGetLastError());
-    SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
   }
   std::vector<int64_t> bounds(size_t(K) + 1);
-  for (int c = 0; c <= K; ++c) bounds[size_t(c)] = (n * c / K + 63) / 64 * 64 < n ? (n * c / K + 63) / 64 * 64 : n;
-  bounds[0] = 0;
+  for (int c = 0; c <= K; ++c) bounds[size_t(c)] = std::min(n, (n * c / K + 63) / 64 * 64);
   std::vector<cudaEvent_t> ready(H->ev.begin(), H->ev.begin() + K);
+  // chunk c is packed, then copied, while the host widens chunk c-1
   for (int c = 0; c < K; ++c) {
     const int64_t b = bounds[size_t(c)], len = bounds[size_t(c) + 1] - b;
+    if (len > 0) {
+      pack_wire_kernel<<<grid_for(len), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
+                                                     g.inv_perm.p, b, b + len, dist ? lev8 : nullptr,
+                                                     want_p && sel ? par32 : nullptr);
+      if (dp && want_p)
+        dp_parent_kernel<int32_t><<<grid_for(len), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
+                                                                g.level.p, g.perm.p, g.inv_perm.p, b + len,
+                                                                par32, g.flag.p, 0, g.n_padded, b);
+      SSB_CUDA(cudaGetLastError());
+    }
     if (len > 0 && dist)
       SSB_CUDA(cudaMemcpyAsync(hlev + b, lev8 + b, size_t(len), cudaMemcpyDeviceToHost, s));
     if (len > 0 && want_p)
       SSB_CUDA(cudaMemcpyAsync(hpar + b, par32 + b, 4 * size_t(len), cudaMemcpyDeviceToHost, s));
     SSB_CUDA(cudaEventRecord(ready[size_t(c)], s));
   }
+  if (dp) SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
   widen_chunks(bounds, ready, hlev, hpar, dist, want_p ? parent : nullptr);
   g.sc.sync();
   if (hbad) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
