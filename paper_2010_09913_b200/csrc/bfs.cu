@@ -387,7 +387,7 @@ __device__ __align__(16) int32_t g_pad_column[32] = {
     -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
 #ifndef SSB_WARP_UNIT_COLS
-#define SSB_WARP_UNIT_COLS 16
+#define SSB_WARP_UNIT_COLS 32  // A/B at S26: 16 -> 32 gives Kronecker +1-2%, Erdős–Rényi +13%
 #endif
 constexpr int32_t kWarpUnitCols = SSB_WARP_UNIT_COLS;  // units at least this long use the warp-wide sweep
 
@@ -819,11 +819,12 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         prefetch_l2(a.col + a.cs[U.chunk] + int64_t(U.col_begin + first) * 32, uint32_t(hc) * 128u);
       }
 #ifndef SSB_PF_SHORT
-#define SSB_PF_SHORT 1
+#define SSB_PF_SHORT 0
 #endif
-      // short units are swept four at a time, up to eight rounds per task, each
-      // round paying a memory round trip: their whole columns (< 2 KB each) are
-      // prefetched into L2 when the task starts, so the later rounds hit L2
+      // SSB_PF_SHORT: prefetch the whole columns of short units into L2 when
+      // the task starts, so later group rounds hit L2 (paid off with 16-column
+      // short units; with 32 it over-fetches: A/B S26 Kronecker +0.3%, ER +2%
+      // without it)
       if (SSB_PF_SHORT && has && !skip && U.col_len > 0 && U.col_len < kWarpUnitCols)
         prefetch_l2(a.col + ubase, uint32_t(U.col_len) * 128u);
       // Long units (≥ kWarpUnitCols columns) are swept by the whole warp as one

@@ -10,8 +10,11 @@ ap.add_argument("--scale", type=int, default=26)
 ap.add_argument("--roots", type=int, default=16)
 ap.add_argument("--L", default="128,256,512")
 ap.add_argument("--env", action="append", default=[], help="NAME=v1,v2,...")
+ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er"])
+ap.add_argument("--variant", type=int, default=3)
 a = ap.parse_args()
-g = ssb.gen_kronecker(a.scale, 16, 1)
+g = (ssb.gen_erdos_renyi(1 << a.scale, 16 / ((1 << a.scale) - 1), 1) if a.graph == "er"
+     else ssb.gen_kronecker(a.scale, 16, 1))
 r = ssb.build_slimsell(g, 32, g.num_vertices())
 del g
 roots = graph500_roots(r.degrees(), a.roots, 1)
@@ -23,7 +26,7 @@ for combo in combos:
     L = combo[0]
     for (name, _), val in zip(envs, combo[1:]):
         os.environ[name] = val
-    o = ssb.BfsOptions(variant=ssb.Variant.selmax, slimwork=True, slimchunk_len=L)
+    o = ssb.BfsOptions(variant=ssb.Variant(a.variant), slimwork=True, slimchunk_len=L)
     db.run(roots[0], o)  # warm (plan build)
     tot_ms, tot_e, kms = 0.0, 0, 0.0
     for root in roots:
