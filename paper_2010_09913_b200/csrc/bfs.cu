@@ -872,6 +872,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
                              gmask, c_front);
       }
 
+      bool first_round = true;
       while (active) {
         // the next (up to) four active units, one per 8-lane group
         int32_t src = -1;
@@ -882,6 +883,30 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
           if (active) active &= active - 1;
         }
         const int32_t sl = src < 0 ? 0 : src;
+#ifndef SSB_PF_NEXT
+#define SSB_PF_NEXT 1  // rounds ahead whose units are prefetched (A/B S26 ER: 0 -> 1 +7%)
+#endif
+        if (SSB_PF_NEXT > 0) {
+          // this group's unit of round +SSB_PF_NEXT (and, in the first round,
+          // of the rounds before it) goes to L2 while this round runs
+          uint32_t rest = active;
+#pragma unroll
+          for (int d = 1; d <= SSB_PF_NEXT; ++d) {
+            int32_t nsrc = -1;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int32_t f = rest ? __ffs(rest) - 1 : -1;
+              if (g == grp) nsrc = f;
+              if (rest) rest &= rest - 1;
+            }
+            if (d == SSB_PF_NEXT || first_round) {
+              const int32_t nl = __shfl_sync(0xffffffffu, U.col_len, nsrc < 0 ? 0 : nsrc);
+              const int64_t nb = __shfl_sync(0xffffffffu, ubase, nsrc < 0 ? 0 : nsrc);
+              if (lg == 0 && nsrc >= 0 && nl > 0) prefetch_l2(a.col + nb, uint32_t(nl) * 128u);
+            }
+          }
+          first_round = false;
+        }
         const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
         const int32_t ulen = __shfl_sync(0xffffffffu, U.col_len, sl);  // all lanes shuffle
         const int32_t len = src < 0 ? 0 : ulen;
@@ -1599,9 +1624,11 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   {
     // Early-exit sweeps pay off once rows get decided quickly: on hub-heavy
     // graphs (most probes land in the shared prefix) from |F| > n/4096 on; on
-    // low-skew graphs only for dense frontiers (A/B on config 3 and config 4).
+    // low-skew graphs from |F| > n/128 (A/B on config 3 and config 4: the
+    // batched exact lookups of the early-exit sweep win once the summary is
+    // mostly set, even when few rows exit early).
     const bool hubby = G.S == 8;
-    const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 4096 : 16));
+    const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 4096 : 128));
     a.dense_thr = std::max<int64_t>(1, g.n / div);
   }
   a.n_chunks = int32_t(g.n_chunks);
