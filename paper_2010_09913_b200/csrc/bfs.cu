@@ -848,6 +848,18 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       while (longs) {
         const int32_t sl = __ffs(longs) - 1;
         longs &= longs - 1;
+#ifndef SSB_PF_NEXT_LONG
+#define SSB_PF_NEXT_LONG 16  // columns of the next long unit prefetched (A/B: +0.2-0.6%)
+#endif
+        if (SSB_PF_NEXT_LONG > 0 && longs) {
+          // head (in sweep order) of the next long unit goes to L2 now
+          const int32_t nx = __ffs(longs) - 1;
+          const int32_t nl = __shfl_sync(0xffffffffu, U.col_len, nx);
+          const int64_t nb = __shfl_sync(0xffffffffu, ubase, nx);
+          const int32_t hc = min(nl, SSB_PF_NEXT_LONG);
+          const int32_t first = (kSelMax && kEarly) ? nl - hc : 0;
+          if (lane == 0) prefetch_l2(a.col + nb + int64_t(first) * 32, uint32_t(hc) * 128u);
+        }
         const int32_t chunk = __shfl_sync(0xffffffffu, U.chunk, sl);
         const int32_t len = __shfl_sync(0xffffffffu, U.col_len, sl);
         const int32_t split = __shfl_sync(0xffffffffu, U.split, sl);
