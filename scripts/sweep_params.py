@@ -12,6 +12,7 @@ ap.add_argument("--L", default="128,256,512")
 ap.add_argument("--env", action="append", default=[], help="NAME=v1,v2,...")
 ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er"])
 ap.add_argument("--variant", type=int, default=3)
+ap.add_argument("--reps", type=int, default=1, help="repeat the whole combination list (interleaved A/B)")
 a = ap.parse_args()
 g = (ssb.gen_erdos_renyi(1 << a.scale, 16 / ((1 << a.scale) - 1), 1) if a.graph == "er"
      else ssb.gen_kronecker(a.scale, 16, 1))
@@ -20,7 +21,7 @@ del g
 roots = graph500_roots(r.degrees(), a.roots, 1)
 db = ssb.DeviceBfs(r)
 envs = [(e.split("=")[0], e.split("=")[1].split(",")) for e in a.env]
-combos = list(itertools.product([int(x) for x in a.L.split(",")], *[v for _, v in envs]))
+combos = list(itertools.product([int(x) for x in a.L.split(",")], *[v for _, v in envs])) * a.reps
 mcc = {}
 for combo in combos:
     L = combo[0]
