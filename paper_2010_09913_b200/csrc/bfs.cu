@@ -1327,7 +1327,32 @@ Geometry geometry32(const ssb_graph& g) {
 // under a budget, the grain of the dynamic scheduler.
 void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
   ssb_bfs_plan& P = g.plan;
-  if (P.L == L && P.cb == cb && P.ce == ce && P.built) return;
+  // Units are SlimChunk segments of at most Lu columns: the reference's L
+  // (which alone defines the subchunks_processed counter, computed
+  // analytically in the kernel) capped for balance — a unit must stay a
+  // small share of one warp's work in a full sweep, or the last long unit of
+  // an iteration idles the grid (S22: one 2048-column unit is ~0.2 ms on a
+  // warp, longer than the whole iteration). L <= 0 (SlimChunk off) splits at
+  // the cap alone.
+  int64_t cap = env_int("SSB_UNIT_CAP", 0);
+  if (cap <= 0) {
+    // the largest power of two (64 .. 4096) not above one warp's share of a
+    // full sweep (A/B S22: 4096 113.8, 512 136.4, 128 131.6 GTEPS); the range
+    // sum is host work, cached with the range
+    if (!(P.cap_cb == cb && P.cap_ce == ce)) {
+      int64_t cols = 0;
+      for (int64_t i = cb; i < ce; ++i) cols += g.cl_host[size_t(i)];
+      const int64_t per_warp = cols / (int64_t(num_sms()) * (kThreads / 32));
+      int64_t c = 64;
+      while (c * 2 <= per_warp && c < 4096) c *= 2;
+      P.cap_auto = c;
+      P.cap_cb = cb;
+      P.cap_ce = ce;
+    }
+    cap = P.cap_auto;
+  }
+  const int64_t Lu = L > 0 ? std::min(L, cap) : cap;
+  if (P.L == L && P.Lu == Lu && P.cb == cb && P.ce == ce && P.built) return;
   std::vector<ssb_unit> units;
   std::vector<int32_t> split_units;
   units.reserve(ce - cb + 16);
@@ -1340,14 +1365,14 @@ void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
       ++P.empty_chunks;
       continue;
     }
-    if (L <= 0 || cl <= L) {
+    if (cl <= Lu) {
       units.push_back({int32_t(i), 0, int32_t(cl), -1});
     } else {
       const int32_t sp = int32_t(split_units.size());
-      const int64_t nseg = (cl + L - 1) / L;
+      const int64_t nseg = (cl + Lu - 1) / Lu;
       split_units.push_back(int32_t(nseg));
       for (int64_t s = 0; s < nseg; ++s)
-        units.push_back({int32_t(i), int32_t(s * L), int32_t(std::min(L, cl - s * L)), sp});
+        units.push_back({int32_t(i), int32_t(s * Lu), int32_t(std::min(Lu, cl - s * Lu)), sp});
     }
   }
   const int64_t budget = env_int("SSB_TASK_BUDGET", 512);
@@ -1368,6 +1393,7 @@ void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
   if (units.size() >= size_t(INT32_MAX)) fail(SSB_EINVAL, "too many work units");
   cudaStream_t s = g.sc.s;
   P.L = L;
+  P.Lu = Lu;
   P.cb = cb;
   P.ce = ce;
   P.built = true;

@@ -111,6 +111,8 @@ struct ssb_unit {
 
 struct ssb_bfs_plan {  // cached per slimchunk_len
   int64_t L = -1;
+  int64_t Lu = -1;  // columns per work unit: min(L, balance cap)
+  int64_t cap_auto = 0, cap_cb = -1, cap_ce = -1;  // balance cap of a chunk range
   int64_t n_units = 0;
   int64_t n_tasks = 0;
   int64_t n_split = 0;
