@@ -174,6 +174,7 @@ struct Args32 {
   unsigned long long gone_base;  // chunks of tasks retired before k_begin
   int64_t front_in;    // frontier size entering iteration k_begin
   int64_t dense_thr;   // frontiers above this use the early-exit sweeps
+  int64_t direct_thr;  // ... and above this the summary-free direct probes
   int32_t n_chunks;
   int32_t PW;      // frontier prefix words staged in shared memory
   int32_t SW;      // summary words staged in shared memory
@@ -305,14 +306,52 @@ struct Probe {
 // column is probed in ascending order and sel-max keeps the LAST hit — the
 // cheapest instruction stream. kEarly = true (dense frontiers, where the exact
 // lookups dominate): decided rows are masked out as described above.
+// Early-exit cells without the summary, for iterations whose previous
+// frontier sets most summary bits anyway (|F| above the summary's bit count):
+// each open cell is ONE generic load of its exact frontier word — from the
+// shared image for c < P, from the global frontier (L1/L2) otherwise — so
+// tail cells skip the summary probe and its dependent second load. Decided
+// rows and padding cells read a zero word of the image.
+template <bool kSelMax, class Probe>
+__device__ __forceinline__ void take_cells_direct(const int4 v, const Probe& pr, uint32_t& hit,
+                                                  int32_t (&best)[4]) {
+  const int32_t c[4] = {v.x, v.y, v.z, v.w};
+  const uint32_t* p[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool open = !((hit >> q) & 1u) && c[q] >= 0;
+    p[q] = !open ? pr.sm - 4 : (c[q] < pr.P ? pr.sm : pr.Fc) + (c[q] >> 5);
+  }
+  uint32_t w[4];
+  asm volatile(
+      "ld.u32 %0, [%4];\n\t"
+      "ld.u32 %1, [%5];\n\t"
+      "ld.u32 %2, [%6];\n\t"
+      "ld.u32 %3, [%7];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+      : "l"(p[0]), "l"(p[1]), "l"(p[2]), "l"(p[3]));
+  uint32_t b = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t bit = (w[q] >> (c[q] & 31)) & 1u;
+    if (kSelMax) best[q] = bit ? c[q] : best[q];
+    b |= bit << q;
+  }
+  hit |= b;
+}
+
 #ifdef SSB_COUNT
 // debug counters (SSB_COUNT builds, one launch per iteration): open probes,
 // tail probes, exact lookups, exact hits, warp steps with a lookup
 __device__ unsigned long long g_cnt[8];
 #endif
-template <bool kSelMax, bool kEarly, class Probe>
+template <bool kSelMax, bool kEarly, bool kDirect, class Probe>
 __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32_t& hit,
                                            int32_t (&best)[4]) {
+  if constexpr (kDirect) {
+    take_cells_direct<kSelMax>(v, pr, hit, best);
+    return;
+  }
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
   const uint32_t open = kEarly ? ~hit : 0xffffffffu;
   // Sparse sweeps are instruction-issue bound and their probes almost always
@@ -468,7 +507,7 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
 // stop the unit once all 32 rows are decided (the semiring "plus" has
 // short-circuited for every row, so the remaining columns cannot change the
 // result). Returns the number of columns swept.
-template <bool kSelMax, bool kEarly, class Probe>
+template <bool kSelMax, bool kEarly, bool kDirect, class Probe>
 __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int lane, int lg,
                                            const Probe& pr, uint64_t pol, uint32_t& hit,
                                            int32_t (&best)[4]) {
@@ -499,13 +538,13 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     for (; s + 9 <= nsteps; s += 4, pf += 128) {
       if (kPfAhead > 0 && lane == 0 && s + 9 + 4 * kPfAhead <= nsteps)
         prefetch_l2(pf - lane + 128 * kPfAhead, 2048);
-      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v0, pr, hit, best);
       v0 = ld_stream(pf, pol);
-      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v1, pr, hit, best);
       v1 = ld_stream(pf + 32, pol);
-      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v2, pr, hit, best);
       v2 = ld_stream(pf + 64, pol);
-      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v3, pr, hit, best);
       v3 = ld_stream(pf + 96, pol);
       if (share()) {
         done = true;
@@ -516,13 +555,13 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     for (; !done && s < nsteps; s += 4) {
       const bool more = s + 4 < nsteps;  // warp-uniform
       const int32_t i0 = (s + 4) * 32 + lane;
-      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v0, pr, hit, best);
       if (more) v0 = ld_stream(base + min(i0, imax), pol);
-      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v1, pr, hit, best);
       if (more) v1 = ld_stream(base + min(i0 + 32, imax), pol);
-      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v2, pr, hit, best);
       if (more) v2 = ld_stream(base + min(i0 + 64, imax), pol);
-      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v3, pr, hit, best);
       if (more) v3 = ld_stream(base + min(i0 + 96, imax), pol);
       if (share()) {
         swept = min(len, 4 * (s + 4));
@@ -547,13 +586,13 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
       // steps top-r-4-4A .. top-r-7-4A: int4 [32(top-r-7-4A), +128)
       if (kPfAhead > 0 && lane == 0 && r + 8 + 4 * kPfAhead <= nsteps)
         prefetch_l2(pf - lane - 96 - 128 * kPfAhead, 2048);
-      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v0, pr, hit, best);
       v0 = ld_stream(pf, pol);
-      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v1, pr, hit, best);
       v1 = ld_stream(pf - 32, pol);
-      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v2, pr, hit, best);
       v2 = ld_stream(pf - 64, pol);
-      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v3, pr, hit, best);
       v3 = ld_stream(pf - 96, pol);
       if (share()) {
         done = true;
@@ -563,13 +602,13 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     }
     for (; !done && r < nsteps; r += 4) {
       const bool more = r + 4 < nsteps;  // warp-uniform
-      take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v0, pr, hit, best);
       if (more) v0 = ld_stream(at(top - r - 4), pol);
-      take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v1, pr, hit, best);
       if (more) v1 = ld_stream(at(top - r - 5), pol);
-      take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v2, pr, hit, best);
       if (more) v2 = ld_stream(at(top - r - 6), pol);
-      take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+      take_cells<kSelMax, kEarly, kDirect>(v3, pr, hit, best);
       if (more) v3 = ld_stream(at(top - r - 7), pol);
       if (share()) {
         swept = cols_of(min(nsteps, r + 4));
@@ -597,7 +636,7 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
 // unit read a padding column. Loads run 4 columns ahead of the probes.
 // Early-exit sweeps stop once every row of the four units is decided. Returns
 // the number of column steps run (the group's unit swept min(len, that)).
-template <bool kSelMax, bool kEarly, class Probe>
+template <bool kSelMax, bool kEarly, bool kDirect, class Probe>
 __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int64_t stride,
                                             int32_t maxlen, const Probe& pr, uint64_t pol,
                                             uint32_t& hit, int32_t (&best)[4]) {
@@ -610,13 +649,13 @@ __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int
   int32_t j = 0;
   while (j < maxlen) {
     const bool more = j + 4 < maxlen;  // warp-uniform
-    take_cells<kSelMax, kEarly>(v0, pr, hit, best);
+    take_cells<kSelMax, kEarly, kDirect>(v0, pr, hit, best);
     if (more) v0 = ld_stream(at(j + 4), pol);
-    take_cells<kSelMax, kEarly>(v1, pr, hit, best);
+    take_cells<kSelMax, kEarly, kDirect>(v1, pr, hit, best);
     if (more) v1 = ld_stream(at(j + 5), pol);
-    take_cells<kSelMax, kEarly>(v2, pr, hit, best);
+    take_cells<kSelMax, kEarly, kDirect>(v2, pr, hit, best);
     if (more) v2 = ld_stream(at(j + 6), pol);
-    take_cells<kSelMax, kEarly>(v3, pr, hit, best);
+    take_cells<kSelMax, kEarly, kDirect>(v3, pr, hit, best);
     if (more) v3 = ld_stream(at(j + 7), pol);
     j += 4;
     if (kEarly && __all_sync(0xffffffffu, hit == 0xfu)) break;
@@ -770,8 +809,9 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     int32_t* list_out = (k & 1) ? a.tlist1 : a.tlist0;
     // dense previous frontier -> early-exit sweeps (see take_cells)
     const bool dense = front_in > a.dense_thr;
-    auto run_tasks = [&](auto early_tag) {
+    auto run_tasks = [&](auto early_tag, auto direct_tag) {
     constexpr bool kEarly = decltype(early_tag)::value;
+    constexpr bool kDirect = decltype(direct_tag)::value;
     // each warp's first task is its global warp id; the rest come from the
     // atomic counter (late iterations with few tasks then cost no atomics)
     const int32_t n_warps = int32_t(nvb) * (kThreads / 32);
@@ -874,7 +914,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         // padding) marked decided: their probes are skipped
         uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
-        const int32_t sw = sweep_long<kSelMax, kEarly>(base, len, lane, lg, pr, pol, hit, best);
+        const int32_t sw = sweep_long<kSelMax, kEarly, kDirect>(base, len, lane, lg, pr, pol, hit, best);
         if (lane == 0) c_swept += uint32_t(sw);
         uint32_t m = hit << (4 * lg);
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
@@ -941,7 +981,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         // (a group without a unit counts as decided)
         uint32_t hit = kEarly ? (src < 0 ? 0xfu : ((uvis | ~ureal) >> (4 * lg)) & 0xfu) : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
-        const int32_t ran = sweep_group<kSelMax, kEarly>(p, jlast, stride, maxlen, pr, pol, hit, best);
+        const int32_t ran = sweep_group<kSelMax, kEarly, kDirect>(p, jlast, stride, maxlen, pr, pol, hit, best);
         if (lg == 0) c_swept += uint32_t(min(len, ran));
         // 32-bit row mask of the unit (rows 4*lg+q)
         uint32_t m = hit << (4 * lg);
@@ -954,8 +994,9 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       }
     }
     };  // run_tasks
-    if (dense) run_tasks(std::true_type{});
-    else run_tasks(std::false_type{});
+    if (dense && front_in > a.direct_thr) run_tasks(std::true_type{}, std::true_type{});
+    else if (dense) run_tasks(std::true_type{}, std::false_type{});
+    else run_tasks(std::false_type{}, std::false_type{});
 
     // -- iteration counters: warp -> block -> grid --------------------------
 #pragma unroll
@@ -1673,6 +1714,9 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     const bool hubby = G.S == 8;
     const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 4096 : 128));
     a.dense_thr = std::max<int64_t>(1, g.n / div);
+    // once |F| exceeds the summary's bits most of them are set: probe exactly
+    const int64_t dt = env_int("SSB_DIRECT_THR", -1);
+    a.direct_thr = dt >= 0 ? dt : (G.SW > 0 ? int64_t(G.SW) * 32 : INT64_MAX);
   }
   a.n_chunks = int32_t(g.n_chunks);
   a.PW = G.PW;

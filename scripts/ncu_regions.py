@@ -37,7 +37,10 @@ for line in sass.splitlines():
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", line)
     if m and chain:
         # skip the run_tasks lambda call (kernel body -> lambda) level
-        c = chain[:-1] if len(chain) > 1 and "run_tasks(" in SRC[chain[-1] - 1] else chain
+        c = list(chain)
+        # skip the kernel -> bfs32_body and body -> run_tasks lambda levels
+        while len(c) > 1 and ("run_tasks(" in SRC[c[-1] - 1] or "bfs32_body<" in SRC[c[-1] - 1]):
+            c = c[:-1]
         addr_site[int(m.group(1), 16)] = (c[-1], c[-2] if len(c) > 1 else c[-1])
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout

@@ -382,6 +382,27 @@ def test_fused_p2p_sharded_bfs_matches_oracle(ssb, port, monkeypatch, world):
     assert np.array_equal(dist, b.dist)
 
 
+def test_fused_p2p_default_geometry_matches_single_gpu(ssb):
+    """The emulated fused multi-GPU BFS at S20 with the production image
+    geometry (160 KB: prefix + summary, dense/direct probe modes all reached)
+    equals the single-GPU engine bit for bit, counters included."""
+    from paper_2010_09913_b200.sharding import partition_chunks, run_p2p_group
+    g = ssb.gen_kronecker(20, 16, 1)
+    n = g.num_vertices()
+    reprs = [ssb.build_slimsell(g, 32, n) for _ in range(4)]
+    for world in (3, 4):
+        ranges = partition_chunks(reprs[0].cl, 32, world)
+        for root in (0, 12345, 777777):
+            for v in (3, 0):
+                o = opts(ssb, v, True, 256)
+                a = ssb.bfs_spmv(reprs[0], root, o)
+                dist, parent, per_iter, _ = run_p2p_group(reprs[:world], ranges, root, o)
+                assert np.array_equal(dist, a.dist), (world, root, v)
+                if v == 3:
+                    assert np.array_equal(parent, a.parent), (world, root, v)
+                assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == dev_rows(a)
+
+
 def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
     """The per-rank entry points a multi-GPU job uses (ssb_p2p_window → IPC
     handle, ssb_p2p_attach, ssb_bfs_p2p with the one-launch-per-rank kernel,
