@@ -608,20 +608,37 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
             dist.barrier()
         torch.cuda.synchronize()
 
-    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
-    deg = r.degrees()
+    # every rank holds only its own chunks' cells: a
+    # metadata-only build (empty range) gives cl for the partition, then each
+    # rank builds its range — the memory that lets S28 span 8 GPUs
+    t0 = time.time()
+    g = (ssb.gen_erdos_renyi(1 << a.scale, a.avg_degree / ((1 << a.scale) - 1), a.seed) if a.graph == "er"
+         else ssb.gen_kronecker(a.scale, a.edgefactor, a.seed))
+    t_gen = time.time() - t0
+    n = g.num_vertices()
+    meta = ssb.build_slimsell(g, 32, n, chunk_range=(0, 0))
+    deg = meta.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
     opts = ssb.BfsOptions(variant=ssb.Variant(variant_id), slimwork=slimwork, slimchunk_len=a.slimchunk)
     emu = max(1, a.emulate_ranks) if world == 1 else 1
+    ranges = partition_chunks(meta.cl, 32, emu if emu > 1 else world)
+    del meta
+    t0 = time.time()
     if emu > 1:
-        reprs = [r] + [ssb.build_slimsell(g, 32, g.num_vertices()) for _ in range(emu - 1)]
-        ranges = partition_chunks(r.cl, 32, emu)
+        reprs = [ssb.build_slimsell(g, 32, n, chunk_range=rg) for rg in ranges]
+        r = reprs[0]
+    else:
+        r = ssb.build_slimsell(g, 32, n, chunk_range=ranges[rank])
+    t_build = time.time() - t0
+    log(f"graph S{a.scale}: n={n} m={g.num_edges()}, cells of rank 0's range {r.range_cells} "
+        f"of {r.n_cells}; gen {t_gen:.2f}s build {t_build:.2f}s")
+    del g
+    if emu > 1:
 
         def one(root, fetch=False):
             d, p, per_iter, ms = run_p2p_group(reprs, ranges, root, opts, fetch=fetch)
             return ms, d
     else:
-        ranges = partition_chunks(r.cl, 32, world)
         shard = P2PShard(r, *ranges[rank])
         if world > 1:
             shard.attach_dist()
@@ -645,7 +662,6 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
     clocks = sampler.stop()
     # m_cc per root from the assembled distances (owned rows, MIN over ranks)
     mcc = {}
-    n = r.n
     dd = np.full(n, np.iinfo(np.int64).max, np.int64)
     pp = np.full(n, -1, np.int64)
     for root in roots:
@@ -677,7 +693,9 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": DATA[a.graph],
         "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
                    "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
-                   "roots_per_step": len(roots), "parallelism": par, "l2": "inputs larger than L2"},
+                   "roots_per_step": len(roots), "parallelism": par, "l2": "inputs larger than L2",
+                   "cells_per_rank_max": max(x.range_cells for x in (reprs if emu > 1 else [r])),
+                   "n_cells": r.n_cells},
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "p2p-sharded mode reports device time only"},

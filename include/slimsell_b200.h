@@ -35,7 +35,7 @@ extern "C" {
 #define SSB_ENOMEM 5
 #define SSB_EPARSE 6 /* slimsell::ParseError (graph.hpp:15-21): "line N: ..." */
 
-#define SSB_ABI_VERSION 1
+#define SSB_ABI_VERSION 2
 
 /* Variant (semiring.hpp:25). */
 #define SSB_TROPICAL 0
@@ -46,9 +46,13 @@ extern "C" {
 typedef struct ssb_edges ssb_edges; /* normalised Graph on the device (graph.hpp:31-51) */
 typedef struct ssb_graph ssb_graph; /* SlimSellRepr on the device (repr.hpp:33-55) */
 
-/* SlimSellRepr scalar fields (repr.hpp:33-45). n_cells = |col| = Σ C·cl. */
+/* SlimSellRepr scalar fields (repr.hpp:33-45). n_cells = |col| = Σ C·cl of
+ * the whole layout. A handle built for a chunk range (ssb_build_slimsell_range)
+ * holds the cells of chunks [range_begin, range_end) only: range_cells of
+ * them; a whole layout has range [0, n_chunks) and range_cells = n_cells. */
 typedef struct {
   int64_t C, sigma, n, n_padded, n_chunks, nonzeros, n_cells, padding, max_chunk_len;
+  int64_t range_begin, range_end, range_cells;
 } ssb_layout_info;
 
 /* BfsOptions (bfs.hpp:16-24). schedule and workers are accepted for API
@@ -121,6 +125,17 @@ void ssb_edges_destroy(ssb_edges* e);
  * by (degree desc, id asc), chunk height C, column-major col with -1 padding,
  * no value array. EINVAL for C <= 0 or sigma <= 0. */
 int ssb_build_slimsell(const ssb_edges* e, int64_t C, int64_t sigma, ssb_graph** out);
+/* One rank's share of a multi-GPU layout ("each GPU holds
+ * its own col/cs/cl"): the same σ-sort, perm and chunk lengths as
+ * ssb_build_slimsell for every chunk, but the cells of chunks
+ * [chunk_begin, chunk_end) only (cs offsets into that partial col). Such a
+ * handle serves the sharded BFS of an owned range inside it
+ * (ssb_bfs_shard_*, ssb_p2p_attach / ssb_bfs_p2p[_group]), ssb_spmv_step on
+ * chunks inside it, ssb_graph_info / degrees / col32 export of its cells;
+ * whole-layout calls (ssb_bfs_run / ssb_bfs_spmv, col / cs export) return
+ * EINVAL. chunk_end < 0 = n_chunks. */
+int ssb_build_slimsell_range(const ssb_edges* e, int64_t C, int64_t sigma, int64_t chunk_begin,
+                             int64_t chunk_end, ssb_graph** out);
 /* Uploads a host SlimSellRepr (the reference struct's arrays, int64). */
 int ssb_graph_from_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
                           const int64_t* col, int64_t n_cells, const int64_t* cs,

@@ -21,7 +21,8 @@ i32p = C.POINTER(C.c_int32)
 
 class LayoutInfo(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("C", "sigma", "n", "n_padded", "n_chunks", "nonzeros",
-                                         "n_cells", "padding", "max_chunk_len")]
+                                         "n_cells", "padding", "max_chunk_len", "range_begin",
+                                         "range_end", "range_cells")]
 
 
 class BfsOptionsC(C.Structure):
@@ -75,6 +76,7 @@ def lib() -> C.CDLL:
         "ssb_to_csr": (C.c_int, [vp, i64p, i64p]),
         "ssb_edges_destroy": (None, [vp]),
         "ssb_build_slimsell": (C.c_int, [vp, C.c_int64, C.c_int64, pvp]),
+        "ssb_build_slimsell_range": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, pvp]),
         "ssb_graph_from_layout": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int64,
                                             i64p, i64p, C.c_int64, i64p, pvp]),
         "ssb_graph_info": (C.c_int, [vp, C.POINTER(LayoutInfo)]),

@@ -270,30 +270,44 @@ class SlimSellRepr:
         self.C, self.sigma, self.n = info.C, info.sigma, info.n
         self.n_padded, self.n_chunks, self.nonzeros = info.n_padded, info.n_chunks, info.nonzeros
         self.n_cells, self.padding, self.max_chunk_len = info.n_cells, info.padding, info.max_chunk_len
-        self._host = None
+        # cells held: chunks [range_begin, range_end) (the whole layout unless
+        # built with build_slimsell(..., chunk_range=...))
+        self.range_begin, self.range_end, self.range_cells = info.range_begin, info.range_end, info.range_cells
+        self._host = {}
 
-    def _export(self):
-        if self._host is None:
-            col = np.empty(max(self.n_cells, 1), np.int64)
-            cs = np.empty(max(self.n_chunks, 1), np.int64)
-            cl = np.empty(max(self.n_chunks, 1), np.int64)
-            perm = np.empty(max(self.n, 1), np.int64)
-            inv = np.empty(max(self.n, 1), np.int64)
-            _check(_L.lib().ssb_graph_export(self._h, _p(col), _p(cs), _p(cl), _p(perm), _p(inv)))
-            self._host = dict(col=col[: self.n_cells], cs=cs[: self.n_chunks], cl=cl[: self.n_chunks],
-                              perm=perm[: self.n], inv_perm=inv[: self.n])
-        return self._host
+    @property
+    def partial(self) -> bool:
+        return self.range_begin > 0 or self.range_end < self.n_chunks
 
-    col = property(lambda self: self._export()["col"])
-    cs = property(lambda self: self._export()["cs"])
-    cl = property(lambda self: self._export()["cl"])
-    perm = property(lambda self: self._export()["perm"])
-    inv_perm = property(lambda self: self._export()["inv_perm"])
+    def _export(self, name):
+        if name not in self._host:
+            if name in ("col", "cs"):
+                col = np.empty(max(self.n_cells, 1), np.int64)
+                cs = np.empty(max(self.n_chunks, 1), np.int64)
+                _check(_L.lib().ssb_graph_export(self._h, _p(col), _p(cs), None, None, None))
+                self._host.update(col=col[: self.n_cells], cs=cs[: self.n_chunks])
+            elif name == "cl":
+                cl = np.empty(max(self.n_chunks, 1), np.int64)
+                _check(_L.lib().ssb_graph_export(self._h, None, None, _p(cl), None, None))
+                self._host["cl"] = cl[: self.n_chunks]
+            else:
+                perm = np.empty(max(self.n, 1), np.int64)
+                inv = np.empty(max(self.n, 1), np.int64)
+                _check(_L.lib().ssb_graph_export(self._h, None, None, None, _p(perm), _p(inv)))
+                self._host.update(perm=perm[: self.n], inv_perm=inv[: self.n])
+        return self._host[name]
+
+    col = property(lambda self: self._export("col"))
+    cs = property(lambda self: self._export("cs"))
+    cl = property(lambda self: self._export("cl"))
+    perm = property(lambda self: self._export("perm"))
+    inv_perm = property(lambda self: self._export("inv_perm"))
 
     def col32(self) -> np.ndarray:
-        out = np.empty(max(self.n_cells, 1), np.int32)
+        """The cells this handle holds (the whole col, or the range's)."""
+        out = np.empty(max(self.range_cells, 1), np.int32)
         _check(_L.lib().ssb_graph_export_col32(self._h, _p(out, _L.i32p)))
-        return out[: self.n_cells]
+        return out[: self.range_cells]
 
     def degrees(self) -> np.ndarray:
         """Degree of every original vertex id (row lengths of to_csr)."""
@@ -314,9 +328,16 @@ class SlimSellRepr:
             self._h = None
 
 
-def build_slimsell(g: Graph, C_: int, sigma: int) -> SlimSellRepr:  # repr.hpp:66
+def build_slimsell(g: Graph, C_: int, sigma: int, chunk_range=None) -> SlimSellRepr:  # repr.hpp:66
+    """build_slimsell on the device. chunk_range=(b, e): one rank's share of a
+    multi-GPU layout — the whole layout's perm / cl, the cells of chunks
+    [b, e) only (ssb_build_slimsell_range)."""
     h = C.c_void_p()
-    _check(_L.lib().ssb_build_slimsell(g._h, C_, sigma, C.byref(h)))
+    if chunk_range is None:
+        _check(_L.lib().ssb_build_slimsell(g._h, C_, sigma, C.byref(h)))
+    else:
+        b, e = chunk_range
+        _check(_L.lib().ssb_build_slimsell_range(g._h, C_, sigma, int(b), int(e), C.byref(h)))
     return SlimSellRepr(h)
 
 

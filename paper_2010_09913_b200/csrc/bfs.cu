@@ -1346,10 +1346,10 @@ Geometry geometry32_for(const ssb_graph& g, int S) {
 // cells and a chunk's rows have degree <= cl, so the cells of the first PW
 // chunks estimate it (exactly the cells of those rows' chunks for σ = n).
 double prefix_coverage(const ssb_graph& g, int64_t PW) {
-  if (g.n_cells <= 0) return 1.0;
+  if (g.total_cells <= 0) return 1.0;
   int64_t c = 0;
   for (int64_t i = 0; i < std::min<int64_t>(PW, g.n_chunks); ++i) c += int64_t(g.cl_host[size_t(i)]) * 32;
-  return double(c) / double(g.n_cells);
+  return double(c) / double(g.total_cells);
 }
 
 Geometry geometry32(const ssb_graph& g) {
@@ -1954,6 +1954,7 @@ int num_sms() {
 
 int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats,
             int64_t stats_cap, int64_t* iterations, double* device_ms) {
+  g.need_full("a single-GPU BFS");
   if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
   // semiring.cpp:57-60
   if (root < 0 || root >= g.n)
@@ -2184,6 +2185,8 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
   if (g.C != 32) fail(SSB_EINVAL, "sharded BFS needs the C = 32 layout");
   if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
   if (cb < 0 || ce > g.n_chunks || cb > ce) fail(SSB_EINVAL, "chunk range out of bounds");
+  if (g.partial() && cb < ce && (cb < g.range_cb || ce > g.range_ce))
+    fail(SSB_EINVAL, "owned chunks outside the range this handle holds");
   if (root < 0 || root >= g.n)
     fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g.n) + ")");
   int32_t root_pos = 0;
@@ -2267,6 +2270,8 @@ void p2p_window(ssb_graph& g, void* ipc_handle, int64_t* bytes) {
 
 void check_range(ssb_graph& g, int64_t cb, int64_t ce) {
   if (cb < 0 || ce > g.n_chunks || cb > ce) fail(SSB_EINVAL, "chunk range out of bounds");
+  if (g.partial() && cb < ce && (cb < g.range_cb || ce > g.range_ce))
+    fail(SSB_EINVAL, "owned chunks outside the range this handle holds");
 }
 
 // Maps every peer's window (CUDA IPC; peer access over NVLink). Collective in
@@ -2347,7 +2352,7 @@ int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t ro
   for (int i = 0; i < n_local; ++i) {
     ssb_graph& g = *gs[i];
     if (g.C != 32) fail(SSB_EINVAL, "the fused multi-GPU BFS needs the C = 32 layout");
-    if (g.n != g0.n || g.n_chunks != g0.n_chunks || g.n_cells != g0.n_cells)
+    if (g.n != g0.n || g.n_chunks != g0.n_chunks || g.total_cells != g0.total_cells)
       fail(SSB_EINVAL, "shards hold different layouts");
   }
   if (root < 0 || root >= g0.n)

@@ -85,15 +85,23 @@ __global__ void perm_derive_kernel(const int32_t* __restrict__ perm, int64_t n,
   }
 }
 
+// cl for every chunk; cells only for the chunks of the built range [cb, ce)
+// (a shard of a multi-GPU layout holds just its own cells)
 __global__ void chunk_len_kernel(const int32_t* __restrict__ deg_perm, int64_t n_chunks,
-                                 int64_t C, int32_t* __restrict__ cl,
+                                 int64_t C, int64_t cb, int64_t ce, int32_t* __restrict__ cl,
                                  int64_t* __restrict__ cells) {
   GRID_STRIDE(i, n_chunks) {
     int32_t mx = 0;
     for (int64_t l = 0; l < C; ++l) mx = max(mx, deg_perm[i * C + l]);
     cl[i] = mx;
-    cells[i] = int64_t(mx) * C;
+    cells[i] = i >= cb && i < ce ? int64_t(mx) * C : 0;
   }
+}
+
+// row degrees of the built range's rows (arc offsets), 0 elsewhere
+__global__ void range_deg_kernel(const int32_t* __restrict__ deg_perm, int64_t n_padded, int64_t r0,
+                                 int64_t r1, int64_t* __restrict__ out) {
+  GRID_STRIDE(p, n_padded) out[p] = p >= r0 && p < r1 ? int64_t(deg_perm[p]) : 0;
 }
 
 __global__ void arc_keys_kernel(const uint64_t* __restrict__ keys, int64_t m, int bits,
@@ -109,6 +117,41 @@ __global__ void arc_keys_kernel(const uint64_t* __restrict__ keys, int64_t m, in
 }
 
 // Sorted arcs: arc a is the (a - rowptr[row])-th smallest neighbour of row.
+// Arcs whose row (permuted) lies in [r0, r1) only, compacted through a
+// warp-aggregated counter (their order does not matter: they are sorted).
+__global__ void arc_keys_range_kernel(const uint64_t* __restrict__ keys, int64_t m, int bits,
+                                      const int32_t* __restrict__ inv_perm, int pbits, int64_t r0,
+                                      int64_t r1, unsigned long long* __restrict__ count,
+                                      uint64_t* __restrict__ arcs) {
+  const uint64_t mask = (uint64_t{1} << bits) - 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < m; base += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint64_t k0 = 0, k1 = 0;
+    bool a0 = false, a1 = false;
+    if (i < m) {
+      const int64_t pu = inv_perm[keys[i] >> bits];
+      const int64_t pv = inv_perm[keys[i] & mask];
+      a0 = pu >= r0 && pu < r1;
+      a1 = pv >= r0 && pv < r1;
+      k0 = (uint64_t(pu) << pbits) | uint64_t(pv);
+      k1 = (uint64_t(pv) << pbits) | uint64_t(pu);
+    }
+    const int mine = int(a0) + int(a1);
+    int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long at = 0;
+    if (lane == 31 && total) at = atomicAdd(count, (unsigned long long)total);
+    at = __shfl_sync(0xffffffffu, at, 31) + uint64_t(incl - mine);
+    if (a0) arcs[at++] = k0;
+    if (a1) arcs[at] = k1;
+  }
+}
+
 __global__ void scatter_kernel(const uint64_t* __restrict__ arcs, int64_t n_arcs, int pbits,
                                const int64_t* __restrict__ rowptr,
                                const int64_t* __restrict__ cs, int64_t C,
@@ -157,8 +200,8 @@ void finish_chunks(ssb_graph& g, cudaStream_t s) {
   DevBuf<int64_t> cells(g.n_chunks + 1);
   SSB_CUDA(cudaMemsetAsync(cells.p, 0, 8 * (g.n_chunks + 1), s));
   if (g.n_chunks)
-    chunk_len_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(g.deg.p, g.n_chunks, g.C, g.cl.p,
-                                                          cells.p);
+    chunk_len_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(g.deg.p, g.n_chunks, g.C, g.range_cb,
+                                                          g.range_ce, g.cl.p, cells.p);
   SSB_CUDA(cudaGetLastError());
   exclusive_scan(cells.p, g.cs.p, g.n_chunks + 1, s);
   SSB_CUDA(cudaMemcpyAsync(&g.n_cells, g.cs.p + g.n_chunks, 8, cudaMemcpyDeviceToHost, s));
@@ -167,12 +210,24 @@ void finish_chunks(ssb_graph& g, cudaStream_t s) {
     SSB_CUDA(cudaMemcpyAsync(g.cl_host.data(), g.cl.p, 4 * g.n_chunks, cudaMemcpyDeviceToHost, s));
   g.sc.sync();
   g.max_cl = 0;
-  for (int32_t c : g.cl_host) g.max_cl = std::max<int64_t>(g.max_cl, c);
+  g.total_cells = 0;
+  for (int32_t c : g.cl_host) {
+    g.max_cl = std::max<int64_t>(g.max_cl, c);
+    g.total_cells += int64_t(c) * g.C;
+  }
 }
 
 }  // namespace
 
 ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma) {
+  return build_range_from_edges(e, C, sigma, 0, -1);
+}
+
+// The layout's metadata (perm, inv_perm, row degrees, cl) for every chunk and
+// the cells (cs, col) of chunks [cb, ce) only — one rank's share of a
+// multi-GPU layout; ce < 0 = all chunks.
+ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, int64_t cb,
+                                  int64_t ce) {
   // repr.cpp:63,85
   if (C <= 0) fail(SSB_EINVAL, "chunk height must be positive");
   if (sigma <= 0) fail(SSB_EINVAL, "sorting scope must be positive");
@@ -187,6 +242,11 @@ ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma) {
   g->n_padded = g->n_chunks * C;
   g->nonzeros = 2 * m;
   if (int64_t(g->n_padded) >= (int64_t{1} << 31)) fail(SSB_EINVAL, "n too large");
+  if (ce < 0) ce = g->n_chunks;
+  if (cb < 0 || cb > ce || ce > g->n_chunks) fail(SSB_EINVAL, "chunk range out of bounds");
+  g->range_cb = cb;
+  g->range_ce = ce;
+  const bool partial = cb > 0 || ce < g->n_chunks;
 
   // 1. degrees
   DevBuf<int32_t> deg(std::max<int64_t>(n, 1));
@@ -237,21 +297,38 @@ ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma) {
   //    (repr.cpp:116-128)
   g->col.alloc(std::max<int64_t>(g->n_cells, 1));
   SSB_CUDA(cudaMemsetAsync(g->col.p, 0xff, 4 * std::max<int64_t>(g->n_cells, 1), s));
-  const int64_t na = 2 * m;
+  int64_t na = 2 * m;
   if (na > 0) {
     const int pbits = bits_for_value(uint64_t(std::max<int64_t>(n - 1, 1)));
-    DevBuf<int64_t> rowptr(g->n_padded);
-    {
+    DevBuf<int64_t> rowptr(g->n_padded + 1);
+    if (partial) {
+      // offsets over the range's rows only; na = their arc count
+      DevBuf<int64_t> rd(g->n_padded + 1);
+      range_deg_kernel<<<grid_for(g->n_padded), 256, 0, s>>>(g->deg.p, g->n_padded, cb * C, ce * C,
+                                                             rd.p);
+      SSB_CUDA(cudaGetLastError());
+      SSB_CUDA(cudaMemsetAsync(rd.p + g->n_padded, 0, 8, s));
+      exclusive_scan(rd.p, rowptr.p, g->n_padded + 1, s);
+      SSB_CUDA(cudaMemcpyAsync(&na, rowptr.p + g->n_padded, 8, cudaMemcpyDeviceToHost, s));
+    } else {
       cub::TransformInputIterator<int64_t, I32ToI64, const int32_t*> it(g->deg.p, I32ToI64());
       size_t tb = 0;
       SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, rowptr.p, g->n_padded, s));
       DevBuf<uint8_t> tmp(tb);
       SSB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, it, rowptr.p, g->n_padded, s));
-      g->sc.sync();
     }
-    DevBuf<uint64_t> arcs(na), alt(na);
-    arc_keys_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
-                                                arcs.p);
+    g->sc.sync();
+    DevBuf<uint64_t> arcs(std::max<int64_t>(na, 1)), alt(std::max<int64_t>(na, 1));
+    if (partial) {
+      DevBuf<unsigned long long> cnt(1);
+      SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+      arc_keys_range_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
+                                                        cb * C, ce * C, cnt.p, arcs.p);
+      g->sc.sync();
+    } else {
+      arc_keys_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
+                                                  arcs.p);
+    }
     SSB_CUDA(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> db(arcs.p, alt.p);
     size_t tb = 0;
@@ -266,7 +343,7 @@ ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma) {
                                                 g->C, g->col.p);
     SSB_CUDA(cudaGetLastError());
   }
-  g->padding = g->n_cells - g->nonzeros;
+  g->padding = g->total_cells - g->nonzeros;
   g->sc.sync();
   return g.release();
 }
@@ -334,6 +411,9 @@ ssb_graph* graph_from_host_layout(int64_t n, int64_t C, int64_t sigma, int64_t n
   SSB_CUDA(cudaGetLastError());
   g->max_cl = 0;
   for (int32_t c : g->cl_host) g->max_cl = std::max<int64_t>(g->max_cl, c);
+  g->total_cells = n_cells;
+  g->range_cb = 0;
+  g->range_ce = g->n_chunks;
   g->padding = n_cells - nonzeros;
   g->sc.sync();
   return g.release();

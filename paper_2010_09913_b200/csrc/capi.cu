@@ -168,6 +168,15 @@ int ssb_to_csr(const ssb_edges* e, int64_t* row, int64_t* col) {
 
 void ssb_edges_destroy(ssb_edges* e) { delete e; }
 
+int ssb_build_slimsell_range(const ssb_edges* e, int64_t C, int64_t sigma, int64_t chunk_begin,
+                             int64_t chunk_end, ssb_graph** out) {
+  return guarded([&] {
+    need(e, "edges");
+    need(out, "out");
+    *out = ssb::build_range_from_edges(*e, C, sigma, chunk_begin, chunk_end);
+  });
+}
+
 int ssb_build_slimsell(const ssb_edges* e, int64_t C, int64_t sigma, ssb_graph** out) {
   return guarded([&] {
     need(e, "edges");
@@ -199,9 +208,12 @@ int ssb_graph_info(const ssb_graph* g, ssb_layout_info* info) {
     info->n_padded = g->n_padded;
     info->n_chunks = g->n_chunks;
     info->nonzeros = g->nonzeros;
-    info->n_cells = g->n_cells;
+    info->n_cells = g->total_cells;
     info->padding = g->padding;
     info->max_chunk_len = g->max_cl;
+    info->range_begin = g->range_cb;
+    info->range_end = g->range_ce < 0 ? g->n_chunks : g->range_ce;
+    info->range_cells = g->n_cells;
   });
 }
 
@@ -210,6 +222,7 @@ int ssb_graph_export(const ssb_graph* cg, int64_t* col, int64_t* cs, int64_t* cl
   return guarded([&] {
     need(cg, "graph");
     ssb_graph& g = const_cast<ssb_graph&>(*cg);
+    if (col || cs) g.need_full("ssb_graph_export of col / cs");
     cudaStream_t s = g.sc.s;
     auto widen32 = [&](const int32_t* src, int64_t count, int64_t* dst) {
       if (!dst || count == 0) return;

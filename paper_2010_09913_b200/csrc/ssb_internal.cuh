@@ -132,7 +132,14 @@ struct ssb_bfs_plan {  // cached per slimchunk_len
 // Device-resident SlimSellRepr (repr.hpp:33-55) plus the BFS workspace.
 struct ssb_graph {
   int64_t C = 1, sigma = 1, n = 0, n_padded = 0, n_chunks = 0, nonzeros = 0;
-  int64_t n_cells = 0, padding = 0, max_cl = 0;
+  int64_t n_cells = 0, padding = 0, max_cl = 0;  // n_cells: cells held (the built range)
+  int64_t total_cells = 0;                 // Σ C·cl over the whole layout
+  int64_t range_cb = 0, range_ce = -1;     // chunks whose cells this handle holds (-1: all)
+  bool partial() const { return range_ce >= 0 && (range_cb > 0 || range_ce < n_chunks); }
+  void need_full(const char* what) const {
+    if (partial()) ssb::fail(SSB_EINVAL, std::string(what) + " needs the whole layout (this handle holds chunks [" +
+                                          std::to_string(range_cb) + ", " + std::to_string(range_ce) + ") only)");
+  }
   ssb::DevBuf<int32_t> col;       // n_cells, -1 = padding cell
   ssb::DevBuf<int64_t> cs;        // n_chunks + 1 (cs[n_chunks] = n_cells)
   ssb::DevBuf<int32_t> cl;        // n_chunks
@@ -174,6 +181,7 @@ struct ssb_graph {
 namespace ssb {
 // builder.cu
 ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma);
+ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, int64_t cb, int64_t ce);
 ssb_graph* graph_from_host_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
                                   const int64_t* col, int64_t n_cells, const int64_t* cs,
                                   const int64_t* cl, int64_t n_chunks, const int64_t* perm);

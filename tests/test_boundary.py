@@ -27,7 +27,7 @@ def test_library_exports_header_symbols(libpath):
     lib = ctypes.CDLL(libpath)
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.ssb_abi_version() == 1
+    assert lib.ssb_abi_version() == 2
 
 
 def test_library_is_sm100a_only(libpath):

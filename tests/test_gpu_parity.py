@@ -403,6 +403,48 @@ def test_fused_p2p_default_geometry_matches_single_gpu(ssb):
                 assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == dev_rows(a)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_range_built_shards(ssb, port, world):
+    """ssb_build_slimsell_range: every rank holds only its own chunks' cells
+    (SURVEY.md §8(e)). The cells equal the matching slice of the whole layout,
+    perm / cl / degrees equal the whole layout's, whole-layout calls are
+    refused, and the fused and the host-driven sharded BFS over range-built
+    handles equal the single-GPU result."""
+    from paper_2010_09913_b200.sharding import (DeviceShard, LocalComm, partition_chunks, run_p2p_group,
+                                                run_sharded_bfs)
+    g = ssb.gen_kronecker(18, 16, 4)
+    n = g.num_vertices()
+    full = ssb.build_slimsell(g, 32, n)
+    ranges = partition_chunks(full.cl, 32, world)
+    col = full.col32()
+    cs = full.cs
+    parts = [ssb.build_slimsell(g, 32, n, chunk_range=rg) for rg in ranges]
+    for (b, e), r in zip(ranges, parts):
+        assert (r.range_begin, r.range_end) == (b, e) and r.n_cells == full.n_cells
+        lo = int(cs[b]) if b < full.n_chunks else full.n_cells
+        hi = int(cs[e]) if e < full.n_chunks else full.n_cells
+        assert np.array_equal(r.col32(), col[lo:hi]), (b, e)
+        assert np.array_equal(r.cl, full.cl) and np.array_equal(r.perm, full.perm)
+        assert np.array_equal(r.degrees(), full.degrees())
+        if r.partial:
+            with pytest.raises(ssb.InvalidArgument):
+                ssb.bfs_spmv(r, 0, opts(ssb, 3))
+            with pytest.raises(ssb.InvalidArgument):
+                r.col
+    shards = [DeviceShard(r, b, e) for r, (b, e) in zip(parts, ranges)]
+    for root in (0, 1000, 200000):
+        for v in (3, 0):
+            o = opts(ssb, v, True, 512)
+            a = ssb.bfs_spmv(full, root, o)
+            d1, p1, it1, _ = run_p2p_group(parts, ranges, root, o)
+            d2, p2, it2 = run_sharded_bfs(shards, LocalComm(), root, o)
+            for d, p, it in ((d1, p1, it1), (d2, p2, it2)):
+                assert np.array_equal(d, a.dist), (world, root, v)
+                if v == 3:
+                    assert np.array_equal(p, a.parent), (world, root, v)
+                assert dev_rows(ssb.BfsResult(d, p, len(it), it)) == dev_rows(a)
+
+
 def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
     """The per-rank entry points a multi-GPU job uses (ssb_p2p_window → IPC
     handle, ssb_p2p_attach, ssb_bfs_p2p with the one-launch-per-rank kernel,
