@@ -1357,9 +1357,12 @@ Geometry geometry32(const ssb_graph& g) {
   if (forced == 6 || forced == 8) return geometry32_for(g, forced);
   Geometry G8 = geometry32_for(g, 8);
   // hub-heavy: the prefix catches most probes, keep it large; otherwise most
-  // probes fall in the tail, where a finer summary saves exact lookups
+  // probes fall in the tail, where a finer summary saves exact lookups — if
+  // that summary fits the budget (not at S28: 4x the S = 8 summary)
   if (G8.SW == 0 || prefix_coverage(g, G8.PW) >= 0.5) return G8;
-  return geometry32_for(g, 6);
+  const Geometry G6 = geometry32_for(g, 6);
+  const int64_t budget = int64_t(env_int("SSB_SMEM_KB", kSmemKB)) * 1024;
+  return int64_t(G6.smem) <= budget ? G6 : G8;
 }
 
 // Work units + tasks for the C=32 engine. A unit is a SlimChunk segment of at

@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 
 #include "ssb_internal.cuh"
@@ -25,6 +26,12 @@ int bits_for_value(uint64_t v) {  // bits to hold values in [0, v]
   int b = 1;
   while (b < 64 && (uint64_t{1} << b) <= v) ++b;
   return b;
+}
+
+// SSB_ARCS_PER_PASS: arcs sorted per builder pass (tests force several passes)
+int64_t env_arcs_per_pass() {
+  const char* v = std::getenv("SSB_ARCS_PER_PASS");
+  return v ? std::atoll(v) : 0;
 }
 
 int grid_for(int64_t items, int threads = 256) {
@@ -297,51 +304,73 @@ ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, 
   //    (repr.cpp:116-128)
   g->col.alloc(std::max<int64_t>(g->n_cells, 1));
   SSB_CUDA(cudaMemsetAsync(g->col.p, 0xff, 4 * std::max<int64_t>(g->n_cells, 1), s));
-  int64_t na = 2 * m;
-  if (na > 0) {
+  // Arcs (row, neighbour) of the built range, sorted and scattered in one or
+  // more passes over row sub-ranges: a pass holds 2 x 8 B per arc (sort
+  // double buffer), so a graph whose 2m arcs do not fit beside its col (S28:
+  // 8.4e9 arcs, 135 GB) is built in several passes into the one col array.
+  if (m > 0 && ce > cb) {
     const int pbits = bits_for_value(uint64_t(std::max<int64_t>(n - 1, 1)));
+    // arcs per chunk of the range -> pass boundaries by cumulative arcs
+    std::vector<int64_t> arcs_to(size_t(ce - cb) + 1, 0);
+    {
+      std::vector<int32_t> degp(size_t((ce - cb) * C));
+      SSB_CUDA(cudaMemcpyAsync(degp.data(), g->deg.p + cb * C, 4 * degp.size(), cudaMemcpyDeviceToHost, s));
+      g->sc.sync();
+      for (int64_t i = 0; i < ce - cb; ++i) {
+        int64_t a = 0;
+        for (int64_t l = 0; l < C; ++l) a += degp[size_t(i * C + l)];
+        arcs_to[size_t(i) + 1] = arcs_to[size_t(i)] + a;
+      }
+    }
+    const int64_t total_arcs = arcs_to.back();
+    size_t free_b = 0, tot_b = 0;
+    SSB_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+    const int64_t cap_env = env_arcs_per_pass();
+    // 16 B per arc for the sort's two buffers + ~25% for its temp storage
+    const int64_t per_pass = cap_env > 0 ? cap_env : std::max<int64_t>(int64_t(double(free_b) * 0.6 / 20.0), 1 << 20);
     DevBuf<int64_t> rowptr(g->n_padded + 1);
-    if (partial) {
-      // offsets over the range's rows only; na = their arc count
-      DevBuf<int64_t> rd(g->n_padded + 1);
-      range_deg_kernel<<<grid_for(g->n_padded), 256, 0, s>>>(g->deg.p, g->n_padded, cb * C, ce * C,
-                                                             rd.p);
+    DevBuf<int64_t> rd(g->n_padded + 1);
+    int64_t pc = cb;  // first chunk of the next pass
+    while (pc < ce) {
+      int64_t pe = pc + 1;
+      while (pe < ce && arcs_to[size_t(pe + 1 - cb)] - arcs_to[size_t(pc - cb)] <= per_pass) ++pe;
+      const int64_t r0 = pc * C, r1 = pe * C;
+      // offsets over this pass's rows only; na = their arc count
+      range_deg_kernel<<<grid_for(g->n_padded), 256, 0, s>>>(g->deg.p, g->n_padded, r0, r1, rd.p);
       SSB_CUDA(cudaGetLastError());
       SSB_CUDA(cudaMemsetAsync(rd.p + g->n_padded, 0, 8, s));
       exclusive_scan(rd.p, rowptr.p, g->n_padded + 1, s);
-      SSB_CUDA(cudaMemcpyAsync(&na, rowptr.p + g->n_padded, 8, cudaMemcpyDeviceToHost, s));
-    } else {
-      cub::TransformInputIterator<int64_t, I32ToI64, const int32_t*> it(g->deg.p, I32ToI64());
-      size_t tb = 0;
-      SSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, rowptr.p, g->n_padded, s));
-      DevBuf<uint8_t> tmp(tb);
-      SSB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, it, rowptr.p, g->n_padded, s));
+      const int64_t na = arcs_to[size_t(pe - cb)] - arcs_to[size_t(pc - cb)];
+      if (na > 0) {
+        DevBuf<uint64_t> arcs(na), alt(na);
+        if (!partial && pc == 0 && pe == g->n_chunks) {
+          arc_keys_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits, arcs.p);
+        } else {
+          DevBuf<unsigned long long> cnt(1);
+          SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+          arc_keys_range_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
+                                                            r0, r1, cnt.p, arcs.p);
+          g->sc.sync();
+        }
+        SSB_CUDA(cudaGetLastError());
+        cub::DoubleBuffer<uint64_t> db(arcs.p, alt.p);
+        size_t tb = 0;
+        SSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, na, 0, 2 * pbits, s));
+        {
+          DevBuf<uint8_t> tmp(tb);
+          SSB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, na, 0, 2 * pbits, s));
+          g->sc.sync();
+        }
+        (db.Current() == arcs.p ? alt : arcs).release();
+        scatter_kernel<<<grid_for(na), 256, 0, s>>>(db.Current(), na, pbits, rowptr.p, g->cs.p,
+                                                    g->C, g->col.p);
+        SSB_CUDA(cudaGetLastError());
+        g->sc.sync();
+      }
+      g->build_passes += 1;
+      pc = pe;
     }
-    g->sc.sync();
-    DevBuf<uint64_t> arcs(std::max<int64_t>(na, 1)), alt(std::max<int64_t>(na, 1));
-    if (partial) {
-      DevBuf<unsigned long long> cnt(1);
-      SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
-      arc_keys_range_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
-                                                        cb * C, ce * C, cnt.p, arcs.p);
-      g->sc.sync();
-    } else {
-      arc_keys_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
-                                                  arcs.p);
-    }
-    SSB_CUDA(cudaGetLastError());
-    cub::DoubleBuffer<uint64_t> db(arcs.p, alt.p);
-    size_t tb = 0;
-    SSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, na, 0, 2 * pbits, s));
-    {
-      DevBuf<uint8_t> tmp(tb);
-      SSB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, na, 0, 2 * pbits, s));
-      g->sc.sync();
-    }
-    (db.Current() == arcs.p ? alt : arcs).release();
-    scatter_kernel<<<grid_for(na), 256, 0, s>>>(db.Current(), na, pbits, rowptr.p, g->cs.p,
-                                                g->C, g->col.p);
-    SSB_CUDA(cudaGetLastError());
+    (void)total_arcs;
   }
   g->padding = g->total_cells - g->nonzeros;
   g->sc.sync();

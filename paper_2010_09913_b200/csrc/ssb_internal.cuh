@@ -135,6 +135,7 @@ struct ssb_graph {
   int64_t n_cells = 0, padding = 0, max_cl = 0;  // n_cells: cells held (the built range)
   int64_t total_cells = 0;                 // Σ C·cl over the whole layout
   int64_t range_cb = 0, range_ce = -1;     // chunks whose cells this handle holds (-1: all)
+  int64_t build_passes = 0;                // arc sort passes the builder needed
   bool partial() const { return range_ce >= 0 && (range_cb > 0 || range_ce < n_chunks); }
   void need_full(const char* what) const {
     if (partial()) ssb::fail(SSB_EINVAL, std::string(what) + " needs the whole layout (this handle holds chunks [" +

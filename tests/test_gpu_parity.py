@@ -445,6 +445,25 @@ def test_range_built_shards(ssb, port, world):
                 assert dev_rows(ssb.BfsResult(d, p, len(it), it)) == dev_rows(a)
 
 
+def test_multi_pass_build_equals_single_pass(ssb, monkeypatch):
+    """The builder sorts and scatters arcs in passes over row sub-ranges when
+    2m arcs do not fit beside col (S28 on one B200); forced to many small
+    passes it must produce the identical layout, whole and range-built."""
+    g = ssb.gen_kronecker(17, 16, 6)
+    n = g.num_vertices()
+    ref = ssb.build_slimsell(g, 32, n)
+    col, cl, perm = ref.col32(), ref.cl, ref.perm
+    monkeypatch.setenv("SSB_ARCS_PER_PASS", "50000")
+    r = ssb.build_slimsell(g, 32, n)
+    assert np.array_equal(r.col32(), col) and np.array_equal(r.cl, cl) and np.array_equal(r.perm, perm)
+    b, e = 100, ref.n_chunks - 77
+    part = ssb.build_slimsell(g, 32, n, chunk_range=(b, e))
+    assert np.array_equal(part.col32(), col[int(ref.cs[b]): int(ref.cs[e])])
+    r8 = ssb.build_slimsell(g, 8, 8)
+    monkeypatch.delenv("SSB_ARCS_PER_PASS")
+    assert np.array_equal(r8.col32(), ssb.build_slimsell(g, 8, 8).col32())
+
+
 def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
     """The per-rank entry points a multi-GPU job uses (ssb_p2p_window → IPC
     handle, ssb_p2p_attach, ssb_bfs_p2p with the one-launch-per-rank kernel,
