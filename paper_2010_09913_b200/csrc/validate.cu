@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
 #include "ssb_internal.cuh"
 
 namespace ssb {
@@ -46,13 +47,50 @@ __global__ void both_arcs_kernel(const uint64_t* __restrict__ keys, int64_t m, i
   }
 }
 
-__global__ void split_arcs_kernel(const uint64_t* __restrict__ arcs, int64_t na, int bits,
-                                  int32_t* __restrict__ col, int64_t* __restrict__ deg) {
+__global__ void endpoint_degree_kernel(const uint64_t* __restrict__ keys, int64_t m, int bits,
+                                       int64_t* __restrict__ deg) {
   const uint64_t mask = (uint64_t{1} << bits) - 1;
-  GRID_LOOP(i, na) {
-    col[i] = int32_t(arcs[i] & mask);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&deg[arcs[i] >> bits]), 1ull);
+  GRID_LOOP(i, m) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&deg[keys[i] >> bits]), 1ull);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&deg[keys[i] & mask]), 1ull);
   }
+}
+
+// arcs (u, v) with u in [u0, u1), compacted through a warp-aggregated counter
+__global__ void range_arcs_kernel(const uint64_t* __restrict__ keys, int64_t m, int bits, int64_t u0,
+                                  int64_t u1, unsigned long long* __restrict__ count,
+                                  uint64_t* __restrict__ arcs) {
+  const uint64_t mask = (uint64_t{1} << bits) - 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < m; base += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint64_t u = 0, v = 0;
+    bool a0 = false, a1 = false;
+    if (i < m) {
+      u = keys[i] >> bits;
+      v = keys[i] & mask;
+      a0 = int64_t(u) >= u0 && int64_t(u) < u1;
+      a1 = int64_t(v) >= u0 && int64_t(v) < u1;
+    }
+    const int mine = int(a0) + int(a1);
+    int incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long at = 0;
+    if (lane == 31 && total) at = atomicAdd(count, (unsigned long long)total);
+    at = __shfl_sync(0xffffffffu, at, 31) + uint64_t(incl - mine);
+    if (a0) arcs[at++] = (u << bits) | v;
+    if (a1) arcs[at] = (v << bits) | u;
+  }
+}
+
+__global__ void low_bits_kernel(const uint64_t* __restrict__ arcs, int64_t na, int bits,
+                                int32_t* __restrict__ col) {
+  const uint64_t mask = (uint64_t{1} << bits) - 1;
+  GRID_LOOP(i, na) col[i] = int32_t(arcs[i] & mask);
 }
 
 // ---- queue BFS -------------------------------------------------------------
@@ -189,6 +227,9 @@ struct DevCsr {
   DevBuf<int32_t> col;  // 2m
 };
 
+// Rows from the endpoint degrees, then the arcs sorted and written in passes
+// over row ranges sized to the free memory (one pass up to ~S26; S28's 8.4e9
+// arcs would need 135 GB of sort buffers at once).
 static DevCsr& device_csr(ssb_edges& e) {
   if (e.csr) return *static_cast<DevCsr*>(e.csr.get());
   if (e.n >= (int64_t{1} << 31)) fail(SSB_EINVAL, "device CSR supports n < 2^31");
@@ -198,26 +239,58 @@ static DevCsr& device_csr(ssb_edges& e) {
   c->na = 2 * e.m;
   c->row.alloc(size_t(e.n + 1));
   c->col.alloc(size_t(std::max<int64_t>(c->na, 1)));
-  DevBuf<int64_t> deg{size_t(std::max<int64_t>(e.n, 1))};
-  SSB_CUDA(cudaMemsetAsync(deg.p, 0, deg.bytes(), s));
-  if (c->na > 0) {
-    DevBuf<uint64_t> arcs{size_t(c->na)}, alt{size_t(c->na)};
-    both_arcs_kernel<<<grid_for(e.m), 256, 0, s>>>(e.keys.p, e.m, e.bits, arcs.p);
+  {
+    DevBuf<int64_t> deg{size_t(std::max<int64_t>(e.n, 1))};
+    SSB_CUDA(cudaMemsetAsync(deg.p, 0, deg.bytes(), s));
+    if (e.m > 0) endpoint_degree_kernel<<<grid_for(e.m), 256, 0, s>>>(e.keys.p, e.m, e.bits, deg.p);
     SSB_CUDA(cudaGetLastError());
-    cub::DoubleBuffer<uint64_t> db(arcs.p, alt.p);
-    size_t tb = 0;
-    SSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, c->na, 0, 2 * e.bits, s));
-    DevBuf<uint8_t> tmp(tb);
-    SSB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, c->na, 0, 2 * e.bits, s));
-    split_arcs_kernel<<<grid_for(c->na), 256, 0, s>>>(db.Current(), c->na, e.bits, c->col.p, deg.p);
-    SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaMemsetAsync(c->row.p, 0, 8, s));
+    if (e.n > 0) {
+      size_t tb = 0;
+      SSB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, deg.p, c->row.p + 1, e.n, s));
+      DevBuf<uint8_t> tmp(tb);
+      SSB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, deg.p, c->row.p + 1, e.n, s));
+    }
+    e.sc.sync();
   }
-  SSB_CUDA(cudaMemsetAsync(c->row.p, 0, 8, s));
-  if (e.n > 0) {
-    size_t tb = 0;
-    SSB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, deg.p, c->row.p + 1, e.n, s));
-    DevBuf<uint8_t> tmp(tb);
-    SSB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, deg.p, c->row.p + 1, e.n, s));
+  if (c->na > 0) {
+    std::vector<int64_t> row(size_t(e.n + 1));
+    SSB_CUDA(cudaMemcpy(row.data(), c->row.p, 8 * row.size(), cudaMemcpyDeviceToHost));
+    size_t free_b = 0, tot_b = 0;
+    SSB_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+    const char* ev = std::getenv("SSB_ARCS_PER_PASS");
+    const int64_t per_pass = ev ? std::max<int64_t>(std::atoll(ev), 1)
+                                : std::max<int64_t>(int64_t(double(free_b) * 0.6 / 20.0), 1 << 20);
+    int64_t u0 = 0;
+    while (u0 < e.n) {
+      // the largest row range starting at u0 whose arcs fit a pass (>= 1 row)
+      const int64_t lim = row[size_t(u0)] + per_pass;
+      int64_t u1 = int64_t(std::upper_bound(row.begin() + u0 + 1, row.end(), lim) - row.begin()) - 1;
+      u1 = std::max<int64_t>(u1, u0 + 1);
+      const int64_t na = row[size_t(u1)] - row[size_t(u0)];
+      if (na > 0) {
+        DevBuf<uint64_t> arcs{size_t(na)}, alt{size_t(na)};
+        if (u0 == 0 && u1 == e.n) {
+          both_arcs_kernel<<<grid_for(e.m), 256, 0, s>>>(e.keys.p, e.m, e.bits, arcs.p);
+        } else {
+          DevBuf<unsigned long long> cnt(1);
+          SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+          range_arcs_kernel<<<grid_for(e.m), 256, 0, s>>>(e.keys.p, e.m, e.bits, u0, u1, cnt.p, arcs.p);
+        }
+        SSB_CUDA(cudaGetLastError());
+        cub::DoubleBuffer<uint64_t> db(arcs.p, alt.p);
+        size_t tb = 0;
+        SSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, na, 0, 2 * e.bits, s));
+        {
+          DevBuf<uint8_t> tmp(tb);
+          SSB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, na, 0, 2 * e.bits, s));
+          low_bits_kernel<<<grid_for(na), 256, 0, s>>>(db.Current(), na, e.bits, c->col.p + row[size_t(u0)]);
+          SSB_CUDA(cudaGetLastError());
+          e.sc.sync();
+        }
+      }
+      u0 = u1;
+    }
   }
   e.sc.sync();
   e.csr = c;

@@ -460,8 +460,14 @@ def test_multi_pass_build_equals_single_pass(ssb, monkeypatch):
     part = ssb.build_slimsell(g, 32, n, chunk_range=(b, e))
     assert np.array_equal(part.col32(), col[int(ref.cs[b]): int(ref.cs[e])])
     r8 = ssb.build_slimsell(g, 8, 8)
+    # the validator's / queue BFS's device CSR is built in passes the same way
+    g2 = ssb.gen_kronecker(17, 16, 6)
+    t_multi = ssb.bfs_traditional(g2, 3)
     monkeypatch.delenv("SSB_ARCS_PER_PASS")
     assert np.array_equal(r8.col32(), ssb.build_slimsell(g, 8, 8).col32())
+    t_one = ssb.bfs_traditional(g, 3)
+    assert np.array_equal(t_multi.dist, t_one.dist) and np.array_equal(t_multi.parent, t_one.parent)
+    assert ssb.validate_bfs(g2, 3, t_one.dist, t_one.parent) is None
 
 
 def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
