@@ -66,6 +66,8 @@ def args_():
                     help="multi-GPU decomposition: independent roots per rank (default), "
                          "chunk-range shards with a per-iteration NCCL frontier all-gather, or "
                          "chunk-range shards with the exchange fused into the BFS kernel (p2p)")
+    ap.add_argument("--segments", type=int, default=4,
+                    help="--shard p2p: chunk segments per rank, dealt round-robin (snake order)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="--shard p2p at N=1: run this many ranks as one cooperative launch on "
                          "the single GPU (measures the fused exchange's overhead)")
@@ -594,7 +596,7 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
     import torch
 
     import paper_2010_09913_b200 as ssb
-    from paper_2010_09913_b200.sharding import P2PShard, partition_chunks, run_p2p_group
+    from paper_2010_09913_b200.sharding import P2PShard, partition_segments, run_p2p_group
 
     if world > 1 and torch.cuda.device_count() < world:
         raise SystemExit("--shard p2p needs one GPU per rank")
@@ -621,14 +623,14 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
     roots = graph500_roots(deg, a.roots, a.seed)
     opts = ssb.BfsOptions(variant=ssb.Variant(variant_id), slimwork=slimwork, slimchunk_len=a.slimchunk)
     emu = max(1, a.emulate_ranks) if world == 1 else 1
-    ranges = partition_chunks(meta.cl, 32, emu if emu > 1 else world)
+    ranges = partition_segments(meta.cl, 32, emu if emu > 1 else world, max(1, a.segments))
     del meta
     t0 = time.time()
     if emu > 1:
-        reprs = [ssb.build_slimsell(g, 32, n, chunk_range=rg) for rg in ranges]
+        reprs = [ssb.build_slimsell(g, 32, n, segments=sg) for sg in ranges]
         r = reprs[0]
     else:
-        r = ssb.build_slimsell(g, 32, n, chunk_range=ranges[rank])
+        r = ssb.build_slimsell(g, 32, n, segments=ranges[rank])
     t_build = time.time() - t0
     log(f"graph S{a.scale}: n={n} m={g.num_edges()}, cells of rank 0's range {r.range_cells} "
         f"of {r.n_cells}; gen {t_gen:.2f}s build {t_build:.2f}s")
@@ -639,7 +641,7 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
             d, p, per_iter, ms = run_p2p_group(reprs, ranges, root, opts, fetch=fetch)
             return ms, d
     else:
-        shard = P2PShard(r, *ranges[rank])
+        shard = P2PShard(r, ranges[rank])
         if world > 1:
             shard.attach_dist()
         else:
@@ -685,8 +687,10 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         max_ms = float(t.item())
     value = sum(mcc.values()) / (max_ms * 1e-3) / 1e9
-    par = (f"chunk-range shards x{world}, fused in-kernel frontier exchange" if emu == 1 else
-           f"{emu} chunk-range shards emulated in one launch on 1 GPU, fused in-kernel exchange")
+    par = (f"chunk-range shards x{world} ({a.segments} round-robin segments each), fused in-kernel "
+           f"frontier exchange" if emu == 1 else
+           f"{emu} chunk-range shards ({a.segments} round-robin segments each) emulated in one launch on "
+           f"1 GPU, fused in-kernel exchange")
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(max_ms, 3), "higher_is_better": True,

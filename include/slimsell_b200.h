@@ -47,12 +47,14 @@ typedef struct ssb_edges ssb_edges; /* normalised Graph on the device (graph.hpp
 typedef struct ssb_graph ssb_graph; /* SlimSellRepr on the device (repr.hpp:33-55) */
 
 /* SlimSellRepr scalar fields (repr.hpp:33-45). n_cells = |col| = Σ C·cl of
- * the whole layout. A handle built for a chunk range (ssb_build_slimsell_range)
- * holds the cells of chunks [range_begin, range_end) only: range_cells of
- * them; a whole layout has range [0, n_chunks) and range_cells = n_cells. */
+ * the whole layout. A handle built for chunk segments
+ * (ssb_build_slimsell_range / _segments) holds the cells of those chunks
+ * only: range_cells of them, in range_segments segments spanning
+ * [range_begin, range_end); a whole layout has one segment [0, n_chunks) and
+ * range_cells = n_cells. */
 typedef struct {
   int64_t C, sigma, n, n_padded, n_chunks, nonzeros, n_cells, padding, max_chunk_len;
-  int64_t range_begin, range_end, range_cells;
+  int64_t range_begin, range_end, range_cells, range_segments;
 } ssb_layout_info;
 
 /* BfsOptions (bfs.hpp:16-24). schedule and workers are accepted for API
@@ -136,6 +138,11 @@ int ssb_build_slimsell(const ssb_edges* e, int64_t C, int64_t sigma, ssb_graph**
  * EINVAL. chunk_end < 0 = n_chunks. */
 int ssb_build_slimsell_range(const ssb_edges* e, int64_t C, int64_t sigma, int64_t chunk_begin,
                              int64_t chunk_end, ssb_graph** out);
+/* The same for several chunk segments (bounds = 2·nseg chunk indices
+ * [b0, e0, b1, e1, ...], disjoint): the round-robin partition that keeps the
+ * ranks balanced once SlimWork skips the hub chunks. */
+int ssb_build_slimsell_segments(const ssb_edges* e, int64_t C, int64_t sigma, const int64_t* bounds,
+                                int64_t nseg, ssb_graph** out);
 /* Uploads a host SlimSellRepr (the reference struct's arrays, int64). */
 int ssb_graph_from_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
                           const int64_t* col, int64_t n_cells, const int64_t* cs,
@@ -222,17 +229,23 @@ int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* 
  * ssb_bfs_p2p: one BFS from `root` on this rank; every rank calls it with
  *   the same root and options. stats: this rank's counters (sum over ranks
  *   for the reference's IterStats). Results: ssb_bfs_shard_fetch (owned rows).
- * ssb_bfs_p2p_group: `world` shards (2..4 handles on THIS device, ranges =
- *   2·world chunk bounds) run as one cooperative launch — the same kernel
- *   and exchange code, peers being plain device memory; stats summed. */
+ * ssb_bfs_p2p_group: `world` shards (2..4 handles on THIS device) run as one
+ *   cooperative launch — the same kernel and exchange code, peers being
+ *   plain device memory; stats summed. */
 int ssb_p2p_window(ssb_graph* g, void* ipc_handle, int64_t* window_bytes);
 int ssb_p2p_attach(ssb_graph* g, int rank, int world, const void* ipc_handles,
                    int64_t chunk_begin, int64_t chunk_end);
+/* ... owning several chunk segments (bounds = 2·nseg, disjoint, nseg <= 8). */
+int ssb_p2p_attach_segments(ssb_graph* g, int rank, int world, const void* ipc_handles,
+                            const int64_t* bounds, int64_t nseg);
 int ssb_bfs_p2p(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, ssb_iter_stats* stats,
                 int64_t stats_cap, int64_t* iterations, double* device_ms);
-int ssb_bfs_p2p_group(ssb_graph* const* shards, int world, const int64_t* ranges, int64_t root,
-                      const ssb_bfs_options* opts, ssb_iter_stats* stats, int64_t stats_cap,
-                      int64_t* iterations, double* device_ms);
+/* bounds: every rank's segments in rank order; seg_counts[i] = rank i's
+ * segment count (NULL: one each, bounds = 2·world). */
+int ssb_bfs_p2p_group(ssb_graph* const* shards, int world, const int64_t* bounds,
+                      const int64_t* seg_counts, int64_t root, const ssb_bfs_options* opts,
+                      ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations,
+                      double* device_ms);
 /* ---- checking at scale --------------------------------
  * bfs_traditional (bfs.hpp:83, bfs.cpp:248-286) on the device: an independent
  * level-synchronous queue BFS over the CSR of original ids; parent = the

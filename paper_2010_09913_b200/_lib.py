@@ -22,7 +22,7 @@ i32p = C.POINTER(C.c_int32)
 class LayoutInfo(C.Structure):
     _fields_ = [(k, C.c_int64) for k in ("C", "sigma", "n", "n_padded", "n_chunks", "nonzeros",
                                          "n_cells", "padding", "max_chunk_len", "range_begin",
-                                         "range_end", "range_cells")]
+                                         "range_end", "range_cells", "range_segments")]
 
 
 class BfsOptionsC(C.Structure):
@@ -77,6 +77,7 @@ def lib() -> C.CDLL:
         "ssb_edges_destroy": (None, [vp]),
         "ssb_build_slimsell": (C.c_int, [vp, C.c_int64, C.c_int64, pvp]),
         "ssb_build_slimsell_range": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, pvp]),
+        "ssb_build_slimsell_segments": (C.c_int, [vp, C.c_int64, C.c_int64, i64p, C.c_int64, pvp]),
         "ssb_graph_from_layout": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, i64p, C.c_int64,
                                             i64p, i64p, C.c_int64, i64p, pvp]),
         "ssb_graph_info": (C.c_int, [vp, C.POINTER(LayoutInfo)]),
@@ -103,7 +104,8 @@ def lib() -> C.CDLL:
         "ssb_p2p_attach": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int64]),
         "ssb_bfs_p2p": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.POINTER(IterStatsC), C.c_int64,
                                   i64p, C.POINTER(C.c_double)]),
-        "ssb_bfs_p2p_group": (C.c_int, [pvp, C.c_int, i64p, C.c_int64, C.POINTER(BfsOptionsC),
+        "ssb_p2p_attach_segments": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, i64p, C.c_int64]),
+        "ssb_bfs_p2p_group": (C.c_int, [pvp, C.c_int, i64p, i64p, C.c_int64, C.POINTER(BfsOptionsC),
                                         C.POINTER(IterStatsC), C.c_int64, i64p, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():

@@ -273,11 +273,12 @@ class SlimSellRepr:
         # cells held: chunks [range_begin, range_end) (the whole layout unless
         # built with build_slimsell(..., chunk_range=...))
         self.range_begin, self.range_end, self.range_cells = info.range_begin, info.range_end, info.range_cells
+        self.range_segments = info.range_segments
         self._host = {}
 
     @property
     def partial(self) -> bool:
-        return self.range_begin > 0 or self.range_end < self.n_chunks
+        return self.range_segments != 1 or self.range_begin > 0 or self.range_end < self.n_chunks
 
     def _export(self, name):
         if name not in self._host:
@@ -328,12 +329,15 @@ class SlimSellRepr:
             self._h = None
 
 
-def build_slimsell(g: Graph, C_: int, sigma: int, chunk_range=None) -> SlimSellRepr:  # repr.hpp:66
-    """build_slimsell on the device. chunk_range=(b, e): one rank's share of a
-    multi-GPU layout — the whole layout's perm / cl, the cells of chunks
-    [b, e) only (ssb_build_slimsell_range)."""
+def build_slimsell(g: Graph, C_: int, sigma: int, chunk_range=None, segments=None) -> SlimSellRepr:  # repr.hpp:66
+    """build_slimsell on the device. chunk_range=(b, e) or segments=[(b, e),
+    ...]: one rank's share of a multi-GPU layout — the whole layout's perm /
+    cl, the cells of those chunks only (ssb_build_slimsell_range/_segments)."""
     h = C.c_void_p()
-    if chunk_range is None:
+    if segments is not None:
+        b = np.array([x for seg in segments for x in seg], dtype=np.int64)
+        _check(_L.lib().ssb_build_slimsell_segments(g._h, C_, sigma, _p(b), len(segments), C.byref(h)))
+    elif chunk_range is None:
         _check(_L.lib().ssb_build_slimsell(g._h, C_, sigma, C.byref(h)))
     else:
         b, e = chunk_range

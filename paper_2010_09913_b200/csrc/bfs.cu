@@ -198,6 +198,7 @@ struct Args32 {
 // per-iteration all-gather + is_converged without leaving the kernel.
 constexpr int kMaxRanks = 8;
 constexpr int kSlotRing = 64;  // generations of |newly| slots kept in a window
+constexpr int kMaxSeg = 8;     // owned chunk segments per rank
 struct P2PArgs {
   uint32_t* win[kMaxRanks];    // every rank's window base (peer-mapped)
   int64_t offF[2];             // word offsets of F0 / F1 in a window
@@ -207,8 +208,9 @@ struct P2PArgs {
   unsigned long long gen_base; // barrier generations completed before this launch
   unsigned long long arrivals; // CTAs per generation over all ranks
   int32_t rank, world;
-  int32_t wcb, wce;            // owned frontier words (= chunks, C = 32)
-  int32_t sw0, sw1;            // owned summary words
+  int32_t nseg;                // owned chunk segments (round-robin partitions)
+  int32_t wseg[2 * kMaxSeg];   // their frontier words [b, e) (= chunks, C = 32)
+  int32_t sseg[2 * kMaxSeg];   // their summary words [b, e) (shared at the ends)
 };
 constexpr int kMaxVRanks = 4;  // ranks emulated in one launch (single-GPU tests)
 struct GroupArgs {
@@ -703,12 +705,14 @@ __device__ __forceinline__ int64_t p2p_exchange(const P2PArgs& x, int32_t k, con
   for (int r = 0; r < x.world; ++r) {
     if (r == x.rank) continue;
     uint32_t* pf = x.win[r] + x.offF[k & 1];
-    for (int32_t w = x.wcb + tid; w < x.wce; w += nth) pf[w] = __ldcg(Fn + w);
-    // summary words at the range ends are shared with the neighbouring ranks
     uint32_t* ps = x.win[r] + x.offS[k % 3];
-    for (int32_t w = x.sw0 + tid; w < x.sw1; w += nth) {
-      const uint32_t v = __ldcg(Sn + w);
-      if (v) atomicOr_system(&ps[w], v);
+    for (int q = 0; q < x.nseg; ++q) {
+      for (int32_t w = x.wseg[2 * q] + tid; w < x.wseg[2 * q + 1]; w += nth) pf[w] = __ldcg(Fn + w);
+      // summary words at the segment ends are shared with other ranks
+      for (int32_t w = x.sseg[2 * q] + tid; w < x.sseg[2 * q + 1]; w += nth) {
+        const uint32_t v = __ldcg(Sn + w);
+        if (v) atomicOr_system(&ps[w], v);
+      }
     }
   }
   const int slot = int(gen % kSlotRing) * kMaxRanks;
@@ -1223,10 +1227,10 @@ __global__ void unpermute_kernel(const uint32_t* __restrict__ visited,
                                  const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ inv_perm, int64_t n,
                                  int selmax_parents, int64_t* __restrict__ dist,
-                                 int64_t* __restrict__ par, int64_t pb, int64_t pe) {
+                                 int64_t* __restrict__ par, const uint8_t* __restrict__ owned) {
   GRID_STRIDE(o, n) {
     const int32_t p = inv_perm[o];
-    if (p < pb || p >= pe) continue;  // another shard's row
+    if (owned && !owned[p >> 5]) continue;  // another shard's row (C = 32: chunk = p / 32)
     const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
     if (dist) dist[o] = reached ? int64_t(level[p]) : INT64_MAX;
     if (selmax_parents) par[o] = reached ? int64_t(perm[parent[p]]) : -1;
@@ -1242,12 +1246,12 @@ __global__ void dp_parent_kernel(const int32_t* __restrict__ col, const int64_t*
                                  const int32_t* __restrict__ level,
                                  const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ inv_perm, int64_t n,
-                                 T* __restrict__ par, int* __restrict__ bad, int64_t pb,
-                                 int64_t pe, int64_t o0 = 0) {
+                                 T* __restrict__ par, int* __restrict__ bad,
+                                 const uint8_t* __restrict__ owned, int64_t o0 = 0) {
   GRID_STRIDE(i, n - o0) {
     const int64_t o = o0 + i;
     const int32_t p = inv_perm[o];
-    if (p < pb || p >= pe) continue;  // another shard's row
+    if (owned && !owned[p / C]) continue;  // another shard's row
     if (!((visited[p >> 5] >> (p & 31)) & 1u)) {
       par[o] = -1;
       continue;
@@ -1369,7 +1373,8 @@ Geometry geometry32(const ssb_graph& g) {
 // most L columns (the whole chunk when L <= 0, as the reference's task list,
 // bfs.cpp:122-138); a task groups up to 32 consecutive units whose cost stays
 // under a budget, the grain of the dynamic scheduler.
-void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
+// segs: the chunk segments this plan covers, [b0, e0, b1, e1, ...]
+void build_plan32(ssb_graph& g, int64_t L, const std::vector<int64_t>& segs) {
   ssb_bfs_plan& P = g.plan;
   // Units are SlimChunk segments of at most Lu columns: the reference's L
   // (which alone defines the subchunks_processed counter, computed
@@ -1383,25 +1388,25 @@ void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
     // the largest power of two (64 .. 4096) not above one warp's share of a
     // full sweep (A/B S22: 4096 113.8, 512 136.4, 128 131.6 GTEPS); the range
     // sum is host work, cached with the range
-    if (!(P.cap_cb == cb && P.cap_ce == ce)) {
+    if (P.cap_segs != segs) {
       int64_t cols = 0;
-      for (int64_t i = cb; i < ce; ++i) cols += g.cl_host[size_t(i)];
+      for (size_t q = 0; q + 1 < segs.size(); q += 2)
+        for (int64_t i = segs[q]; i < segs[q + 1]; ++i) cols += g.cl_host[size_t(i)];
       const int64_t per_warp = cols / (int64_t(num_sms()) * (kThreads / 32));
       int64_t c = 64;
       while (c * 2 <= per_warp && c < 4096) c *= 2;
       P.cap_auto = c;
-      P.cap_cb = cb;
-      P.cap_ce = ce;
+      P.cap_segs = segs;
     }
     cap = P.cap_auto;
   }
   const int64_t Lu = L > 0 ? std::min(L, cap) : cap;
-  if (P.L == L && P.Lu == Lu && P.cb == cb && P.ce == ce && P.built) return;
+  if (P.L == L && P.Lu == Lu && P.segs == segs && P.built) return;
   std::vector<ssb_unit> units;
   std::vector<int32_t> split_units;
-  units.reserve(ce - cb + 16);
   P.empty_chunks = 0;
-  for (int64_t i = cb; i < ce; ++i) {
+  for (size_t q = 0; q + 1 < segs.size(); q += 2)
+  for (int64_t i = segs[q]; i < segs[q + 1]; ++i) {
     const int64_t cl = g.cl_host[i];
     if (cl == 0) {
       // Chunks without cells (all rows isolated; 1.07M of 2.1M at S26) can
@@ -1438,8 +1443,7 @@ void build_plan32(ssb_graph& g, int64_t L, int64_t cb, int64_t ce) {
   cudaStream_t s = g.sc.s;
   P.L = L;
   P.Lu = Lu;
-  P.cb = cb;
-  P.ce = ce;
+  P.segs = segs;
   P.built = true;
   P.n_units = int64_t(units.size());
   P.n_tasks = int64_t(tb.size()) - 1;
@@ -1528,7 +1532,7 @@ struct Run32 {
   std::vector<int64_t> rec;
   bool stepping = false;         // shard mode: always carry state to the next launch
   bool zeroed = false;           // stats/control words already clear for the next launch
-  int64_t cb = 0, ce = 0;        // owned chunk range
+  std::vector<int64_t> segs;     // owned chunk segments
 };
 
 // The shared-memory image geometry depends on the layout and the SSB_* knobs
@@ -1568,7 +1572,7 @@ WinGeom win_geom(ssb_graph& g) {
 
 struct P2PHost {
   int rank = 0, world = 1;
-  int64_t cb = 0, ce = 0;
+  std::vector<int64_t> segs;  // owned chunk segments
   uint32_t* win[kMaxRanks] = {};
   std::vector<void*> opened;  // peer windows mapped through CUDA IPC
   unsigned long long gen = 0;  // barrier generations completed
@@ -1595,12 +1599,13 @@ uint32_t* p2p_window_alloc(ssb_graph& g, WinGeom& wg) {
 // chunk range [cb, ce) (all chunks for a single-GPU BFS). With a window (a
 // fused multi-GPU shard) the frontier and summaries live in the window.
 Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
-                int64_t cb, int64_t ce, const P2PHost* p2p = nullptr) {
+                const std::vector<int64_t>& segs, const P2PHost* p2p = nullptr) {
   cudaStream_t s = g.sc.s;
   Run32 r;
   r.sel = o.variant == SSB_SELMAX;
   r.root_pos = root_pos;
-  build_plan32(g, o.slimchunk_len, cb, ce);
+  build_plan32(g, o.slimchunk_len, segs);
+  r.segs = segs;
   r.G = cached_geometry(g);
   const Geometry& G = r.G;
   BitRegions R = bit_regions(g, G.SW);
@@ -1742,7 +1747,9 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   // chunks without cells are processed (0 columns, 0 segments) unless SlimWork
   // skips the root's own chunk when the root is its only real row
   const int64_t rc = root_pos / 32;
-  r.z_skip = o.slimwork && rc >= cb && rc < ce && g.cl_host[rc] == 0 &&
+  bool owns_rc = false;
+  for (size_t q = 0; q + 1 < segs.size(); q += 2) owns_rc = owns_rc || (rc >= segs[q] && rc < segs[q + 1]);
+  r.z_skip = o.slimwork && owns_rc && g.cl_host[rc] == 0 &&
              std::min<int64_t>(32, g.n - rc * 32) == 1;
   r.rec.resize(size_t(kItersPerLaunch) * kStatW);
   r.k = 1;
@@ -1859,7 +1866,7 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
 bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
            int64_t cap, std::vector<ssb_iter_stats>& stats) {
   const auto h0 = std::chrono::steady_clock::now();
-  Run32 r = prepare32(g, root_pos, root_code, o, 0, g.n_chunks);
+  Run32 r = prepare32(g, root_pos, root_code, o, {0, g.n_chunks});
   if (std::getenv("SSB_GAPS"))
     fprintf(stderr, "[ssb gaps] host prepare32 %.1f us\n",
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
@@ -2023,11 +2030,11 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
 }
 
 void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
-                int64_t* parent_len, int64_t pb, int64_t pe);
+                int64_t* parent_len, const uint8_t* owned);
 
 void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
                int64_t* parent_len) {
-  fetch_rows(g, want_parents, dist, parent, parent_len, 0, g.n_padded);
+  fetch_rows(g, want_parents, dist, parent, parent_len, nullptr);
 }
 
 // Pinned host copy of the wire buffer and the per-chunk completion events.
@@ -2090,7 +2097,7 @@ void fetch_wire(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent, 
       if (dp && want_p)
         dp_parent_kernel<int32_t><<<grid_for(len), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
                                                                 g.level.p, g.perm.p, g.inv_perm.p, b + len,
-                                                                par32, g.flag.p, 0, g.n_padded, b);
+                                                                par32, g.flag.p, nullptr, b);
       SSB_CUDA(cudaGetLastError());
     }
     if (len > 0 && dist)
@@ -2106,9 +2113,10 @@ void fetch_wire(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent, 
   if (parent_len) *parent_len = want_parents ? n : 0;
 }
 
-// Results of the rows at positions [pb, pe) only (a shard), original ids.
+// Results in original ids; owned (device, per chunk, may be null = all): only
+// the rows of a shard's chunks, the caller's other entries kept.
 void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
-                int64_t* parent_len, int64_t pb, int64_t pe) {
+                int64_t* parent_len, const uint8_t* owned) {
   if (!g.last_valid) fail(SSB_EINVAL, "no BFS result on this graph");
   cudaStream_t s = g.sc.s;
   const int64_t n = g.n;
@@ -2118,7 +2126,7 @@ void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
   }
   // whole results of shallow BFS (levels fit a byte) of graphs worth it take
   // the narrow wire format (SSB_WIRE=0: the direct int64 path below)
-  const bool whole = pb <= 0 && pe >= g.n_padded;
+  const bool whole = owned == nullptr;
   if (whole && g.last_iterations <= 254 && n >= env_int("SSB_WIRE_MIN", 1 << 16) &&
       env_int("SSB_WIRE", 1) != 0) {
     fetch_wire(g, want_parents, dist, parent, parent_len);
@@ -2142,14 +2150,14 @@ void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
   if ((dist && !dd) || (want_parents && parent && !dp)) g.stage.ensure(size_t(2 * n));
   int64_t* d_out = dd ? dd : (dist ? g.stage.p : nullptr);
   int64_t* p_out = dp ? dp : (want_parents && parent ? g.stage.p + n : nullptr);
-  const bool partial = pb > 0 || pe < g.n_padded;  // a shard: keep the caller's other rows
+  const bool partial = !whole;  // a shard: keep the caller's other rows
   if (partial && dist && !dd)
     SSB_CUDA(cudaMemcpyAsync(d_out, dist, 8 * n, cudaMemcpyHostToDevice, s));
   if (partial && p_out && !dp)
     SSB_CUDA(cudaMemcpyAsync(p_out, parent, 8 * n, cudaMemcpyHostToDevice, s));
   unpermute_kernel<<<grid_for(n), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
                                                g.inv_perm.p, n, sel && p_out != nullptr, d_out,
-                                               p_out, pb, pe);
+                                               p_out, owned);
   SSB_CUDA(cudaGetLastError());
   int64_t plen = 0;
   if (want_parents && !sel) {
@@ -2158,7 +2166,7 @@ void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
     if (p_out)
       dp_parent_kernel<int64_t><<<grid_for(n), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
                                                    g.level.p, g.perm.p, g.inv_perm.p, n, p_out,
-                                                   g.flag.p, pb, pe);
+                                                   g.flag.p, owned);
     SSB_CUDA(cudaGetLastError());
     int hbad = 0;
     SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
@@ -2182,14 +2190,23 @@ struct ShardState {
   Run32 r;
   ssb_bfs_options o;
   std::vector<ssb_iter_stats> stats;
+  DevBuf<uint8_t> owned;  // per chunk: owned by this rank (result fetch)
 };
+
+// device mask of the owned chunks of a segment list
+void owned_mask(const ssb_graph& g, const std::vector<int64_t>& segs, DevBuf<uint8_t>& out) {
+  std::vector<uint8_t> h(size_t(std::max<int64_t>(g.n_chunks, 1)), 0);
+  for (size_t q = 0; q + 1 < segs.size(); q += 2)
+    for (int64_t c = segs[q]; c < segs[q + 1]; ++c) h[size_t(c)] = 1;
+  out.alloc(h.size());
+  SSB_CUDA(cudaMemcpy(out.p, h.data(), h.size(), cudaMemcpyHostToDevice));
+}
 
 void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t cb, int64_t ce) {
   if (g.C != 32) fail(SSB_EINVAL, "sharded BFS needs the C = 32 layout");
   if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
   if (cb < 0 || ce > g.n_chunks || cb > ce) fail(SSB_EINVAL, "chunk range out of bounds");
-  if (g.partial() && cb < ce && (cb < g.range_cb || ce > g.range_ce))
-    fail(SSB_EINVAL, "owned chunks outside the range this handle holds");
+  if (!g.holds(cb, ce)) fail(SSB_EINVAL, "owned chunks outside the segments this handle holds");
   if (root < 0 || root >= g.n)
     fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g.n) + ")");
   int32_t root_pos = 0;
@@ -2200,10 +2217,9 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
   g.last_kernel_ms = 0;
   g.last_launches = 0;
   g.last_swept = 0;
-  st->r = prepare32(g, root_pos, root_code, o, cb, ce);
+  st->r = prepare32(g, root_pos, root_code, o, {cb, ce});
   st->r.stepping = true;
-  st->r.cb = cb;
-  st->r.ce = ce;
+  owned_mask(g, st->r.segs, st->owned);
   st->o = o;
   g.shard = st;
   g.last_root = root;
@@ -2223,8 +2239,9 @@ void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words) {
   if (local) *local = one.front();
   st->stats.push_back(one.front());
   const uint32_t* Fn = (k & 1) ? r.a.F1 : r.a.F0;
-  if (owned_words && r.ce > r.cb)
-    SSB_CUDA(cudaMemcpyAsync(owned_words, Fn + r.cb, 4 * (r.ce - r.cb), cudaMemcpyDeviceToDevice,
+  const int64_t cb = r.segs[0], ce = r.segs[1];
+  if (owned_words && ce > cb)
+    SSB_CUDA(cudaMemcpyAsync(owned_words, Fn + cb, 4 * (ce - cb), cudaMemcpyDeviceToDevice,
                              g.sc.s));
   g.sc.sync();
 }
@@ -2255,7 +2272,7 @@ void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent)
   auto st = std::static_pointer_cast<ShardState>(g.shard);
   if (!st) fail(SSB_EINVAL, "no sharded BFS (ssb_bfs_shard_begin)");
   g.last_valid = true;
-  fetch_rows(g, want_parents, dist, parent, nullptr, st->r.cb * 32, st->r.ce * 32);
+  fetch_rows(g, want_parents, dist, parent, nullptr, st->owned.p);
 }
 
 // ---- fused multi-GPU chunk-range BFS (frontier exchange inside the kernel) ----
@@ -2271,26 +2288,27 @@ void p2p_window(ssb_graph& g, void* ipc_handle, int64_t* bytes) {
   }
 }
 
-void check_range(ssb_graph& g, int64_t cb, int64_t ce) {
-  if (cb < 0 || ce > g.n_chunks || cb > ce) fail(SSB_EINVAL, "chunk range out of bounds");
-  if (g.partial() && cb < ce && (cb < g.range_cb || ce > g.range_ce))
-    fail(SSB_EINVAL, "owned chunks outside the range this handle holds");
+std::vector<int64_t> check_segments(ssb_graph& g, const int64_t* bounds, int64_t nseg) {
+  std::vector<int64_t> segs = normalize_segments(bounds, nseg, g.n_chunks);
+  if (int64_t(segs.size() / 2) > kMaxSeg) fail(SSB_EINVAL, "at most 8 owned segments per rank");
+  if (!g.holds_segments(segs)) fail(SSB_EINVAL, "owned chunks outside the segments this handle holds");
+  return segs;
 }
 
 // Maps every peer's window (CUDA IPC; peer access over NVLink). Collective in
 // spirit: every rank attaches before any rank runs a BFS, and the windows'
 // arrival counters start at zero together.
-void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, int64_t cb, int64_t ce) {
+void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, const int64_t* bounds,
+                int64_t nseg) {
   if (world < 1 || world > kMaxRanks) fail(SSB_EINVAL, "world must be in [1, 8]");
   if (rank < 0 || rank >= world) fail(SSB_EINVAL, "rank outside [0, world)");
-  check_range(g, cb, ce);
+  const std::vector<int64_t> segs = check_segments(g, bounds, nseg);
   auto h = std::make_shared<P2PHost>();
   uint32_t* mine = p2p_window_alloc(g, h->wg);
   SSB_CUDA(cudaMemset(mine, 0, g.p2p_win.bytes()));
   h->rank = rank;
   h->world = world;
-  h->cb = cb;
-  h->ce = ce;
+  h->segs = segs;
   for (int r = 0; r < world; ++r) {
     if (r == rank) {
       h->win[r] = mine;
@@ -2319,14 +2337,18 @@ P2PArgs p2p_args(const ssb_graph& g, const P2PHost& h, const Geometry& G, unsign
   x.arrivals = arrivals;
   x.rank = h.rank;
   x.world = h.world;
-  x.wcb = int32_t(h.cb);
-  x.wce = int32_t(h.ce);
-  // summary words holding bits of the owned chunks (shared at the range ends)
-  x.sw0 = x.sw1 = 0;
-  const int64_t lo = std::max<int64_t>(h.cb, G.PW);
-  if (G.SW > 0 && h.ce > lo) {
-    x.sw0 = int32_t(((lo - G.PW) >> G.gshift) >> 5);
-    x.sw1 = int32_t((((h.ce - 1 - G.PW) >> G.gshift) >> 5) + 1);
+  x.nseg = int32_t(h.segs.size() / 2);
+  for (int q = 0; q < x.nseg; ++q) {
+    const int64_t cb = h.segs[size_t(2 * q)], ce = h.segs[size_t(2 * q + 1)];
+    x.wseg[2 * q] = int32_t(cb);
+    x.wseg[2 * q + 1] = int32_t(ce);
+    // summary words holding bits of the segment's chunks
+    x.sseg[2 * q] = x.sseg[2 * q + 1] = 0;
+    const int64_t lo = std::max<int64_t>(cb, G.PW);
+    if (G.SW > 0 && ce > lo) {
+      x.sseg[2 * q] = int32_t(((lo - G.PW) >> G.gshift) >> 5);
+      x.sseg[2 * q + 1] = int32_t((((ce - 1 - G.PW) >> G.gshift) >> 5) + 1);
+    }
   }
   (void)g;
   return x;
@@ -2346,8 +2368,8 @@ const void* bfs32p_fn(bool sel, int S, bool group) {
 // p2p_attach); n_local > 1: all ranks emulated on this device in ONE
 // cooperative launch (ranges[2i], ranges[2i+1] = rank i's chunk range).
 // stats: per iteration, counters summed over the local shards.
-int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t root,
-            const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
+int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* bounds, const int64_t* seg_counts,
+            int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
             int64_t* iterations, double* device_ms) {
   if (n_local < 1 || n_local > kMaxVRanks) fail(SSB_EINVAL, "local shards must be in [1, 4]");
   if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
@@ -2364,8 +2386,12 @@ int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t ro
     // emulated group: the windows are plain device memory of this device
     std::vector<uint32_t*> wins(static_cast<size_t>(n_local));
     std::vector<std::shared_ptr<P2PHost>> hs(static_cast<size_t>(n_local));
+    std::vector<std::vector<int64_t>> segs(static_cast<size_t>(n_local));
+    int64_t at = 0;  // bounds offset of rank i's segments
     for (int i = 0; i < n_local; ++i) {
-      check_range(*gs[i], ranges[2 * i], ranges[2 * i + 1]);
+      const int64_t ns = seg_counts ? seg_counts[i] : 1;
+      segs[size_t(i)] = check_segments(*gs[i], bounds + 2 * at, ns);
+      at += ns;
       auto* prev = static_cast<P2PHost*>(gs[i]->p2p.get());
       hs[size_t(i)] = std::make_shared<P2PHost>();
       wins[size_t(i)] = p2p_window_alloc(*gs[i], hs[size_t(i)]->wg);
@@ -2384,8 +2410,7 @@ int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t ro
       P2PHost& h = *hs[size_t(i)];
       h.rank = i;
       h.world = n_local;
-      h.cb = ranges[2 * i];
-      h.ce = ranges[2 * i + 1];
+      h.segs = segs[size_t(i)];
       for (int r = 0; r < n_local; ++r) h.win[r] = wins[size_t(r)];
       if (gen == ~0ull) {  // a new group: restart the barrier counters together
         SSB_CUDA(cudaMemset(wins[size_t(i)], 0, gs[i]->p2p_win.bytes()));
@@ -2416,7 +2441,7 @@ int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t ro
     g.last_launches = 0;
     g.last_swept = 0;
     g.last_valid = false;
-    rs.push_back(prepare32(g, root_pos, root_code, o, H[size_t(i)]->cb, H[size_t(i)]->ce, H[size_t(i)]));
+    rs.push_back(prepare32(g, root_pos, root_code, o, H[size_t(i)]->segs, H[size_t(i)]));
   }
   const Geometry G = rs[0].G;
   const bool sel = rs[0].sel;
@@ -2547,8 +2572,7 @@ int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t ro
     g.last_valid = true;
     auto ss = std::make_shared<ShardState>();
     ss->r = rs[size_t(i)];
-    ss->r.cb = H[size_t(i)]->cb;
-    ss->r.ce = H[size_t(i)]->ce;
+    owned_mask(g, ss->r.segs, ss->owned);
     ss->o = o;
     ss->stats = st[size_t(i)];
     g.shard = ss;  // results of the owned rows: ssb_bfs_shard_fetch

@@ -92,23 +92,26 @@ __global__ void perm_derive_kernel(const int32_t* __restrict__ perm, int64_t n,
   }
 }
 
-// cl for every chunk; cells only for the chunks of the built range [cb, ce)
-// (a shard of a multi-GPU layout holds just its own cells)
+// cl for every chunk; cells only for the chunks the handle holds (held[i],
+// null = all): a shard of a multi-GPU layout holds just its own cells
+//
 __global__ void chunk_len_kernel(const int32_t* __restrict__ deg_perm, int64_t n_chunks,
-                                 int64_t C, int64_t cb, int64_t ce, int32_t* __restrict__ cl,
+                                 int64_t C, const uint8_t* __restrict__ held, int32_t* __restrict__ cl,
                                  int64_t* __restrict__ cells) {
   GRID_STRIDE(i, n_chunks) {
     int32_t mx = 0;
     for (int64_t l = 0; l < C; ++l) mx = max(mx, deg_perm[i * C + l]);
     cl[i] = mx;
-    cells[i] = i >= cb && i < ce ? int64_t(mx) * C : 0;
+    cells[i] = !held || held[i] ? int64_t(mx) * C : 0;
   }
 }
 
-// row degrees of the built range's rows (arc offsets), 0 elsewhere
-__global__ void range_deg_kernel(const int32_t* __restrict__ deg_perm, int64_t n_padded, int64_t r0,
-                                 int64_t r1, int64_t* __restrict__ out) {
-  GRID_STRIDE(p, n_padded) out[p] = p >= r0 && p < r1 ? int64_t(deg_perm[p]) : 0;
+// row degrees of the held rows in [r0, r1) (arc offsets of a pass), 0 elsewhere
+__global__ void range_deg_kernel(const int32_t* __restrict__ deg_perm, int64_t n_padded, int64_t C,
+                                 const uint8_t* __restrict__ held, int64_t r0, int64_t r1,
+                                 int64_t* __restrict__ out) {
+  GRID_STRIDE(p, n_padded)
+    out[p] = p >= r0 && p < r1 && (!held || held[p / C]) ? int64_t(deg_perm[p]) : 0;
 }
 
 __global__ void arc_keys_kernel(const uint64_t* __restrict__ keys, int64_t m, int bits,
@@ -127,8 +130,9 @@ __global__ void arc_keys_kernel(const uint64_t* __restrict__ keys, int64_t m, in
 // Arcs whose row (permuted) lies in [r0, r1) only, compacted through a
 // warp-aggregated counter (their order does not matter: they are sorted).
 __global__ void arc_keys_range_kernel(const uint64_t* __restrict__ keys, int64_t m, int bits,
-                                      const int32_t* __restrict__ inv_perm, int pbits, int64_t r0,
-                                      int64_t r1, unsigned long long* __restrict__ count,
+                                      const int32_t* __restrict__ inv_perm, int pbits, int64_t C,
+                                      const uint8_t* __restrict__ held, int64_t r0, int64_t r1,
+                                      unsigned long long* __restrict__ count,
                                       uint64_t* __restrict__ arcs) {
   const uint64_t mask = (uint64_t{1} << bits) - 1;
   const int lane = threadIdx.x & 31;
@@ -139,8 +143,8 @@ __global__ void arc_keys_range_kernel(const uint64_t* __restrict__ keys, int64_t
     if (i < m) {
       const int64_t pu = inv_perm[keys[i] >> bits];
       const int64_t pv = inv_perm[keys[i] & mask];
-      a0 = pu >= r0 && pu < r1;
-      a1 = pv >= r0 && pv < r1;
+      a0 = pu >= r0 && pu < r1 && (!held || held[pu / C]);
+      a1 = pv >= r0 && pv < r1 && (!held || held[pv / C]);
       k0 = (uint64_t(pu) << pbits) | uint64_t(pv);
       k1 = (uint64_t(pv) << pbits) | uint64_t(pu);
     }
@@ -207,8 +211,9 @@ void finish_chunks(ssb_graph& g, cudaStream_t s) {
   DevBuf<int64_t> cells(g.n_chunks + 1);
   SSB_CUDA(cudaMemsetAsync(cells.p, 0, 8 * (g.n_chunks + 1), s));
   if (g.n_chunks)
-    chunk_len_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(g.deg.p, g.n_chunks, g.C, g.range_cb,
-                                                          g.range_ce, g.cl.p, cells.p);
+    chunk_len_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(g.deg.p, g.n_chunks, g.C,
+                                                          g.partial() ? g.held.p : nullptr, g.cl.p,
+                                                          cells.p);
   SSB_CUDA(cudaGetLastError());
   exclusive_scan(cells.p, g.cs.p, g.n_chunks + 1, s);
   SSB_CUDA(cudaMemcpyAsync(&g.n_cells, g.cs.p + g.n_chunks, 8, cudaMemcpyDeviceToHost, s));
@@ -227,14 +232,35 @@ void finish_chunks(ssb_graph& g, cudaStream_t s) {
 }  // namespace
 
 ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma) {
-  return build_range_from_edges(e, C, sigma, 0, -1);
+  return build_range_from_edges(e, C, sigma, {});
+}
+
+std::vector<int64_t> normalize_segments(const int64_t* bounds, int64_t nseg, int64_t n_chunks) {
+  if (nseg < 0 || (nseg > 0 && !bounds)) fail(SSB_EINVAL, "bad segment list");
+  std::vector<std::pair<int64_t, int64_t>> v;
+  for (int64_t i = 0; i < nseg; ++i) {
+    const int64_t b = bounds[2 * i], e = bounds[2 * i + 1];
+    if (b < 0 || b > e || e > n_chunks) fail(SSB_EINVAL, "chunk range out of bounds");
+    if (b < e) v.push_back({b, e});
+  }
+  std::sort(v.begin(), v.end());
+  std::vector<int64_t> out;
+  for (auto& x : v) {
+    if (!out.empty() && x.first < out.back()) fail(SSB_EINVAL, "overlapping chunk segments");
+    if (!out.empty() && x.first == out.back()) out.back() = x.second;  // merge adjacent
+    else {
+      out.push_back(x.first);
+      out.push_back(x.second);
+    }
+  }
+  return out;
 }
 
 // The layout's metadata (perm, inv_perm, row degrees, cl) for every chunk and
-// the cells (cs, col) of chunks [cb, ce) only — one rank's share of a
-// multi-GPU layout; ce < 0 = all chunks.
-ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, int64_t cb,
-                                  int64_t ce) {
+// the cells (cs, col) of the chunk segments `segs` only — one rank's share of
+// a multi-GPU layout; empty segs = the whole layout.
+ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma,
+                                  const std::vector<int64_t>& segs_in) {
   // repr.cpp:63,85
   if (C <= 0) fail(SSB_EINVAL, "chunk height must be positive");
   if (sigma <= 0) fail(SSB_EINVAL, "sorting scope must be positive");
@@ -249,11 +275,23 @@ ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, 
   g->n_padded = g->n_chunks * C;
   g->nonzeros = 2 * m;
   if (int64_t(g->n_padded) >= (int64_t{1} << 31)) fail(SSB_EINVAL, "n too large");
-  if (ce < 0) ce = g->n_chunks;
-  if (cb < 0 || cb > ce || ce > g->n_chunks) fail(SSB_EINVAL, "chunk range out of bounds");
-  g->range_cb = cb;
-  g->range_ce = ce;
-  const bool partial = cb > 0 || ce < g->n_chunks;
+  {
+    const std::vector<int64_t> sg =
+        segs_in.empty() ? std::vector<int64_t>{}
+                        : normalize_segments(segs_in.data(), int64_t(segs_in.size() / 2), g->n_chunks);
+    const bool whole = segs_in.empty() || (sg.size() == 2 && sg[0] == 0 && sg[1] == g->n_chunks);
+    if (!whole) {
+      g->segs = sg.empty() ? std::vector<int64_t>{0, 0} : sg;  // {0, 0}: no cells (metadata only)
+      std::vector<uint8_t> h(size_t(std::max<int64_t>(g->n_chunks, 1)), 0);
+      for (size_t i = 0; i + 1 < sg.size(); i += 2)
+        for (int64_t c = sg[i]; c < sg[i + 1]; ++c) h[size_t(c)] = 1;
+      g->held.alloc(h.size());
+      SSB_CUDA(cudaMemcpyAsync(g->held.p, h.data(), h.size(), cudaMemcpyHostToDevice, s));
+    }
+  }
+  const bool partial = g->partial();
+  const uint8_t* held = partial ? g->held.p : nullptr;
+  const int64_t cb = 0, ce = g->n_chunks;  // passes walk every chunk; the mask keeps the held ones
 
   // 1. degrees
   DevBuf<int32_t> deg(std::max<int64_t>(n, 1));
@@ -310,15 +348,18 @@ ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, 
   // 8.4e9 arcs, 135 GB) is built in several passes into the one col array.
   if (m > 0 && ce > cb) {
     const int pbits = bits_for_value(uint64_t(std::max<int64_t>(n - 1, 1)));
-    // arcs per chunk of the range -> pass boundaries by cumulative arcs
+    // arcs per held chunk -> pass boundaries by cumulative arcs
     std::vector<int64_t> arcs_to(size_t(ce - cb) + 1, 0);
     {
       std::vector<int32_t> degp(size_t((ce - cb) * C));
+      std::vector<uint8_t> h(partial ? size_t(g->n_chunks) : 0);
       SSB_CUDA(cudaMemcpyAsync(degp.data(), g->deg.p + cb * C, 4 * degp.size(), cudaMemcpyDeviceToHost, s));
+      if (partial) SSB_CUDA(cudaMemcpyAsync(h.data(), g->held.p, h.size(), cudaMemcpyDeviceToHost, s));
       g->sc.sync();
       for (int64_t i = 0; i < ce - cb; ++i) {
         int64_t a = 0;
-        for (int64_t l = 0; l < C; ++l) a += degp[size_t(i * C + l)];
+        if (!partial || h[size_t(i)])
+          for (int64_t l = 0; l < C; ++l) a += degp[size_t(i * C + l)];
         arcs_to[size_t(i) + 1] = arcs_to[size_t(i)] + a;
       }
     }
@@ -336,7 +377,8 @@ ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, 
       while (pe < ce && arcs_to[size_t(pe + 1 - cb)] - arcs_to[size_t(pc - cb)] <= per_pass) ++pe;
       const int64_t r0 = pc * C, r1 = pe * C;
       // offsets over this pass's rows only; na = their arc count
-      range_deg_kernel<<<grid_for(g->n_padded), 256, 0, s>>>(g->deg.p, g->n_padded, r0, r1, rd.p);
+      range_deg_kernel<<<grid_for(g->n_padded), 256, 0, s>>>(g->deg.p, g->n_padded, C, held, r0, r1,
+                                                             rd.p);
       SSB_CUDA(cudaGetLastError());
       SSB_CUDA(cudaMemsetAsync(rd.p + g->n_padded, 0, 8, s));
       exclusive_scan(rd.p, rowptr.p, g->n_padded + 1, s);
@@ -349,7 +391,7 @@ ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, 
           DevBuf<unsigned long long> cnt(1);
           SSB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
           arc_keys_range_kernel<<<grid_for(m), 256, 0, s>>>(e.keys.p, m, e.bits, g->inv_perm.p, pbits,
-                                                            r0, r1, cnt.p, arcs.p);
+                                                            C, held, r0, r1, cnt.p, arcs.p);
           g->sc.sync();
         }
         SSB_CUDA(cudaGetLastError());
@@ -441,8 +483,6 @@ ssb_graph* graph_from_host_layout(int64_t n, int64_t C, int64_t sigma, int64_t n
   g->max_cl = 0;
   for (int32_t c : g->cl_host) g->max_cl = std::max<int64_t>(g->max_cl, c);
   g->total_cells = n_cells;
-  g->range_cb = 0;
-  g->range_ce = g->n_chunks;
   g->padding = n_cells - nonzeros;
   g->sc.sync();
   return g.release();

@@ -173,7 +173,31 @@ int ssb_build_slimsell_range(const ssb_edges* e, int64_t C, int64_t sigma, int64
   return guarded([&] {
     need(e, "edges");
     need(out, "out");
-    *out = ssb::build_range_from_edges(*e, C, sigma, chunk_begin, chunk_end);
+    if (C <= 0) ssb::fail(SSB_EINVAL, "chunk height must be positive");
+    const int64_t nc = (e->n + C - 1) / C;
+    const int64_t b[2] = {chunk_begin, chunk_end < 0 ? nc : chunk_end};
+    if (b[0] < 0 || b[0] > b[1] || b[1] > nc) ssb::fail(SSB_EINVAL, "chunk range out of bounds");
+    // an empty range holds no cells (metadata only); [0, n_chunks) is the whole layout
+    std::vector<int64_t> segs = {b[0], b[1]};
+    if (b[0] == b[1]) segs = {0, 0};
+    *out = ssb::build_range_from_edges(*e, C, sigma, segs);
+  });
+}
+
+int ssb_build_slimsell_segments(const ssb_edges* e, int64_t C, int64_t sigma, const int64_t* bounds,
+                                int64_t nseg, ssb_graph** out) {
+  return guarded([&] {
+    need(e, "edges");
+    need(out, "out");
+    if (C <= 0) ssb::fail(SSB_EINVAL, "chunk height must be positive");
+    if (nseg < 1) ssb::fail(SSB_EINVAL, "need at least one segment");
+    need(bounds, "bounds");
+    std::vector<int64_t> segs(bounds, bounds + 2 * nseg);
+    ssb::normalize_segments(segs.data(), nseg, (e->n + C - 1) / C);  // validates
+    bool empty = true;
+    for (int64_t i = 0; i < nseg; ++i) empty = empty && segs[size_t(2 * i)] == segs[size_t(2 * i + 1)];
+    if (empty) segs = {0, 0};
+    *out = ssb::build_range_from_edges(*e, C, sigma, segs);
   });
 }
 
@@ -211,9 +235,10 @@ int ssb_graph_info(const ssb_graph* g, ssb_layout_info* info) {
     info->n_cells = g->total_cells;
     info->padding = g->padding;
     info->max_chunk_len = g->max_cl;
-    info->range_begin = g->range_cb;
-    info->range_end = g->range_ce < 0 ? g->n_chunks : g->range_ce;
+    info->range_begin = g->partial() ? g->segs.front() : 0;
+    info->range_end = g->partial() ? g->segs.back() : g->n_chunks;
     info->range_cells = g->n_cells;
+    info->range_segments = g->partial() ? int64_t(g->segs.size() / 2) : 1;
   });
 }
 
@@ -410,7 +435,17 @@ int ssb_p2p_attach(ssb_graph* g, int rank, int world, const void* ipc_handles, i
                    int64_t chunk_end) {
   return guarded([&] {
     need(g, "graph");
-    ssb::p2p_attach(*g, rank, world, ipc_handles, chunk_begin, chunk_end);
+    const int64_t b[2] = {chunk_begin, chunk_end};
+    ssb::p2p_attach(*g, rank, world, ipc_handles, b, 1);
+  });
+}
+
+int ssb_p2p_attach_segments(ssb_graph* g, int rank, int world, const void* ipc_handles,
+                            const int64_t* bounds, int64_t nseg) {
+  return guarded([&] {
+    need(g, "graph");
+    if (nseg > 0) need(bounds, "bounds");
+    ssb::p2p_attach(*g, rank, world, ipc_handles, bounds, nseg);
   });
 }
 
@@ -420,24 +455,26 @@ int ssb_bfs_p2p(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, ssb_ite
   const int st = guarded([&] {
     need(g, "graph");
     need(opts, "opts");
-    rc = ssb::bfs_p2p(&g, 1, nullptr, root, *opts, stats, stats_cap, iterations, device_ms);
+    rc = ssb::bfs_p2p(&g, 1, nullptr, nullptr, root, *opts, stats, stats_cap, iterations, device_ms);
   });
   if (st != SSB_OK) return st;
   if (rc == SSB_ECAP) g_last_error = "iteration cap reached before fixed point";
   return rc;
 }
 
-int ssb_bfs_p2p_group(ssb_graph* const* shards, int world, const int64_t* ranges, int64_t root,
-                      const ssb_bfs_options* opts, ssb_iter_stats* stats, int64_t stats_cap,
-                      int64_t* iterations, double* device_ms) {
+int ssb_bfs_p2p_group(ssb_graph* const* shards, int world, const int64_t* bounds,
+                      const int64_t* seg_counts, int64_t root, const ssb_bfs_options* opts,
+                      ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations,
+                      double* device_ms) {
   int rc = SSB_OK;
   const int st = guarded([&] {
     need(shards, "shards");
-    need(ranges, "ranges");
+    need(bounds, "bounds");
     need(opts, "opts");
     if (world < 2) ssb::fail(SSB_EINVAL, "a group needs at least 2 shards");
     for (int i = 0; i < world; ++i) need(shards[i], "shard");
-    rc = ssb::bfs_p2p(shards, world, ranges, root, *opts, stats, stats_cap, iterations, device_ms);
+    rc = ssb::bfs_p2p(shards, world, bounds, seg_counts, root, *opts, stats, stats_cap, iterations,
+                      device_ms);
   });
   if (st != SSB_OK) return st;
   if (rc == SSB_ECAP) g_last_error = "iteration cap reached before fixed point";

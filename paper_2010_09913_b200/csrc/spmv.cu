@@ -79,8 +79,8 @@ void spmv_step(const ssb_graph& cg, int variant, const int64_t* x_prev, int64_t*
   if (variant < 0 || variant > 3) fail(SSB_EINVAL, "bad variant");
   if (chunk_begin < 0 || chunk_end > g.n_chunks || chunk_begin > chunk_end)
     fail(SSB_EINVAL, "chunk range out of bounds");
-  if (g.partial() && chunk_begin < chunk_end && (chunk_begin < g.range_cb || chunk_end > g.range_ce))
-    fail(SSB_EINVAL, "chunk range outside the range this handle holds");
+  if (!g.holds(chunk_begin, chunk_end))
+    fail(SSB_EINVAL, "chunk range outside the segments this handle holds");
   const int64_t np = g.n_padded;
   if (np == 0) return;
   cudaStream_t s = g.sc.s;

@@ -112,12 +112,13 @@ struct ssb_unit {
 struct ssb_bfs_plan {  // cached per slimchunk_len
   int64_t L = -1;
   int64_t Lu = -1;  // columns per work unit: min(L, balance cap)
-  int64_t cap_auto = 0, cap_cb = -1, cap_ce = -1;  // balance cap of a chunk range
+  int64_t cap_auto = 0;               // balance cap of the segments below
+  std::vector<int64_t> cap_segs;
   int64_t n_units = 0;
   int64_t n_tasks = 0;
   int64_t n_split = 0;
   int64_t empty_chunks = 0;  // chunks with cl == 0 (no unit)
-  int64_t cb = 0, ce = 0;    // chunk range the plan covers (a shard, or all)
+  std::vector<int64_t> segs;  // chunk segments the plan covers (a shard, or all)
   bool built = false;
   ssb::DevBuf<ssb_unit> units;
   ssb::DevBuf<int32_t> task_begin;    // n_tasks + 1
@@ -134,12 +135,31 @@ struct ssb_graph {
   int64_t C = 1, sigma = 1, n = 0, n_padded = 0, n_chunks = 0, nonzeros = 0;
   int64_t n_cells = 0, padding = 0, max_cl = 0;  // n_cells: cells held (the built range)
   int64_t total_cells = 0;                 // Σ C·cl over the whole layout
-  int64_t range_cb = 0, range_ce = -1;     // chunks whose cells this handle holds (-1: all)
+  // chunk segments whose cells this handle holds, [b0, e0, b1, e1, ...]
+  // ascending and disjoint; empty = the whole layout
+  std::vector<int64_t> segs;
+  ssb::DevBuf<uint8_t> held;               // per chunk: cells held (partial handles)
   int64_t build_passes = 0;                // arc sort passes the builder needed
-  bool partial() const { return range_ce >= 0 && (range_cb > 0 || range_ce < n_chunks); }
+  bool partial() const { return !segs.empty(); }
+  // every chunk of [cb, ce) is held
+  bool holds(int64_t cb, int64_t ce) const {
+    if (cb >= ce || !partial()) return true;
+    for (size_t i = 0; i + 1 < segs.size(); i += 2)
+      if (cb >= segs[i] && ce <= segs[i + 1]) return true;
+    return false;
+  }
+  bool holds_segments(const std::vector<int64_t>& o) const {
+    for (size_t i = 0; i + 1 < o.size(); i += 2) {
+      if (o[i] >= o[i + 1]) continue;
+      bool in = false;
+      for (size_t j = 0; !in && j + 1 < segs.size(); j += 2) in = o[i] >= segs[j] && o[i + 1] <= segs[j + 1];
+      if (partial() && !in) return false;
+    }
+    return true;
+  }
   void need_full(const char* what) const {
-    if (partial()) ssb::fail(SSB_EINVAL, std::string(what) + " needs the whole layout (this handle holds chunks [" +
-                                          std::to_string(range_cb) + ", " + std::to_string(range_ce) + ") only)");
+    if (partial()) ssb::fail(SSB_EINVAL, std::string(what) + " needs the whole layout (this handle holds "
+                                          "the cells of " + std::to_string(segs.size() / 2) + " chunk segment(s) only)");
   }
   ssb::DevBuf<int32_t> col;       // n_cells, -1 = padding cell
   ssb::DevBuf<int64_t> cs;        // n_chunks + 1 (cs[n_chunks] = n_cells)
@@ -182,7 +202,10 @@ struct ssb_graph {
 namespace ssb {
 // builder.cu
 ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma);
-ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma, int64_t cb, int64_t ce);
+ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma,
+                                  const std::vector<int64_t>& segs);
+// segments: [b0, e0, b1, e1, ...] chunk bounds; checked, sorted, merged
+std::vector<int64_t> normalize_segments(const int64_t* bounds, int64_t nseg, int64_t n_chunks);
 ssb_graph* graph_from_host_layout(int64_t n, int64_t C, int64_t sigma, int64_t nonzeros,
                                   const int64_t* col, int64_t n_cells, const int64_t* cs,
                                   const int64_t* cl, int64_t n_chunks, const int64_t* perm);
@@ -205,9 +228,10 @@ void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);
 void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total);
 void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent);
 void p2p_window(ssb_graph& g, void* ipc_handle, int64_t* bytes);
-void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, int64_t cb, int64_t ce);
-int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* ranges, int64_t root,
-            const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
+void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, const int64_t* bounds,
+                int64_t nseg);
+int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* bounds, const int64_t* seg_counts,
+            int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
             int64_t* iterations, double* device_ms);
 // hostio.cpp: widen the uint8 / int32 wire chunks into int64 host arrays on a
 // persistent host thread pool, chunk c once ready[c] has completed

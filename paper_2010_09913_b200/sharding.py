@@ -51,6 +51,29 @@ def partition_chunks(cl: np.ndarray, C: int, world: int) -> list[tuple[int, int]
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
 
+def partition_segments(cl: np.ndarray, C: int, world: int, k: int) -> list[list[tuple[int, int]]]:
+    """k·world contiguous cell-balanced pieces dealt to the ranks in snake
+    order (0..W-1, W-1..0, ...): every rank gets k segments spread over the
+    whole id range, so the hub chunks at the front — skipped once SlimWork
+    marks them visited — do not idle one rank ("deal
+    cell-balanced segments round-robin"). k = 1 is partition_chunks."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    pieces = partition_chunks(cl, C, world * k)
+    out: list[list[tuple[int, int]]] = [[] for _ in range(world)]
+    for j, pc in enumerate(pieces):
+        rnd, pos = divmod(j, world)
+        out[pos if rnd % 2 == 0 else world - 1 - pos].append(pc)
+    return out
+
+
+def _segments_of(spec) -> list[tuple[int, int]]:
+    """(b, e) or [(b, e), ...] -> [(b, e), ...]"""
+    if len(spec) == 2 and all(isinstance(x, (int, np.integer)) for x in spec):
+        return [(int(spec[0]), int(spec[1]))]
+    return [(int(b), int(e)) for b, e in spec]
+
+
 @dataclass
 class ExchangeResult:
     frontier: np.ndarray  # full frontier bitmap words (uint32)
@@ -163,8 +186,10 @@ class P2PShard:
     iterations. attach() is collective over torch.distributed: the ranks swap
     their windows' CUDA IPC handles (all_gather_object) and map each other's."""
 
-    def __init__(self, r, cb: int, ce: int):
-        self.r, self.cb, self.ce = r, int(cb), int(ce)
+    def __init__(self, r, *segments):
+        """segments: (cb, ce), or one list of (cb, ce) segments."""
+        self.r = r
+        self.segs = _segments_of(segments if len(segments) == 2 else segments[0])
 
     def window_handle(self) -> bytes:
         import ctypes as C
@@ -184,7 +209,9 @@ class P2PShard:
         if len(handles) != world or any(len(h) != 64 for h in handles):
             raise ValueError("need one 64-byte IPC handle per rank")
         buf = C.create_string_buffer(b"".join(handles), 64 * world)
-        _check(L.lib().ssb_p2p_attach(self.r._h, int(rank), int(world), buf, self.cb, self.ce))
+        b = np.array([x for seg in self.segs for x in seg], dtype=np.int64)
+        _check(L.lib().ssb_p2p_attach_segments(self.r._h, int(rank), int(world), buf,
+                                               b.ctypes.data_as(L.i64p), len(self.segs)))
 
     def attach_dist(self, group=None) -> None:
         import torch.distributed as dist
@@ -229,14 +256,16 @@ def run_p2p_group(reprs, ranges, root: int, opts, fetch: bool = True):
     from .api import KINF, _check, _p, _stats_list
     world = len(reprs)
     hs = (C.c_void_p * world)(*[r._h for r in reprs])
-    rg = np.array([x for b_e in ranges for x in b_e], dtype=np.int64)
+    segs = [_segments_of(x) for x in ranges]  # per rank: (b, e) or [(b, e), ...]
+    rg = np.array([x for sg in segs for seg in sg for x in seg], dtype=np.int64)
+    cnt = np.array([len(sg) for sg in segs], dtype=np.int64)
     o = opts._c()
     cap = 4096
     st = (L.IterStatsC * cap)()
     k = np.zeros(1, np.int64)
     ms = C.c_double()
-    rc = L.lib().ssb_bfs_p2p_group(hs, world, rg.ctypes.data_as(L.i64p), int(root), C.byref(o), st, cap,
-                                   k.ctypes.data_as(L.i64p), C.byref(ms))
+    rc = L.lib().ssb_bfs_p2p_group(hs, world, rg.ctypes.data_as(L.i64p), cnt.ctypes.data_as(L.i64p),
+                                   int(root), C.byref(o), st, cap, k.ctypes.data_as(L.i64p), C.byref(ms))
     _check(rc)
     if not fetch:
         return None, None, _stats_list(st, int(k[0])), float(ms.value)

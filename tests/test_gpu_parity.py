@@ -445,6 +445,37 @@ def test_range_built_shards(ssb, port, world):
                 assert dev_rows(ssb.BfsResult(d, p, len(it), it)) == dev_rows(a)
 
 
+@pytest.mark.parametrize("world,k", [(2, 3), (3, 2), (4, 4)])
+def test_round_robin_segment_shards(ssb, world, k):
+    """Ranks owning k round-robin (snake-dealt) chunk segments each, built
+    with only those segments' cells (ssb_build_slimsell_segments): the cells
+    are the matching slices of the whole layout in order, and the fused BFS
+    over them (segments exchanged separately, summary words shared at every
+    segment end) equals the single-GPU result."""
+    from paper_2010_09913_b200.sharding import partition_segments, run_p2p_group
+    g = ssb.gen_kronecker(18, 16, 8)
+    n = g.num_vertices()
+    full = ssb.build_slimsell(g, 32, n)
+    segs = partition_segments(full.cl, 32, world, k)
+    assert sorted(x for sg in segs for x in sg) == [tuple(x) for x in
+                                                    __import__("paper_2010_09913_b200.sharding", fromlist=["x"])
+                                                    .partition_chunks(full.cl, 32, world * k)]
+    col, cs = full.col32(), np.concatenate([full.cs, [full.n_cells]])
+    parts = [ssb.build_slimsell(g, 32, n, segments=sg) for sg in segs]
+    for sg, r in zip(segs, parts):
+        want = np.concatenate([col[cs[b]:cs[e]] for b, e in sg if e > b] or [col[:0]])
+        assert np.array_equal(r.col32(), want)
+    for root in (0, 4321, 150000):
+        for v in (3, 1):
+            o = opts(ssb, v, True, 256)
+            a = ssb.bfs_spmv(full, root, o)
+            d, p, it, _ = run_p2p_group(parts, segs, root, o)
+            assert np.array_equal(d, a.dist), (world, k, root, v)
+            if v == 3:
+                assert np.array_equal(p, a.parent), (world, k, root, v)
+            assert dev_rows(ssb.BfsResult(d, p, len(it), it)) == dev_rows(a)
+
+
 def test_multi_pass_build_equals_single_pass(ssb, monkeypatch):
     """The builder sorts and scatters arcs in passes over row sub-ranges when
     2m arcs do not fit beside col (S28 on one B200); forced to many small
