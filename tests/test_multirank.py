@@ -28,6 +28,28 @@ def test_partition_chunks_balanced():
     assert root_shard(range(10), 1, 4) == [1, 5, 9]
 
 
+def test_partition_segments_snake_and_balance():
+    """Round-robin segments: the k·W cell-balanced pieces of
+    partition_chunks dealt in snake order — every piece owned once, k per
+    rank, each rank's share of the head (hub) pieces and of the cells even."""
+    from paper_2010_09913_b200.sharding import partition_segments
+    rng = np.random.default_rng(1)
+    cl = np.sort(rng.integers(0, 5000, 20000) ** 2 // 5000)[::-1].copy()
+    for world, k in ((2, 4), (3, 2), (8, 4), (4, 1)):
+        segs = partition_segments(cl, 32, world, k)
+        pieces = partition_chunks(cl, 32, world * k)
+        assert sorted(x for sg in segs for x in sg) == sorted(pieces)
+        assert all(len(sg) == k for sg in segs)
+        # snake: round 0 deals pieces 0..W-1 to ranks 0..W-1, round 1 back
+        assert [sg[0] for sg in segs] == pieces[:world]
+        if k > 1:
+            assert [sg[1] for sg in segs] == pieces[world:2 * world][::-1]
+        cells = [sum(int((32 * cl[b:e] + 1).sum()) for b, e in sg) for sg in segs]
+        assert max(cells) <= (sum(cells) / world) * 1.05 + 2 * k * 32 * cl.max()
+    with pytest.raises(ValueError):
+        partition_segments(cl, 32, 2, 0)
+
+
 def sweep_range(L, b, e, F, visited, k, root_code, level, parent, slimwork, Lseg):
     """One BFS iteration over chunks [b, e) in 1-bit form (C = 32)."""
     n = L.n
