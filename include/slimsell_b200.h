@@ -180,6 +180,17 @@ int ssb_bfs_spmv(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, int64_
                  int64_t* parent, int64_t* parent_len, ssb_iter_stats* stats,
                  int64_t stats_cap, int64_t* iterations);
 
+/* A batch of bfs_spmv calls (Graph500 runs a root list): root i's result is
+ * written to dist[i] / parent[i] (parent may be NULL or hold NULLs; entries may
+ * alias — root i's result then replaces root i-1's), as ssb_bfs_spmv would.
+ * Root i's result crosses PCIe and is widened on the host while root i+1's
+ * BFS runs on the device. ERANGE for a bad root (nothing run); ECAP when a
+ * root hits the iteration cap: *capped_at = its index (its dist delivered, no
+ * parents, later roots not run), else -1. iterations (may be NULL): per root. */
+int ssb_bfs_spmv_batch(ssb_graph* g, const int64_t* roots, int64_t nroots, const ssb_bfs_options* opts,
+                       int64_t* const* dist, int64_t* const* parent, int64_t* iterations,
+                       int64_t* capped_at);
+
 /* Device-resident form used by benchmarks: runs the BFS and leaves the
  * result on the device. device_ms = CUDA-event time of the iteration loop on
  * the handle's stream. */

@@ -89,6 +89,8 @@ def lib() -> C.CDLL:
         "ssb_spmv_step": (C.c_int, [vp, C.c_int, i64p, i64p, C.c_int64, C.c_int64]),
         "ssb_bfs_spmv": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), i64p, i64p, i64p,
                                    C.POINTER(IterStatsC), C.c_int64, i64p]),
+        "ssb_bfs_spmv_batch": (C.c_int, [vp, i64p, C.c_int64, C.POINTER(BfsOptionsC), C.POINTER(i64p),
+                                         C.POINTER(i64p), i64p, i64p]),
         "ssb_bfs_run": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.POINTER(IterStatsC),
                                   C.c_int64, i64p, C.POINTER(C.c_double)]),
         "ssb_bfs_fetch": (C.c_int, [vp, C.c_int, i64p, i64p, i64p]),

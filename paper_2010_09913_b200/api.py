@@ -416,6 +416,43 @@ def bfs_spmv(r: SlimSellRepr, root: int, opts: BfsOptions | None = None,
     return res
 
 
+def bfs_spmv_batch(r: SlimSellRepr, roots, opts: BfsOptions | None = None,
+                   csr_for_parents: CsrView | None = None, out_dists=None, out_parents=None):
+    """A Graph500 root list through ssb_bfs_spmv_batch: root i's result lands in
+    out_dists[i] / out_parents[i] (contiguous int64[n]; entries may repeat — a
+    later root's result then replaces an earlier one's) while the next root's
+    BFS runs on the device. Parents as bfs_spmv (sel-max, or any variant with
+    a CSR). Returns the per-root iteration counts; BfsCapError carries the
+    capped root's index as .root_index."""
+    opts = opts or BfsOptions()
+    roots = np.ascontiguousarray(roots, dtype=np.int64)
+    k = roots.shape[0]
+    n = r.n
+    want = bool(opts.want_parents) and (opts.variant == Variant.selmax or csr_for_parents is not None)
+    o = opts._c()
+    o.want_parents = int(want)
+    if out_dists is None:
+        out_dists = [np.empty(max(n, 1), np.int64) for _ in range(k)]
+    if want and out_parents is None:
+        out_parents = [np.empty(max(n, 1), np.int64) for _ in range(k)]
+    for buf in list(out_dists) + list(out_parents or []):
+        if buf.dtype != np.int64 or buf.shape[0] < n or not buf.flags.c_contiguous:
+            raise InvalidArgument("output buffers must be contiguous int64[n]")
+    dp = (_L.i64p * max(k, 1))(*[_p(out_dists[i]) for i in range(k)])
+    pp = (_L.i64p * max(k, 1))(*[_p(out_parents[i]) for i in range(k)]) if want else None
+    iters = np.zeros(max(k, 1), np.int64)
+    capped = np.zeros(1, np.int64)
+    rc = _L.lib().ssb_bfs_spmv_batch(r._h, _p(roots), k, C.byref(o), dp, pp, _p(iters), _p(capped))
+    if rc == _L.SSB_ECAP:
+        i = int(capped[0])
+        e = BfsCapError(_L.lib().ssb_last_error().decode(),
+                        BfsResult(out_dists[i][:n], np.empty(0, np.int64), int(iters[i]), []))
+        e.root_index = i
+        raise e
+    _check(rc)
+    return [int(x) for x in iters[:k]]
+
+
 def bfs_traditional(g: Graph, root: int) -> BfsResult:  # bfs.hpp:86, bfs.cpp:248-291
     """The reference's queue BFS, on the device over the graph's CSR: parent =
     smallest neighbour one level closer, root self-parented."""

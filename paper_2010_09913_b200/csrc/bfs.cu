@@ -35,6 +35,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <future>
 #include <chrono>
 #include <mutex>
 #include <climits>
@@ -1818,7 +1819,9 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
   SSB_CUDA(cudaMemcpyAsync(r.rec.data(), g.dstats.p, size_t(first) * kStatW * 8,
                            cudaMemcpyDeviceToHost, s));
   SSB_CUDA(cudaEventRecord(g.sc.e_end, s));
-  g.sc.sync();
+  // blocking wait (e_end is a blocking-sync event): the host threads widening
+  // the previous root's result during a batch keep every core
+  SSB_CUDA(cudaEventSynchronize(g.sc.e_end));
   if (nrec > first && r.rec[size_t(first - 1) * kStatW] != 0) {
     SSB_CUDA(cudaMemcpy(r.rec.data() + first * kStatW, g.dstats.p + first * kStatW,
                         size_t(nrec - first) * kStatW * 8, cudaMemcpyDeviceToHost));
@@ -2038,79 +2041,170 @@ void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
 }
 
 // Pinned host copy of the wire buffer and the per-chunk completion events.
-struct WireHost {
-  uint8_t* p = nullptr;
+// One slot of the result fetch: the device wire buffer, its pinned host copy,
+// a copy stream and the per-chunk events (pack done / copy done). Two slots
+// let a batch pack root i+1 while the host still widens root i.
+struct WireSlot {
+  DevBuf<uint8_t> dev;
+  uint8_t* host = nullptr;
   size_t bytes = 0;
-  std::vector<cudaEvent_t> ev;
-  ~WireHost() {
-    if (p) cudaFreeHost(p);
-    for (auto e : ev) cudaEventDestroy(e);
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> packed, ready;
+  DevBuf<int> flag;        // dp_transform consistency flag of this slot's root
+  int* hflag = nullptr;    // ... its pinned host copy
+  std::vector<int64_t> bounds;
+  ~WireSlot() {
+    if (host) cudaFreeHost(host);
+    if (hflag) cudaFreeHost(hflag);
+    for (auto e : packed) cudaEventDestroy(e);
+    for (auto e : ready) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
   }
 };
+struct WireSlots {
+  WireSlot slot[2];
+};
+
+WireSlot& wire_slot(ssb_graph& g, int k, size_t bytes, int K) {
+  auto* W = static_cast<WireSlots*>(g.wire_host.get());
+  if (!W) {
+    auto w = std::make_shared<WireSlots>();
+    g.wire_host = w;
+    W = w.get();
+  }
+  WireSlot& S = W->slot[k];
+  if (S.bytes < bytes) {
+    S.dev.alloc(bytes);
+    if (S.host) cudaFreeHost(S.host);
+    S.host = nullptr;
+    SSB_CUDA(cudaHostAlloc(&S.host, bytes, cudaHostAllocDefault));
+    S.bytes = bytes;
+  }
+  if (!S.copy) SSB_CUDA(cudaStreamCreateWithFlags(&S.copy, cudaStreamNonBlocking));
+  if (!S.hflag) SSB_CUDA(cudaHostAlloc(&S.hflag, sizeof(int), cudaHostAllocDefault));
+  S.flag.ensure(1);
+  while (int(S.ready.size()) < K) {
+    cudaEvent_t a, b;
+    SSB_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    SSB_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming | cudaEventBlockingSync));
+    S.packed.push_back(a);
+    S.ready.push_back(b);
+  }
+  return S;
+}
+
+size_t wire_poff(int64_t n) { return (size_t(n) + 255) & ~size_t(255); }
+
+// Device half of a whole-result fetch through the narrow wire format: the
+// pack kernels run on the BFS stream (so the next BFS may reuse level /
+// parent once they are done), each chunk's D2H copy on the slot's copy stream
+// as soon as that chunk is packed. Returns at once.
+void wire_launch(ssb_graph& g, WireSlot& S, int K, bool want_dist, bool want_parents) {
+  cudaStream_t s = g.sc.s;
+  const int64_t n = g.n;
+  const bool sel = g.last_variant == SSB_SELMAX;
+  const size_t poff = wire_poff(n);
+  uint8_t* lev8 = S.dev.p;
+  int32_t* par32 = reinterpret_cast<int32_t*>(S.dev.p + poff);
+  uint8_t* hlev = S.host;
+  int32_t* hpar = reinterpret_cast<int32_t*>(S.host + poff);
+  BitRegions R = bit_regions(g, 0);
+  const bool dp = want_parents && !sel;
+  *S.hflag = 0;
+  if (dp) SSB_CUDA(cudaMemsetAsync(S.flag.p, 0, 4, s));
+  S.bounds.assign(size_t(K) + 1, 0);
+  for (int c = 0; c <= K; ++c) S.bounds[size_t(c)] = std::min(n, (n * c / K + 63) / 64 * 64);
+  for (int c = 0; c < K; ++c) {
+    const int64_t b = S.bounds[size_t(c)], len = S.bounds[size_t(c) + 1] - b;
+    if (len > 0) {
+      pack_wire_kernel<<<grid_for(len), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
+                                                     g.inv_perm.p, b, b + len, want_dist ? lev8 : nullptr,
+                                                     want_parents && sel ? par32 : nullptr);
+      if (dp)
+        dp_parent_kernel<int32_t><<<grid_for(len), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
+                                                                g.level.p, g.perm.p, g.inv_perm.p, b + len,
+                                                                par32, S.flag.p, nullptr, b);
+      SSB_CUDA(cudaGetLastError());
+    }
+    SSB_CUDA(cudaEventRecord(S.packed[size_t(c)], s));
+    SSB_CUDA(cudaStreamWaitEvent(S.copy, S.packed[size_t(c)], 0));
+    if (len > 0 && want_dist)
+      SSB_CUDA(cudaMemcpyAsync(hlev + b, lev8 + b, size_t(len), cudaMemcpyDeviceToHost, S.copy));
+    if (len > 0 && want_parents)
+      SSB_CUDA(cudaMemcpyAsync(hpar + b, par32 + b, 4 * size_t(len), cudaMemcpyDeviceToHost, S.copy));
+    SSB_CUDA(cudaEventRecord(S.ready[size_t(c)], S.copy));
+  }
+  if (dp) SSB_CUDA(cudaMemcpyAsync(S.hflag, S.flag.p, 4, cudaMemcpyDeviceToHost, S.copy));
+}
+
+// Host half: the pool widens chunk c into the caller's int64 arrays once it
+// has landed (dist INT64_MAX where unreached, parent -1).
+void wire_finish(WireSlot& S, int64_t n, int64_t* dist, int64_t* parent) {
+  const int K = int(S.bounds.size()) - 1;
+  std::vector<cudaEvent_t> ready(S.ready.begin(), S.ready.begin() + K);
+  widen_chunks(S.bounds, ready, S.host, reinterpret_cast<int32_t*>(S.host + wire_poff(n)), dist, parent);
+  SSB_CUDA(cudaStreamSynchronize(S.copy));
+  if (*S.hflag) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
+}
+
+int wire_chunks() { return std::max(1, std::min(64, env_int("SSB_WIRE_CHUNKS", 16))); }
 
 // Whole-result fetch through the narrow wire format: pack (device) -> chunked
 // D2H into pinned staging -> host threads widen chunk c while c+1 is in
 // flight. 5 bytes per vertex cross PCIe instead of 16.
 void fetch_wire(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent, int64_t* parent_len) {
-  cudaStream_t s = g.sc.s;
   const int64_t n = g.n;
-  const bool sel = g.last_variant == SSB_SELMAX;
+  const int K = wire_chunks();
+  WireSlot& S = wire_slot(g, 0, wire_poff(n) + 4 * size_t(n), K);
   const bool want_p = want_parents && parent != nullptr;
-  const size_t poff = (size_t(n) + 255) & ~size_t(255);
-  const size_t bytes = poff + 4 * size_t(n);
-  g.wire.ensure(bytes);
-  auto* H = static_cast<WireHost*>(g.wire_host.get());
-  if (!H || H->bytes < bytes) {
-    auto h = std::make_shared<WireHost>();
-    SSB_CUDA(cudaHostAlloc(&h->p, bytes, cudaHostAllocDefault));
-    h->bytes = bytes;
-    g.wire_host = h;
-    H = h.get();
-  }
-  const int K = std::max(1, std::min(64, env_int("SSB_WIRE_CHUNKS", 16)));
-  while (int(H->ev.size()) < K) {
-    cudaEvent_t e;
-    SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
-    H->ev.push_back(e);
-  }
-  uint8_t* lev8 = g.wire.p;
-  int32_t* par32 = reinterpret_cast<int32_t*>(g.wire.p + poff);
-  uint8_t* hlev = H->p;
-  int32_t* hpar = reinterpret_cast<int32_t*>(H->p + poff);
-  BitRegions R = bit_regions(g, 0);
-  int hbad = 0;
-  const bool dp = want_parents && !sel;
-  if (dp) {
-    g.flag.ensure(1);
-    SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, 4, s));
-  }
-  std::vector<int64_t> bounds(size_t(K) + 1);
-  for (int c = 0; c <= K; ++c) bounds[size_t(c)] = std::min(n, (n * c / K + 63) / 64 * 64);
-  std::vector<cudaEvent_t> ready(H->ev.begin(), H->ev.begin() + K);
-  // chunk c is packed, then copied, while the host widens chunk c-1
-  for (int c = 0; c < K; ++c) {
-    const int64_t b = bounds[size_t(c)], len = bounds[size_t(c) + 1] - b;
-    if (len > 0) {
-      pack_wire_kernel<<<grid_for(len), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
-                                                     g.inv_perm.p, b, b + len, dist ? lev8 : nullptr,
-                                                     want_p && sel ? par32 : nullptr);
-      if (dp && want_p)
-        dp_parent_kernel<int32_t><<<grid_for(len), 256, 0, s>>>(g.col.p, g.cs.p, g.cl.p, g.C, R.visited,
-                                                                g.level.p, g.perm.p, g.inv_perm.p, b + len,
-                                                                par32, g.flag.p, nullptr, b);
-      SSB_CUDA(cudaGetLastError());
-    }
-    if (len > 0 && dist)
-      SSB_CUDA(cudaMemcpyAsync(hlev + b, lev8 + b, size_t(len), cudaMemcpyDeviceToHost, s));
-    if (len > 0 && want_p)
-      SSB_CUDA(cudaMemcpyAsync(hpar + b, par32 + b, 4 * size_t(len), cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaEventRecord(ready[size_t(c)], s));
-  }
-  if (dp) SSB_CUDA(cudaMemcpyAsync(&hbad, g.flag.p, 4, cudaMemcpyDeviceToHost, s));
-  widen_chunks(bounds, ready, hlev, hpar, dist, want_p ? parent : nullptr);
+  wire_launch(g, S, K, dist != nullptr, want_p);
+  wire_finish(S, n, dist, want_p ? parent : nullptr);
   g.sc.sync();
-  if (hbad) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
   if (parent_len) *parent_len = want_parents ? n : 0;
+}
+
+// A batch of BFS from `roots`, results delivered like ssb_bfs_spmv's into
+// dist[i] / parent[i] (entries may repeat: root i's result then replaces
+// root i-1's): root i's result is packed on the device, crosses PCIe and is
+// widened by the host threads WHILE root i+1's BFS runs — the device and the
+// PCIe / host-memory bound fetch overlap (two wire slots). Returns the index
+// of the first root that hit the iteration cap (its dist delivered, no
+// parents, later roots not run), or -1.
+int64_t bfs_batch(ssb_graph& g, const int64_t* roots, int64_t nroots, const ssb_bfs_options& o,
+                  int64_t* const* dist, int64_t* const* parent, int64_t* iterations) {
+  g.need_full("a single-GPU BFS");
+  const int64_t n = g.n;
+  const int K = wire_chunks();
+  std::future<void> pending;
+  auto join = [&] {
+    if (pending.valid()) pending.get();
+  };
+  try {
+    for (int64_t i = 0; i < nroots; ++i) {
+      int64_t it = 0;
+      const int rc = bfs_run(g, roots[i], o, nullptr, 0, &it, nullptr);
+      if (iterations) iterations[i] = it;
+      const bool want_p = rc == SSB_OK && o.want_parents && parent && parent[i];
+      if (rc != SSB_OK || it > 254 || n < env_int("SSB_WIRE_MIN", 1 << 16) || env_int("SSB_WIRE", 1) == 0) {
+        join();  // the direct path (deep or capped BFS, small graphs)
+        fetch_rows(g, want_p, dist ? dist[i] : nullptr, want_p ? parent[i] : nullptr, nullptr, nullptr);
+        if (rc == SSB_ECAP) return i;
+        continue;
+      }
+      join();  // root i-1 widened: its slot is free for root i+1
+      WireSlot& S = wire_slot(g, int(i & 1), wire_poff(n) + 4 * size_t(n), K);
+      int64_t* d = dist ? dist[i] : nullptr;
+      int64_t* p = want_p ? parent[i] : nullptr;
+      wire_launch(g, S, K, d != nullptr, want_p);
+      pending = std::async(std::launch::async, [&S, n, d, p] { wire_finish(S, n, d, p); });
+    }
+    join();
+  } catch (...) {
+    if (pending.valid()) pending.wait();
+    throw;
+  }
+  g.sc.sync();
+  return -1;
 }
 
 // Results in original ids; owned (device, per chunk, may be null = all): only

@@ -347,6 +347,32 @@ int ssb_bfs_spmv(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, int64_
   return rc;
 }
 
+int ssb_bfs_spmv_batch(ssb_graph* g, const int64_t* roots, int64_t nroots, const ssb_bfs_options* opts,
+                       int64_t* const* dist, int64_t* const* parent, int64_t* iterations,
+                       int64_t* capped_at) {
+  int64_t cap_i = -1;
+  const int st = guarded([&] {
+    need(g, "graph");
+    need(opts, "opts");
+    if (nroots < 0) ssb::fail(SSB_EINVAL, "nroots < 0");
+    if (nroots > 0) need(roots, "roots");
+    need(dist, "dist");
+    for (int64_t i = 0; i < nroots; ++i) {
+      need(dist[i], "dist[i]");
+      if (roots[i] < 0 || roots[i] >= g->n)
+        ssb::fail(SSB_ERANGE, "root " + std::to_string(roots[i]) + " outside [0, " + std::to_string(g->n) + ")");
+    }
+    cap_i = ssb::bfs_batch(*g, roots, nroots, *opts, dist, parent, iterations);
+  });
+  if (capped_at) *capped_at = cap_i;
+  if (st != SSB_OK) return st;
+  if (cap_i >= 0) {
+    g_last_error = "iteration cap reached before fixed point (root index " + std::to_string(cap_i) + ")";
+    return SSB_ECAP;
+  }
+  return SSB_OK;
+}
+
 int ssb_bfs_last_timing(ssb_graph* g, double* kernel_ms, int64_t* launches) {
   return guarded([&] {
     need(g, "graph");

@@ -7,6 +7,7 @@
 // 5 instead of 16 bytes per vertex over PCIe, the bound of the e2e path.
 #include <immintrin.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
@@ -137,16 +138,30 @@ void widen(const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* paren
 void widen_chunks(const std::vector<int64_t>& bounds, const std::vector<cudaEvent_t>& ready,
                   const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent) {
   Pool& p = pool();
-  const int T = p.size();
-  p.run([&](int w) {
-    for (size_t c = 0; c + 1 < bounds.size(); ++c) {
-      cudaEventSynchronize(ready[c]);
-      const int64_t b = bounds[c], len = bounds[c + 1] - b;
-      // 64-entry granules keep the workers' stores in separate cache lines
-      const int64_t gran = 64, ng = (len + gran - 1) / gran;
-      const int64_t g0 = ng * w / T, g1 = ng * (w + 1) / T;
-      const int64_t lo = b + g0 * gran, hi = std::min(b + g1 * gran, b + len);
-      if (lo < hi) widen(lev, par, dist, parent, lo, hi);
+  // Pieces of 64K entries (multiples of 64: the workers' stores stay in
+  // separate cache lines) handed out in order through one counter, so a
+  // worker slowed down by another thread on its core delays only its piece.
+  constexpr int64_t kPiece = 1 << 16;
+  std::vector<int64_t> first(bounds.size(), 0);  // first piece of chunk c
+  for (size_t c = 0; c + 1 < bounds.size(); ++c)
+    first[c + 1] = first[c] + (bounds[c + 1] - bounds[c] + kPiece - 1) / kPiece;
+  std::atomic<int64_t> next{0};
+  const int64_t total = first.back();
+  p.run([&](int) {
+    size_t c = 0;
+    bool waited = false;
+    for (int64_t q = next.fetch_add(1); q < total; q = next.fetch_add(1)) {
+      while (q >= first[c + 1]) {
+        ++c;
+        waited = false;
+      }
+      if (!waited) {
+        cudaEventSynchronize(ready[c]);
+        waited = true;
+      }
+      const int64_t lo = bounds[c] + (q - first[c]) * kPiece;
+      const int64_t hi = std::min(lo + kPiece, bounds[c + 1]);
+      widen(lev, par, dist, parent, lo, hi);
     }
   });
 }

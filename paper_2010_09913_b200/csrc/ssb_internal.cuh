@@ -73,7 +73,7 @@ struct StreamCtx {
     SSB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     SSB_CUDA(cudaEventCreate(&e0));
     SSB_CUDA(cudaEventCreate(&e1));
-    SSB_CUDA(cudaEventCreate(&e_end));
+    SSB_CUDA(cudaEventCreateWithFlags(&e_end, cudaEventBlockingSync));
   }
   ~StreamCtx() {
     if (e0) cudaEventDestroy(e0);
@@ -222,6 +222,8 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
             int64_t stats_cap, int64_t* iterations, double* device_ms);
 void bfs_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
                int64_t* parent_len);
+int64_t bfs_batch(ssb_graph& g, const int64_t* roots, int64_t nroots, const ssb_bfs_options& o,
+                  int64_t* const* dist, int64_t* const* parent, int64_t* iterations);
 int64_t bfs_edges_traversed(ssb_graph& g);
 void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t cb, int64_t ce);
 void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);

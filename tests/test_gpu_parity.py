@@ -564,6 +564,45 @@ def test_fetch_wire_format_equals_direct_path(ssb, port, monkeypatch):
                 assert np.array_equal(p1, b.parent) and np.array_equal(p2, b.parent), (root, v)
 
 
+def test_bfs_spmv_batch_equals_single_calls(ssb, port):
+    """ssb_bfs_spmv_batch (root i's fetch overlapped with root i+1's BFS, two
+    wire slots) delivers exactly what per-root ssb_bfs_spmv calls deliver —
+    sel-max parents, dp_transform parents with a CSR, aliased output buffers
+    (the last root's result survives), the small-graph direct path, and the
+    iteration cap (the capped root's dist delivered, its index reported)."""
+    import torch
+    for scale in (17, 10):
+        n, uv = port.gen_kronecker(scale, 16, 2)
+        g = ssb.Graph.from_pairs(uv, n)
+        r = ssb.build_slimsell(g, 32, n)
+        csr = ssb.to_csr(g)
+        roots = [0, 77, 5, n - 1, 123]
+        for v, c in ((3, None), (0, csr), (2, None)):
+            o = opts(ssb, v, True, 64)
+            ref = [ssb.bfs_spmv(r, x, o, c) for x in roots]
+            ds = [np.full(n, -9, np.int64) for _ in roots]
+            ps = [np.full(n, -9, np.int64) for _ in roots]
+            its = ssb.bfs_spmv_batch(r, roots, o, c, ds, ps)
+            assert its == [x.iterations for x in ref]
+            for a, d, p in zip(ref, ds, ps):
+                assert np.array_equal(a.dist, d), (scale, v)
+                if len(a.parent):
+                    assert np.array_equal(a.parent, p), (scale, v)
+            # aliased pinned outputs: the last root's result remains
+            pd = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+            pp = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+            ssb.bfs_spmv_batch(r, roots, o, c, [pd] * len(roots), [pp] * len(roots))
+            assert np.array_equal(pd, ref[-1].dist)
+            if len(ref[-1].parent):
+                assert np.array_equal(pp, ref[-1].parent)
+    o = opts(ssb, 3, True, 64, max_it=2)
+    with pytest.raises(ssb.BfsCapError) as ei:
+        ssb.bfs_spmv_batch(r, [0, 5], o)
+    assert ei.value.root_index == 0
+    with pytest.raises(ssb.OutOfRange):
+        ssb.bfs_spmv_batch(r, [0, n], opts(ssb, 3))
+
+
 def test_device_erdos_renyi_matches_oracle(ssb, port):
     """gen_erdos_renyi (generator.cpp:15-58) bit-exact, incl. p = 0 / 1 and
     the config-4 shape (average degree 16) at 2^18 and 2^20 vertices."""
