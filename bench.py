@@ -540,7 +540,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
     def one(root):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        dist_, parent_, per_iter = run_sharded_bfs([shard], comm, root, opts)
+        dist_, parent_, per_iter = run_sharded_bfs([shard], comm, root, opts, fetch=False)
         e1.record()
         torch.cuda.synchronize()
         launches[0] += shard.launches()

@@ -270,6 +270,8 @@ def run_p2p_group(reprs, ranges, root: int, opts, fetch: bool = True):
     if not fetch:
         return None, None, _stats_list(st, int(k[0])), float(ms.value)
     n = reprs[0].n
+    if not fetch:  # the BFS only (results stay on the devices)
+        return None, None, per_iter
     dist = np.full(n, KINF, dtype=np.int64)
     parent = np.full(n, -1, dtype=np.int64)
     want = bool(opts.want_parents) and int(opts.variant) == 3
@@ -331,7 +333,7 @@ class TorchComm:
         return t.cpu().numpy()
 
 
-def run_sharded_bfs(shards, comm, root: int, opts, max_iterations: int = 0):
+def run_sharded_bfs(shards, comm, root: int, opts, max_iterations: int = 0, fetch: bool = True):
     """A BFS over chunk-range shards: per iteration every shard sweeps its
     chunks, the owned frontier words are all-gathered, |newly| is summed, and
     the full frontier is installed on every shard. Returns (dist, parent,
@@ -355,6 +357,8 @@ def run_sharded_bfs(shards, comm, root: int, opts, max_iterations: int = 0):
         per_iter.append(IterStats(k, int(counts[5]), *[int(x) for x in counts[:5]]))
         if counts[4] == 0:
             break
+    if not fetch:  # the BFS only (results stay on the devices)
+        return None, None, per_iter
     dist = np.full(n, KINF, dtype=np.int64)
     parent = np.full(n, -1, dtype=np.int64)
     want = bool(opts.want_parents) and int(opts.variant) == 3
