@@ -240,7 +240,7 @@ int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* 
  * ssb_bfs_p2p: one BFS from `root` on this rank; every rank calls it with
  *   the same root and options. stats: this rank's counters (sum over ranks
  *   for the reference's IterStats). Results: ssb_bfs_shard_fetch (owned rows).
- * ssb_bfs_p2p_group: `world` shards (2..4 handles on THIS device) run as one
+ * ssb_bfs_p2p_group: `world` shards (2..8 handles on THIS device) run as one
  *   cooperative launch — the same kernel and exchange code, peers being
  *   plain device memory; stats summed. */
 int ssb_p2p_window(ssb_graph* g, void* ipc_handle, int64_t* window_bytes);

@@ -213,7 +213,7 @@ struct P2PArgs {
   int32_t wseg[2 * kMaxSeg];   // their frontier words [b, e) (= chunks, C = 32)
   int32_t sseg[2 * kMaxSeg];   // their summary words [b, e) (shared at the ends)
 };
-constexpr int kMaxVRanks = 4;  // ranks emulated in one launch (single-GPU tests)
+constexpr int kMaxVRanks = 8;  // ranks emulated in one launch (single-GPU tests, config 5 shape)
 struct GroupArgs {
   Args32 a[kMaxVRanks];
   P2PArgs x[kMaxVRanks];
@@ -2467,7 +2467,7 @@ const void* bfs32p_fn(bool sel, int S, bool group) {
 int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* bounds, const int64_t* seg_counts,
             int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats, int64_t stats_cap,
             int64_t* iterations, double* device_ms) {
-  if (n_local < 1 || n_local > kMaxVRanks) fail(SSB_EINVAL, "local shards must be in [1, 4]");
+  if (n_local < 1 || n_local > kMaxVRanks) fail(SSB_EINVAL, "local shards must be in [1, 8]");
   if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
   ssb_graph& g0 = *gs[0];
   for (int i = 0; i < n_local; ++i) {

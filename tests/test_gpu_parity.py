@@ -342,7 +342,7 @@ def test_chunk_sharded_device_bfs_matches_single_gpu(ssb, port, monkeypatch, wor
             assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_fused_p2p_sharded_bfs_matches_oracle(ssb, port, monkeypatch, world):
     """The fused multi-GPU BFS (frontier words stored into the peers' windows
     and a counter barrier inside the BFS kernel, ssb_bfs_p2p*) with `world`
@@ -445,7 +445,7 @@ def test_range_built_shards(ssb, port, world):
                 assert dev_rows(ssb.BfsResult(d, p, len(it), it)) == dev_rows(a)
 
 
-@pytest.mark.parametrize("world,k", [(2, 3), (3, 2), (4, 4)])
+@pytest.mark.parametrize("world,k", [(2, 3), (3, 2), (4, 4), (8, 4)])
 def test_round_robin_segment_shards(ssb, world, k):
     """Ranks owning k round-robin (snake-dealt) chunk segments each, built
     with only those segments' cells (ssb_build_slimsell_segments): the cells
