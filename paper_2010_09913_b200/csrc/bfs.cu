@@ -773,6 +773,12 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     uint32_t* Sn = (k % 3) == 0 ? a.S0 : ((k % 3) == 1 ? a.S1 : a.S2);
     uint32_t* Sx = ((k + 1) % 3) == 0 ? a.S0 : (((k + 1) % 3) == 1 ? a.S1 : a.S2);
 
+    // sweep mode of this iteration (grid-uniform, from |F_{k-1}|): dense ->
+    // early exit; dense and direct -> summary-free probes, whose image is the
+    // prefix alone, so the summary's words extend the prefix instead
+    const bool dense = front_in > a.dense_thr;
+    const bool direct = dense && front_in > a.direct_thr;
+    const int32_t img_words = direct ? a.PW + a.SW : a.PW;
     // -- stage the frontier prefix and the summary into shared memory -------
     // One thread issues TMA bulk copies (global -> shared, completion on an
     // mbarrier); everyone else goes on to the per-iteration setup and then
@@ -783,10 +789,10 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         // prior generic accesses (reads of the previous image, other CTAs'
         // frontier stores ordered by grid.sync) before the async-proxy copies
         asm volatile("fence.proxy.async;" ::: "memory");
-        const uint32_t bytes_p = uint32_t(a.PW) * 4u, bytes_s = uint32_t(a.SW) * 4u;
+        const uint32_t bytes_p = uint32_t(img_words) * 4u, bytes_s = direct ? 0u : uint32_t(a.SW) * 4u;
         mbar_arrive_expect_tx(stage_bar, bytes_p + bytes_s);
         bulk_g2s(sm + 4, Fc, bytes_p, stage_bar);
-        bulk_g2s(summ, Sc, bytes_s, stage_bar);
+        if (bytes_s) bulk_g2s(summ, Sc, bytes_s, stage_bar);
       }
       // clear the summary buffer of iteration k+1 (last read at k-1)
       for (int i = vb * kThreads + threadIdx.x; i < a.SW; i += nvb * kThreads)
@@ -803,7 +809,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0, c_swept = 0;
-    const Probe<kS> pr{sm + 4, Fc, a.PW * 32, a.PW * 32 - ((a.PW * 32) >> kS)};
+    const Probe<kS> pr{sm + 4, Fc, img_words * 32, a.PW * 32 - ((a.PW * 32) >> kS)};
 
     // Active task list: iteration 1 walks every task; later iterations only the
     // tasks kept by the previous one. A task whose units were all skipped in
@@ -812,8 +818,6 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     // counted as skipped through gone_chunks.
     const int32_t* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
     int32_t* list_out = (k & 1) ? a.tlist1 : a.tlist0;
-    // dense previous frontier -> early-exit sweeps (see take_cells)
-    const bool dense = front_in > a.dense_thr;
     auto run_tasks = [&](auto early_tag, auto direct_tag) {
     constexpr bool kEarly = decltype(early_tag)::value;
     constexpr bool kDirect = decltype(direct_tag)::value;
@@ -999,7 +1003,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       }
     }
     };  // run_tasks
-    if (dense && front_in > a.direct_thr) run_tasks(std::true_type{}, std::true_type{});
+    if (direct) run_tasks(std::true_type{}, std::true_type{});
     else if (dense) run_tasks(std::true_type{}, std::false_type{});
     else run_tasks(std::false_type{}, std::false_type{});
 
