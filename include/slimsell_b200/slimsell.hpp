@@ -498,6 +498,44 @@ inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& o
   return res;
 }
 
+/// Extension: a Graph500 root list through ssb_bfs_spmv_batch — results as
+/// from bfs_spmv per root (no per_iter records), root i's host fetch
+/// overlapped with root i+1's BFS on the device.
+inline std::vector<BfsResult> bfs_spmv_batch(const SlimSellRepr& r, const std::vector<vid_t>& roots,
+                                             const BfsOptions& opts,
+                                             const CsrView* csr_for_parents = nullptr) {
+  ssb_bfs_options o{};
+  o.variant = static_cast<std::int32_t>(opts.variant);
+  o.slimwork = opts.slimwork;
+  o.slimchunk_len = opts.slimchunk_len;
+  o.schedule = static_cast<std::int32_t>(opts.schedule);
+  o.workers = opts.workers;
+  o.max_iterations = opts.max_iterations;
+  o.want_parents = opts.want_parents &&
+                   (opts.variant == Variant::selmax || csr_for_parents != nullptr);
+  o.selmax_compat = opts.selmax_compat;
+  std::vector<BfsResult> out(roots.size());
+  std::vector<std::int64_t*> dp(roots.size()), pp(roots.size());
+  for (std::size_t i = 0; i < roots.size(); ++i) {
+    out[i].dist.resize(r.n);
+    out[i].parent.resize(o.want_parents ? r.n : 0);
+    dp[i] = out[i].dist.data();
+    pp[i] = o.want_parents ? out[i].parent.data() : nullptr;
+  }
+  std::vector<std::int64_t> iters(roots.size() + 1);
+  std::int64_t capped = -1;
+  const int rc = ssb_bfs_spmv_batch(r.handle(), roots.data(), static_cast<std::int64_t>(roots.size()),
+                                    &o, dp.data(), pp.data(), iters.data(), &capped);
+  for (std::size_t i = 0; i < roots.size(); ++i) out[i].iterations = iters[i];
+  if (rc == SSB_ECAP) {
+    BfsResult partial = std::move(out[static_cast<std::size_t>(capped)]);
+    partial.parent.clear();
+    throw BfsCapError(ssb_last_error(), std::move(partial));
+  }
+  if (rc != SSB_OK) detail::raise(rc);
+  return out;
+}
+
 /// bfs.hpp:86 (bfs.cpp:248-291) — the reference's queue BFS, run on the
 /// device over the graph's CSR: dist, parent = smallest neighbour one level
 /// closer (root self-parented), per_iter {iteration, elapsed_ns,

@@ -158,6 +158,22 @@ TEST_CASE(kronecker_matches_oracle) {
         }
         CHECK(counters);
       }
+      // the batch extension delivers the same results as per-root calls
+      if (C == 32) {
+        BfsOptions o;
+        o.variant = v;
+        o.slimwork = true;
+        o.slimchunk_len = 16;
+        const std::vector<vid_t> roots = {0, 77, 5};
+        std::vector<BfsResult> batch = bfs_spmv_batch(r, roots, o, &csr);
+        bool same = batch.size() == roots.size();
+        for (std::size_t i = 0; same && i < roots.size(); ++i) {
+          const BfsResult one = bfs_spmv(r, roots[i], o, &csr);
+          same = one.dist == batch[i].dist && one.parent == batch[i].parent &&
+                 one.iterations == batch[i].iterations;
+        }
+        CHECK(same);
+      }
     }
     so_repr_free(&L);
   }
