@@ -10,8 +10,11 @@ root of the batch (--roots, default 64).
   value  = Σ_roots m_cc / Σ_roots t  (GTEPS; t = device time of the BFS, CUDA
            events on the launching stream; m_cc = edges in the root's
            component; graph resident in HBM)
-  e2e    = the same through the public C-ABI call with HOST outputs
-           (dist + parent, int64[n] each, into pinned buffers) — copies inside
+  e2e    = the same through the public C-ABI with HOST outputs (dist +
+           parent, int64[n] each, into pinned buffers) — copies inside: the
+           step's root list through ssb_bfs_spmv_batch (each root's fetch
+           overlapped with the next root's BFS); e2e.single_call = one
+           ssb_bfs_spmv call per root
   roofline: bfs32_kernel, algorithmic bytes B_alg = 4·C·Σ_k cols_k
            + 3·iters·n_padded/8 + 8·n_padded per launch
   cpu_baseline: the reference library itself (oracle/_ref, built from
