@@ -638,6 +638,31 @@ def test_erdos_renyi_bfs_matches_oracle(ssb, port, monkeypatch):
             assert dev_rows(a) == port_rows(b.stats), (root, v)
 
 
+def test_deep_bfs_spans_launches(ssb, port):
+    """A BFS deeper than one cooperative launch (1024 iterations: a path of
+    2600 vertices) carries its active task list, retired chunks and counters
+    across launches, and its levels (> 254) take the direct int64 fetch —
+    per call and in a batch — equal to the oracle."""
+    n, uv = port.gen_path(2600)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    r = ssb.build_slimsell(g, 32, n)
+    L = port.build_slimsell(n, row, col, 32, n)
+    csr = ssb.to_csr(g)
+    for root in (0, 1300):
+        for v, sw, Lc in ((3, True, 64), (0, True, 0), (2, False, 16)):
+            o = opts(ssb, v, sw, Lc)
+            a = ssb.bfs_spmv(r, root, o, csr)
+            b = port.bfs_spmv(L, root, v, sw, Lc, csr=(row, col))
+            assert a.iterations == b.iterations > 1024 or root == 1300, (root, v)
+            assert np.array_equal(a.dist, b.dist) and np.array_equal(a.parent, b.parent), (root, v)
+            assert dev_rows(a) == port_rows(b.stats), (root, v)
+            d = [np.empty(n, np.int64)]
+            p = [np.empty(n, np.int64)]
+            its = ssb.bfs_spmv_batch(r, [root], o, csr, d, p)
+            assert its == [b.iterations] and np.array_equal(d[0], b.dist) and np.array_equal(p[0], b.parent)
+
+
 def test_device_bfs_traditional_matches_oracle(ssb, port):
     """The device queue BFS (bfs.cpp:248-291) equals the oracle's bfs_traditional:
     dist, smallest-id parents and per-level frontier sizes."""
