@@ -433,6 +433,10 @@ __device__ __align__(16) int32_t g_pad_column[32] = {
 #endif
 constexpr int32_t kWarpUnitCols = SSB_WARP_UNIT_COLS;  // units at least this long use the warp-wide sweep
 
+#ifndef SSB_SPLIT_X
+#define SSB_SPLIT_X 1  // tasks are shared by D ≤ 8 warps while n_tasks · D · X ≤ warps (0: never)
+#endif
+
 // Completes one work unit; called by all 32 lanes, `valid` per 8-lane group.
 // m = the unit's 32-row hit mask, best[q] = last hit of row 4·lg+q (sel-max).
 // SlimChunk combine (bfs.cpp:205-220): partial results of a split chunk meet
@@ -824,6 +828,13 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     // each warp's first task is its global warp id; the rest come from the
     // atomic counter (late iterations with few tasks then cost no atomics)
     const int32_t n_warps = int32_t(nvb) * (kThreads / 32);
+    // Few active tasks (late iterations): each task is shared by D warps, the
+    // d-th non-skipped unit going to sub-task d mod D, so a task's units are
+    // not swept four per round by one warp while the others idle. Sub-task 0
+    // does the task's bookkeeping (counters, retirement).
+    int32_t dsh = 0;
+    while (SSB_SPLIT_X > 0 && dsh < 3 && int64_t(n_in) * SSB_SPLIT_X << (dsh + 1) <= n_warps) ++dsh;
+    const int32_t n_v = n_in << dsh;
     int32_t t_first = int32_t(vb) * (kThreads / 32) + int32_t(threadIdx.x >> 5);
     for (;;) {
       int32_t t = t_first;
@@ -832,7 +843,9 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         t = __shfl_sync(0xffffffffu, t, 0);
       }
       t_first = -1;
-      if (t >= n_in) break;
+      if (t >= n_v) break;
+      const int32_t sub = t & ((1 << dsh) - 1);
+      t >>= dsh;
       if (k > 1) t = list_in[t];
       const int32_t ub = a.task_begin[t], ue = a.task_begin[t + 1];
 
@@ -849,7 +862,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         vis = a.visited[U.chunk];
         realm = U.chunk == a.n_chunks - 1 ? a.last_real : 0xffffffffu;
         skip = a.slimwork && vis == realm;  // should_skip_chunk
-        if (U.col_begin == 0) {
+        if (U.col_begin == 0 && sub == 0) {
           if (skip) {
             ++c_skip;
             Fn[U.chunk] = 0u;
@@ -861,6 +874,11 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
           }
         }
       }
+      const uint32_t open_all = __ballot_sync(0xffffffffu, has && !skip);
+      // this sub-task's units: the d-th open unit of the task, d mod D == sub
+      const bool mine = dsh == 0 ||
+          (int32_t(__popc(open_all & ((1u << lane) - 1u))) & ((1 << dsh) - 1)) == sub;
+      if (!mine) skip = true;
       // every lane prefetches the head (in sweep order) of its unit into L2
       if (kPfHeadSteps > 0 && has && !skip && U.col_len > 0) {
         const int32_t hc = min(U.col_len, 4 * kPfHeadSteps);  // columns
@@ -882,9 +900,9 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       uint32_t longs = __ballot_sync(0xffffffffu, is_long);
       uint32_t active = __ballot_sync(0xffffffffu, has && !skip && !is_long);
       {
-        const bool all_skipped = (longs | active) == 0u;
+        const bool all_skipped = open_all == 0u;
         const uint32_t firsts = __ballot_sync(0xffffffffu, has && U.col_begin == 0);
-        if (lane == 0) {
+        if (lane == 0 && sub == 0) {
           if (a.slimwork && all_skipped && a.tskip[t]) {
             atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
           } else {
