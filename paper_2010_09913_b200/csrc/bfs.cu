@@ -61,7 +61,10 @@ constexpr int kUnitsPerTask = 32;
 constexpr int kStatW = 8;  // int64 per iteration record
 // record: 0 frontier_size, 1 chunks_processed, 2 chunks_skipped,
 //         3 subchunks_processed, 4 columns_processed, 5 elapsed_ns
-constexpr int kItersPerLaunch = 1024;
+#ifndef SSB_ITERS_PER_LAUNCH
+#define SSB_ITERS_PER_LAUNCH 1024  // (1: one launch per iteration, for per-iteration profiles)
+#endif
+constexpr int kItersPerLaunch = SSB_ITERS_PER_LAUNCH;
 
 int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
@@ -433,6 +436,12 @@ __device__ __align__(16) int32_t g_pad_column[32] = {
 #endif
 constexpr int32_t kWarpUnitCols = SSB_WARP_UNIT_COLS;  // units at least this long use the warp-wide sweep
 
+#ifndef SSB_KEEP_BUF
+#define SSB_KEEP_BUF 1  // kept tasks appended 32 per atomic (0: one atomic per task)
+#endif
+#ifndef SSB_GRAB
+#define SSB_GRAB 1  // tasks taken per counter atomic in early-exit iterations
+#endif
 #ifndef SSB_SPLIT_X
 #define SSB_SPLIT_X 1  // tasks are shared by D ≤ 8 warps while n_tasks · D · X ≤ warps (0: never)
 #endif
@@ -836,14 +845,41 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     while (SSB_SPLIT_X > 0 && dsh < 3 && int64_t(n_in) * SSB_SPLIT_X << (dsh + 1) <= n_warps) ++dsh;
     const int32_t n_v = n_in << dsh;
     int32_t t_first = int32_t(vb) * (kThreads / 32) + int32_t(threadIdx.x >> 5);
+    // Kept tasks are buffered one per lane and appended to list_out with one
+    // atomic per 32 (a per-task append on one counter stalled every task on
+    // its round trip: 13% of k = 4-5's stall samples at S26). Only in the
+    // early-exit iterations: buffering groups the list by warp, and the
+    // sparse iterations' lists must keep the heavy (hub) tasks first for the
+    // dense sweep that follows (A/B: buffering there slowed S22 k = 3 by 20%).
+    constexpr bool kBuf = SSB_KEEP_BUF && kEarly;
+    int32_t keep_t = 0, keep_n = 0;  // keep_n warp-uniform
+    auto flush_kept = [&]() {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&a.task_out[rec], uint32_t(keep_n));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (lane < keep_n) list_out[base + lane] = keep_t;
+      keep_n = 0;
+    };
+    // early-exit iterations grab kGrab tasks per atomic (their tasks are
+    // mostly skip-only walks, where the counter's round trip dominated)
+    constexpr int32_t kGrab = kEarly ? SSB_GRAB : 1;
+    int32_t t_pend = 0, n_pend = 0;  // warp-uniform: grabbed, not yet started
     for (;;) {
       int32_t t = t_first;
       if (t < 0) {
-        if (lane == 0) t = int32_t(atomicAdd(&a.task_ctr[rec], 1u)) + n_warps;
-        t = __shfl_sync(0xffffffffu, t, 0);
+        if (n_pend == 0) {
+          if (lane == 0) t_pend = int32_t(atomicAdd(&a.task_ctr[rec], uint32_t(kGrab))) + n_warps;
+          t_pend = __shfl_sync(0xffffffffu, t_pend, 0);
+          n_pend = kGrab;
+        }
+        t = t_pend++;
+        --n_pend;
       }
       t_first = -1;
-      if (t >= n_v) break;
+      if (t >= n_v) {
+        if (kBuf && keep_n) flush_kept();
+        break;
+      }
       const int32_t sub = t & ((1 << dsh) - 1);
       t >>= dsh;
       if (k > 1) t = list_in[t];
@@ -902,12 +938,24 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       {
         const bool all_skipped = open_all == 0u;
         const uint32_t firsts = __ballot_sync(0xffffffffu, has && U.col_begin == 0);
-        if (lane == 0 && sub == 0) {
-          if (a.slimwork && all_skipped && a.tskip[t]) {
-            atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
+        if (!kBuf) {
+          if (lane == 0 && sub == 0) {
+            if (a.slimwork && all_skipped && a.tskip[t]) {
+              atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
+            } else {
+              list_out[atomicAdd(&a.task_out[rec], 1u)] = t;
+              a.tskip[t] = all_skipped;
+            }
+          }
+        } else if (sub == 0) {
+          const bool retire = a.slimwork && all_skipped &&
+                              __shfl_sync(0xffffffffu, lane == 0 ? a.tskip[t] : 0, 0);
+          if (retire) {
+            if (lane == 0) atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
           } else {
-            list_out[atomicAdd(&a.task_out[rec], 1u)] = t;
-            a.tskip[t] = all_skipped;
+            if (lane == 0) a.tskip[t] = all_skipped;
+            if (lane == keep_n) keep_t = t;
+            if (++keep_n == 32) flush_kept();
           }
         }
       }
