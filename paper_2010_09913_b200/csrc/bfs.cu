@@ -1454,23 +1454,31 @@ void build_plan32(ssb_graph& g, int64_t L, const std::vector<int64_t>& segs) {
   // an iteration idles the grid (S22: one 2048-column unit is ~0.2 ms on a
   // warp, longer than the whole iteration). L <= 0 (SlimChunk off) splits at
   // the cap alone.
-  int64_t cap = env_int("SSB_UNIT_CAP", 0);
-  if (cap <= 0) {
-    // the largest power of two (64 .. 4096) not above one warp's share of a
-    // full sweep (A/B S22: 4096 113.8, 512 136.4, 128 131.6 GTEPS); the range
-    // sum is host work, cached with the range
-    if (P.cap_segs != segs) {
-      int64_t cols = 0;
-      for (size_t q = 0; q + 1 < segs.size(); q += 2)
-        for (int64_t i = segs[q]; i < segs[q + 1]; ++i) cols += g.cl_host[size_t(i)];
-      const int64_t per_warp = cols / (int64_t(num_sms()) * (kThreads / 32));
-      int64_t c = 64;
-      while (c * 2 <= per_warp && c < 4096) c *= 2;
-      P.cap_auto = c;
-      P.cap_segs = segs;
-    }
-    cap = P.cap_auto;
+  // one warp's share of a full sweep (columns); the range sum is host work,
+  // cached with the range
+  if (P.cap_segs != segs) {
+    int64_t cols = 0;
+    for (size_t q = 0; q + 1 < segs.size(); q += 2)
+      for (int64_t i = segs[q]; i < segs[q + 1]; ++i) cols += g.cl_host[size_t(i)];
+    const int64_t per_warp = cols / (int64_t(num_sms()) * (kThreads / 32));
+    // unit cap: the largest power of two (64 .. 4096) not above the share
+    // (A/B S22: 4096 113.8, 512 136.4, 128 131.6 GTEPS)
+    int64_t c = 64;
+    while (c * 2 <= per_warp && c < 4096) c *= 2;
+    P.cap_auto = c;
+    // task budget: the largest power of two (128 .. 8192) not above half the
+    // share. Small graphs need fine tasks for the sweeps' tail balance, large
+    // ones coarse tasks for cheap skip-only walks in the late iterations
+    // (scripts/sweep_budget.sh, GTEPS at 128/256/512/1024/2048/4096/8192:
+    // S22 145.8/148.4/136.0/119.5/-/-/-, S24 -/212.1/216.2/211.0/199.9/-/-,
+    // S26 215.4/229.8/233.5/236.5/237.4/238.7/239.6, ER 2^26 512 51.6, 2048 53.2)
+    int64_t b = 128;
+    while (b * 2 <= per_warp / 2 && b < 8192) b *= 2;
+    P.budget_auto = b;
+    P.cap_segs = segs;
   }
+  int64_t cap = env_int("SSB_UNIT_CAP", 0);
+  if (cap <= 0) cap = P.cap_auto;
   const int64_t Lu = L > 0 ? std::min(L, cap) : cap;
   if (P.L == L && P.Lu == Lu && P.segs == segs && P.built) return;
   std::vector<ssb_unit> units;
@@ -1495,7 +1503,7 @@ void build_plan32(ssb_graph& g, int64_t L, const std::vector<int64_t>& segs) {
         units.push_back({int32_t(i), int32_t(s * Lu), int32_t(std::min(Lu, cl - s * Lu)), sp});
     }
   }
-  const int64_t budget = env_int("SSB_TASK_BUDGET", 512);
+  const int64_t budget = env_int("SSB_TASK_BUDGET", int(P.budget_auto));
   const int64_t overhead = env_int("SSB_UNIT_OVERHEAD", 4);
   std::vector<int32_t> tb;
   tb.push_back(0);

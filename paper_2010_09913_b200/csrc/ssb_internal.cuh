@@ -113,6 +113,7 @@ struct ssb_bfs_plan {  // cached per slimchunk_len
   int64_t L = -1;
   int64_t Lu = -1;  // columns per work unit: min(L, balance cap)
   int64_t cap_auto = 0;               // balance cap of the segments below
+  int64_t budget_auto = 512;          // task budget (columns) of the same segments
   std::vector<int64_t> cap_segs;
   int64_t n_units = 0;
   int64_t n_tasks = 0;
