@@ -151,6 +151,31 @@ def test_selftest_grid_vs_oracle(ssb, port):
     assert count == 16 * 3 * 2 * 2 * 4 * 4
 
 
+def test_edge_graphs_vs_oracle(ssb, port, edge_graphs):
+    """One vertex, no edges, loops only, two components, ragged n around C = 32
+    (the port is pinned to the reference on the same list in test_oracle.py):
+    layout, dist, parents and every counter equal the oracle."""
+    for name, n, uv in edge_graphs:
+        g = ssb.Graph.from_pairs(uv, n)
+        assert g.num_vertices() == n and np.array_equal(g.edges(), uv), name
+        row, col = port.to_csr(n, uv)
+        csr = ssb.to_csr(g)
+        for C_, sig in ((1, 1), (8, n), (32, n), (32, 1)):
+            r = ssb.build_slimsell(g, C_, sig)
+            L = port.build_slimsell(n, row, col, C_, sig)
+            assert np.array_equal(r.col, L.col) and np.array_equal(r.perm, L.perm), (name, C_, sig)
+            for root in sorted({0, n // 2, n - 1}):
+                for v in range(4):
+                    for sw, Lc in ((False, 0), (True, 0), (True, 4)):
+                        a = ssb.bfs_spmv(r, root, opts(ssb, v, sw, Lc), csr)
+                        b = port.bfs_spmv(L, root, v, sw, Lc, csr=(row, col))
+                        key = (name, C_, sig, root, v, sw, Lc)
+                        assert a.iterations == b.iterations, key
+                        assert np.array_equal(a.dist, b.dist), key
+                        assert np.array_equal(a.parent, b.parent), key
+                        assert dev_rows(a) == port_rows(b.stats), key
+
+
 def test_cfg1_golden(ssb, port, golden):
     """Config 1: S16, C=8, σ=C, sel-max, the 16 pick_roots roots (4 isolated,
     10 not perm fixed points — the reference's parent encoding is active)."""

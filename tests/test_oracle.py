@@ -142,6 +142,27 @@ def test_port_matches_reference(port, ref, scale, seed):
                     assert rows(a.stats) == rows(b.stats)
 
 
+def test_port_edge_graphs_match_reference(port, ref, edge_graphs):
+    """Pins the port on the edge cases the GPU suite replays on the device."""
+    for name, n, uv in edge_graphs:
+        g = ref.from_pairs(uv, n)
+        assert np.array_equal(uv, g.edges()), name
+        row, col = port.to_csr(n, uv)
+        for C_, sig in ((1, 1), (8, n), (32, n), (32, 1)):
+            L = port.build_slimsell(n, row, col, C_, sig)
+            r = ref.build_slimsell(g, C_, sig)
+            Lr = r.layout()
+            assert np.array_equal(L.col, Lr.col) and np.array_equal(L.perm, Lr.perm), name
+            for root in sorted({0, n // 2, n - 1}):
+                for v in (TROPICAL, REAL, BOOLEAN, SELMAX):
+                    for sw, Lc in ((False, 0), (True, 0), (True, 4)):
+                        a = port.bfs_spmv(L, root, v, sw, Lc, csr=(row, col))
+                        b = ref.bfs_spmv(r, root, v, sw, Lc, csr_graph=g)
+                        key = (name, C_, sig, root, v, sw, Lc)
+                        assert np.array_equal(a.dist, b.dist) and np.array_equal(a.parent, b.parent), key
+                        assert rows(a.stats) == rows(b.stats), key
+
+
 def test_port_er_matches_reference(port, ref):
     for n, p, seed in ((64, 0.15, 3), (500, 0.02, 9)):
         assert np.array_equal(port.gen_erdos_renyi(n, p, seed)[1], ref.gen_erdos_renyi(n, p, seed).edges())
