@@ -145,6 +145,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #endif
 constexpr int32_t kPfAhead = SSB_PF_AHEAD;
 #ifndef SSB_PF_HEAD
+#ifndef SSB_TLIST64
+#define SSB_TLIST64 1
+#endif
+// SSB_TLIST64: a list entry carries its task's unit range (first unit | count
+// << 32), so a kept task's walk starts without the dependent task_begin load;
+// the skip flags are then indexed by the task's first unit.
+#if SSB_TLIST64
+typedef int64_t ssb_tentry;
+#else
+typedef int32_t ssb_tentry;
+#endif
 #define SSB_PF_HEAD 0  // steps (512 B) of each unit prefetched when its task starts
 #endif
 constexpr int32_t kPfHeadSteps = SSB_PF_HEAD;
@@ -170,9 +181,9 @@ struct Args32 {
   int64_t* stats;      // [kItersPerLaunch][kStatW]
   uint32_t* task_ctr;  // [kItersPerLaunch] tasks grabbed per iteration
   uint32_t* task_out;  // [kItersPerLaunch] tasks kept for the next iteration
-  int32_t* tlist0;     // active task lists (ping-pong by iteration parity)
-  int32_t* tlist1;
-  uint8_t* tskip;      // per task: every unit skipped in its last sweep
+  ssb_tentry* tlist0;  // active task lists (ping-pong by iteration parity)
+  ssb_tentry* tlist1;
+  uint8_t* tskip;      // per task (SSB_TLIST64: per first unit): every unit skipped in its last sweep
   unsigned long long* gone_chunks;  // chunks of retired tasks (skipped forever)
   int32_t n_tasks;     // active tasks entering iteration k_begin
   unsigned long long gone_base;  // chunks of tasks retired before k_begin
@@ -829,8 +840,8 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     // two consecutive iterations (so both frontier buffers hold zeros for its
     // chunks) is retired: SlimWork would skip it forever, and its chunks are
     // counted as skipped through gone_chunks.
-    const int32_t* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
-    int32_t* list_out = (k & 1) ? a.tlist1 : a.tlist0;
+    const ssb_tentry* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
+    ssb_tentry* list_out = (k & 1) ? a.tlist1 : a.tlist0;
     auto run_tasks = [&](auto early_tag, auto direct_tag) {
     constexpr bool kEarly = decltype(early_tag)::value;
     constexpr bool kDirect = decltype(direct_tag)::value;
@@ -852,7 +863,8 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     // sparse iterations' lists must keep the heavy (hub) tasks first for the
     // dense sweep that follows (A/B: buffering there slowed S22 k = 3 by 20%).
     constexpr bool kBuf = SSB_KEEP_BUF && kEarly;
-    int32_t keep_t = 0, keep_n = 0;  // keep_n warp-uniform
+    ssb_tentry keep_t = 0;
+    int32_t keep_n = 0;  // warp-uniform
     auto flush_kept = [&]() {
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&a.task_out[rec], uint32_t(keep_n));
@@ -882,8 +894,24 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       }
       const int32_t sub = t & ((1 << dsh) - 1);
       t >>= dsh;
+#if SSB_TLIST64
+      int32_t ub, ue;
+      if (k > 1) {
+        const int64_t e = list_in[t];
+        ub = int32_t(e);
+        ue = ub + int32_t(e >> 32);
+      } else {
+        ub = a.task_begin[t];
+        ue = a.task_begin[t + 1];
+      }
+      const ssb_tentry t_entry = int64_t(uint32_t(ub)) | (int64_t(ue - ub) << 32);
+      const int32_t t_skip = ub;  // tskip index
+#else
       if (k > 1) t = list_in[t];
       const int32_t ub = a.task_begin[t], ue = a.task_begin[t + 1];
+      const ssb_tentry t_entry = t;
+      const int32_t t_skip = t;
+#endif
 
       // window: lane l owns unit ub + l
       const int32_t u = ub + lane;
@@ -940,21 +968,21 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         const uint32_t firsts = __ballot_sync(0xffffffffu, has && U.col_begin == 0);
         if (!kBuf) {
           if (lane == 0 && sub == 0) {
-            if (a.slimwork && all_skipped && a.tskip[t]) {
+            if (a.slimwork && all_skipped && a.tskip[t_skip]) {
               atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
             } else {
-              list_out[atomicAdd(&a.task_out[rec], 1u)] = t;
-              a.tskip[t] = all_skipped;
+              list_out[atomicAdd(&a.task_out[rec], 1u)] = t_entry;
+              a.tskip[t_skip] = all_skipped;
             }
           }
         } else if (sub == 0) {
           const bool retire = a.slimwork && all_skipped &&
-                              __shfl_sync(0xffffffffu, lane == 0 ? a.tskip[t] : 0, 0);
+                              __shfl_sync(0xffffffffu, lane == 0 ? a.tskip[t_skip] : 0, 0);
           if (retire) {
             if (lane == 0) atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
           } else {
-            if (lane == 0) a.tskip[t] = all_skipped;
-            if (lane == keep_n) keep_t = t;
+            if (lane == 0) a.tskip[t_skip] = all_skipped;
+            if (lane == keep_n) keep_t = t_entry;
             if (++keep_n == 32) flush_kept();
           }
         }
@@ -1533,8 +1561,8 @@ void build_plan32(ssb_graph& g, int64_t L, const std::vector<int64_t>& segs) {
   P.split_hit.alloc(std::max<size_t>(split_units.size(), 1));
   P.split_best.alloc(std::max<size_t>(split_units.size(), 1) * 32);
   P.split_count.alloc(std::max<size_t>(split_units.size(), 1));
-  P.tlist.alloc(std::max<size_t>(2 * (tb.size() - 1), 2));
-  P.tskip.alloc(std::max<size_t>(tb.size() - 1, 1));
+  P.tlist.alloc(std::max<size_t>(2 * (tb.size() - 1), 2) * (sizeof(ssb_tentry) / 4));
+  P.tskip.alloc(std::max<size_t>(SSB_TLIST64 ? units.size() : tb.size() - 1, 1));
   SSB_CUDA(cudaMemcpyAsync(P.units.p, units.data(), sizeof(ssb_unit) * units.size(),
                            cudaMemcpyHostToDevice, s));
   SSB_CUDA(cudaMemcpyAsync(P.task_begin.p, tb.data(), 4 * tb.size(), cudaMemcpyHostToDevice, s));
@@ -1786,8 +1814,8 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.task_ctr = task_ctr;
   a.task_out = r.task_out;
   a.gone_chunks = r.gone;
-  a.tlist0 = g.plan.tlist.p;
-  a.tlist1 = g.plan.tlist.p + g.plan.n_tasks;
+  a.tlist0 = reinterpret_cast<ssb_tentry*>(g.plan.tlist.p);
+  a.tlist1 = a.tlist0 + g.plan.n_tasks;
   a.tskip = g.plan.tskip.p;
   a.n_tasks = int32_t(g.plan.n_tasks);
   a.gone_base = 0;
