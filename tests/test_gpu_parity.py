@@ -764,3 +764,24 @@ def test_ingest_to_device_graph(ssb, port):
         ssb.Graph.from_edge_list("0 1\n", reject_asymmetric=True)
     with pytest.raises(ssb.OutOfRange):
         ssb.Graph.from_edge_list("H 2 1\n0 5\n")
+
+
+def test_edge_graphs_batch_equals_single_calls(ssb, edge_graphs):
+    """ssb_bfs_spmv_batch on the edge graphs (one vertex, no edges, ragged n):
+    every root class, every semiring, the same results as per-root calls."""
+    for name, n, uv in edge_graphs:
+        g = ssb.Graph.from_pairs(uv, n)
+        r = ssb.build_slimsell(g, 32, n)
+        csr = ssb.to_csr(g)
+        roots = sorted({0, n // 2, n - 1})
+        for v in range(4):
+            o = opts(ssb, v, True, 4)
+            c = csr if v in (0, 1) else None
+            ref = [ssb.bfs_spmv(r, x, o, c) for x in roots]
+            ds = [np.full(n, -9, np.int64) for _ in roots]
+            ps = [np.full(n, -9, np.int64) for _ in roots]
+            assert ssb.bfs_spmv_batch(r, roots, o, c, ds, ps) == [x.iterations for x in ref], name
+            for a, d, p in zip(ref, ds, ps):
+                assert np.array_equal(a.dist, d), (name, v)
+                if len(a.parent):
+                    assert np.array_equal(a.parent, p), (name, v)
