@@ -785,3 +785,33 @@ def test_edge_graphs_batch_equals_single_calls(ssb, edge_graphs):
                 assert np.array_equal(a.dist, d), (name, v)
                 if len(a.parent):
                     assert np.array_equal(a.parent, p), (name, v)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_edge_graphs_sharded_paths(ssb, port, edge_graphs, world):
+    """The edge graphs through both multi-GPU decompositions (chunk-range
+    shards + all-gather, and the fused peer-window kernel), emulated on one
+    GPU: ranks owning no chunk (n = 1, n ≤ 64), ragged last chunks, no edges."""
+    from paper_2010_09913_b200.sharding import (DeviceShard, LocalComm, partition_chunks,
+                                                 run_p2p_group, run_sharded_bfs)
+    for name, n, uv in edge_graphs:
+        g = ssb.Graph.from_pairs(uv, n)
+        row, col = port.to_csr(n, uv)
+        L = port.build_slimsell(n, row, col, 32, n)
+        reprs = [ssb.build_slimsell(g, 32, n) for _ in range(world)]
+        ranges = partition_chunks(reprs[0].cl, 32, world)
+        shards = [DeviceShard(r, b, e) for r, (b, e) in zip(reprs, ranges)]
+        for root in sorted({0, n // 2, n - 1}):
+            for v, sw, Lc in ((3, True, 4), (0, True, 0), (2, False, 0)):
+                o = opts(ssb, v, sw, Lc)
+                b = port.bfs_spmv(L, root, v, sw, Lc)
+                for how in ("allgather", "p2p"):
+                    if how == "allgather":
+                        dist, parent, per_iter = run_sharded_bfs(shards, LocalComm(), root, o)
+                    else:
+                        dist, parent, per_iter, _ = run_p2p_group(reprs, ranges, root, o)
+                    key = (name, how, root, v, world)
+                    assert np.array_equal(dist, b.dist), key
+                    if v == 3:
+                        assert np.array_equal(parent, b.parent), key
+                    assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats), key
