@@ -20,9 +20,23 @@ root of the batch (--roots, default 64).
   cpu_baseline: the reference library itself (oracle/_ref, built from
            /root/reference sources) on this host, all cores, one root.
 
---impl reference runs the reference's own bfs_spmv (oracle/_ref) instead.
-Multi-GPU (torchrun): each rank holds the whole graph and runs its share of
-the root batch (independent BFS per root, no data-path collective).
+--impl reference runs the reference's OWN path on the host cores: its
+gen_kronecker / gen_erdos_renyi, build_slimsell and bfs_spmv (oracle/_ref,
+compiled from the unmodified sources); no libslimsell_b200.so is loaded.
+
+Multi-GPU: `--gpus N` without WORLD_SIZE re-launches itself under
+torch.distributed.run with N ranks (one per GPU). N > 1 defaults to
+north_star's decomposition — chunk-range shards (round-robin segments) with the
+frontier exchange fused into the BFS kernel over peer-mapped memory (--shard
+p2p) — and falls back to the NCCL all-gather form (--shard chunks) when the
+GPUs cannot map each other's memory or the backend is not NCCL. --shard roots
+is root-parallel (every rank holds the whole graph).
+
+Parity in the bench: every root of the step is validated on the device against
+the reference's deterministic rules (Graph500 edge checks + bit-exact parents:
+sel-max max-position rule with the root encoding, or the smallest-id rule), and
+compared with the reference's own recorded outputs (tests/golden/golden_big.json,
+ph64 of dist and parent + every IterStats counter) where it holds that root.
 """
 from __future__ import annotations
 
@@ -65,9 +79,10 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-slimwork", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
-    ap.add_argument("--shard", default="roots", choices=["roots", "chunks", "p2p"],
-                    help="multi-GPU decomposition: independent roots per rank (default), "
-                         "chunk-range shards with a per-iteration NCCL frontier all-gather, or "
+    ap.add_argument("--shard", default=None, choices=["roots", "chunks", "p2p"],
+                    help="multi-GPU decomposition (default: p2p for N > 1 when the GPUs map each "
+                         "other's memory, else chunks; single GPU at N = 1): independent roots per "
+                         "rank, chunk-range shards with a per-iteration NCCL frontier all-gather, or "
                          "chunk-range shards with the exchange fused into the BFS kernel (p2p)")
     ap.add_argument("--segments", type=int, default=4,
                     help="--shard p2p: chunk segments per rank, dealt round-robin (snake order)")
@@ -77,28 +92,44 @@ def args_():
     return ap.parse_args()
 
 
-def mix64(x: int) -> int:
-    M = (1 << 64) - 1
-    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
-    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
-    return x ^ (x >> 31)
+from paper_2010_09913_b200.fingerprint import graph500_roots, ph64_torch  # noqa: E402  (loads no .so)
+
+GOLDEN_BIG = os.path.join(ROOT, "tests", "golden", "golden_big.json")
+ROOT_RULE = "pick_roots stream (cli.cpp:114-134) rejecting degree 0"
 
 
-def graph500_roots(deg: np.ndarray, want: int, seed: int) -> list[int]:
-    """pick_roots' stream (cli.cpp:114-134: SplitMix64(seed).split(0x526f),
-    next() % n, distinct) additionally rejecting degree-0 vertices."""
-    M = (1 << 64) - 1
-    n = deg.shape[0]
-    s = mix64(seed ^ mix64((0x526F + 0x6A09E667F3BCC909) & M))
-    out, seen = [], set()
-    while len(out) < min(want, int(np.count_nonzero(deg))):
-        s = (s + 0x9E3779B97F4A7C15) & M
-        r = mix64(s) % n
-        if r not in seen:
-            seen.add(r)
-            if deg[r] > 0:
-                out.append(int(r))
-    return out
+def golden_entry(a):
+    """The reference's recorded outputs for this workload's graph, if any
+    (tests/golden/golden_big.json, written by tests/golden/make_golden_big.py
+    from the unmodified reference): (entry, {(root, variant, slimwork, L): case})."""
+    key = None
+    if a.seed == 1 and a.graph == "kronecker" and a.edgefactor == 16:
+        key = f"kron{a.scale}"
+    elif a.seed == 1 and a.graph == "er" and a.avg_degree == 16.0:
+        key = f"er{a.scale}"
+    try:
+        with open(GOLDEN_BIG) as f:
+            e = json.load(f).get(key)
+    except Exception:
+        e = None
+    if not e:
+        return None, {}
+    return e, {(c["root"], c["variant"], c["slimwork"], c["L"]): c for c in e.get("cases", [])}
+
+
+def config_of(a, slimwork, n_roots, parallelism, **extra):
+    """The workload description both arms print (same keys, same values)."""
+    gdesc = (f"erdos-renyi n=2^{a.scale} avg degree {a.avg_degree:g} seed {a.seed}" if a.graph == "er"
+             else f"kronecker scale {a.scale} ef {a.edgefactor} seed {a.seed}")
+    cfg = {"workload": (f"{gdesc}, SlimSell C=32 sigma=n, {a.variant}, "
+                        f"slimwork={'on' if slimwork else 'off'}, slimchunk L={a.slimchunk}, "
+                        f"{n_roots} Graph500 roots/step"),
+           "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32, "sigma": "n",
+           "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
+           "roots_per_step": n_roots, "root_rule": ROOT_RULE, "parallelism": parallelism,
+           "l2": "inputs larger than L2 (col >> 126 MB); no flush needed"}
+    cfg.update(extra)
+    return cfg
 
 
 def hbm_peak():
@@ -110,16 +141,22 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic():
-    """dram bytes per bfs32 launch from the committed ncu summary, if any."""
+def profiled_traffic(a):
+    """dram bytes per bfs32 launch from the committed ncu capture OF THIS
+    WORKLOAD (graph, scale, semiring), or (None, None) when none exists."""
     p = os.path.join(ROOT, "profiles", "ncu_bfs32_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), (f"{d.get('workload')}; algorithmic bytes of that launch "
-                                                f"{d.get('algorithmic_bytes_same_launch')}; {d.get('source')}")
     except Exception:
         return None, None
+    for e in d.get("entries", []):
+        m = e.get("match", {})
+        if (m.get("graph"), m.get("scale"), m.get("variant")) == (a.graph, a.scale, a.variant):
+            return e.get("dram_bytes_per_launch"), (
+                f"{e.get('workload')}; algorithmic bytes of that launch "
+                f"{e.get('algorithmic_bytes_same_launch')}; {e.get('source')}")
+    return None, None
 
 
 class ClockSampler:
@@ -269,26 +306,113 @@ def m_cc_of(dist: np.ndarray, deg: np.ndarray) -> int:
     return int(deg[dist != np.iinfo(np.int64).max].sum() // 2)
 
 
+def validate_roots(ssb, torch, a, g, r, db, opts, roots, variant_id, pin_d, pin_p):
+    """Bit-exact parity of every root, without the host oracle:
+    * ssb_validate_bfs_exact — Graph500 edge checks + every parent equal to the
+      reference's deterministic value (sel-max: perm of the max neighbour
+      position one level up, root encoding at levels 0-1, bfs.cpp:94-101 /
+      SURVEY.md App. A.3; tropical / real / boolean: the smallest-id neighbour
+      one level up, dp_transform semiring.cpp:159-187). Edge checks + exact
+      parents fix dist and parent uniquely.
+    * the reference's own outputs where tests/golden/golden_big.json holds the
+      root: ph64(dist), ph64(parent) and every IterStats counter."""
+    t0 = time.time()
+    gold, cases = golden_entry(a)
+    compat = variant_id == 3  # the bench runs the reference's sel-max encoding
+    exact = "selmax" if variant_id == 3 else "min"
+    bad, first, g_cmp, g_eq, g_first = 0, None, 0, 0, None
+    for root in roots:
+        k, _, stats, _ = db.run(root, opts)
+        dd, pp = db.fetch(True, pin_d, pin_p)  # parents: sel-max decode, else dp_transform
+        rep = ssb.validate_bfs(g, root, dd, pp, selmax_compat=compat, exact=exact, layout=r)
+        if rep is not None:
+            bad += 1
+            first = first or f"root {root}: {rep}"
+        c = cases.get((root, variant_id, not a.no_slimwork, a.slimchunk))
+        if c is not None:
+            g_cmp += 1
+            got = {"dist_ph": ph64_torch(torch.from_numpy(dd).cuda()),
+                   "parent_ph": ph64_torch(torch.from_numpy(pp).cuda()) if c["parent_ph"] else None,
+                   "stats": [[x.iteration, x.chunks_processed, x.chunks_skipped, x.subchunks_processed,
+                              x.columns_processed, x.frontier_size] for x in stats]}
+            diff = [key for key in ("dist_ph", "parent_ph", "stats") if got[key] != c[key]]
+            if diff:
+                g_first = g_first or f"root {root}: {diff} differ"
+            else:
+                g_eq += 1
+    # the device queue BFS (independent of the SlimSell path) for the first root
+    t = ssb.bfs_traditional(g, roots[0])
+    db.run(roots[0], opts)
+    dd, _ = db.fetch(False, pin_d, pin_p)
+    return {"roots": len(roots), "roots_bit_exact": len(roots) - bad, "roots_failed": bad,
+            "first_failure": first,
+            "checks": "ssb_validate_bfs_exact: Graph500 edge checks (cli.cpp:73-112 + Graph500) and every "
+                      "parent equal to the reference's deterministic rule (" +
+                      ("sel-max max-position, root encoding at levels 0-1, bfs.cpp:94-101" if exact == "selmax"
+                       else "smallest-id neighbour one level up, semiring.cpp:159-187") + ")",
+            "reference_golden": {"roots_compared": g_cmp, "roots_equal": g_eq, "first_difference": g_first,
+                                 "what": "ph64(dist), ph64(parent), every IterStats counter vs the unmodified "
+                                         "reference's bfs_spmv (tests/golden/golden_big.json)"},
+            "dist_equal_queue_bfs_first_root": bool(np.array_equal(dd, t.dist)),
+            "seconds": round(time.time() - t0, 2)}
+
+
 # ---------------------------------------------------------------------------
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1; rank 0
+    prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def peer_access_ok(torch, world: int) -> tuple[bool, str]:
+    """Every pair of the first `world` GPUs can map each other's memory (the
+    fused exchange's peer stores), and the collective backend is NCCL."""
+    if os.environ.get("SSB_BENCH_BACKEND", "nccl") != "nccl":
+        return False, "backend is not NCCL"
+    if torch.cuda.device_count() < world:
+        return False, f"{torch.cuda.device_count()} visible GPU(s) for {world} ranks"
+    for i in range(world):
+        for j in range(world):
+            if i != j and not torch.cuda.can_device_access_peer(i, j):
+                return False, f"GPU {i} cannot access GPU {j}"
+    return True, "peer access between every pair"
+
+
 def main():
     a = args_()
     world, rank, local = dist_env()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a.gpus))
     log = (lambda *x: print("[bench]", *x, file=sys.stderr, flush=True)) if rank == 0 else (lambda *x: None)
     variant_id = {"tropical": 0, "real": 1, "boolean": 2, "selmax": 3}[a.variant]
     slimwork = not a.no_slimwork
     cores = os.cpu_count() or 1
-    gdesc = (f"erdos-renyi n=2^{a.scale} avg degree {a.avg_degree:g} seed {a.seed}" if a.graph == "er"
-             else f"kronecker scale {a.scale} ef {a.edgefactor} seed {a.seed}")
-    workload = (f"{gdesc}, SlimSell C=32 sigma=n, "
-                f"{a.variant}, slimwork={'on' if slimwork else 'off'}, slimchunk L={a.slimchunk}, "
-                f"{a.roots} Graph500 roots/step")
 
     if a.impl == "reference":
-        return main_reference(a, world, rank, local, log, variant_id, slimwork, cores, workload)
-    if a.shard == "chunks":
-        return main_chunks(a, world, rank, local, log, variant_id, slimwork, workload)
-    if a.shard == "p2p":
-        return main_p2p(a, world, rank, local, log, variant_id, slimwork, workload)
+        return main_reference(a, world, rank, local, log, variant_id, slimwork, cores)
+    shard = a.shard
+    if shard is None:
+        shard = "roots"
+        if world > 1:
+            import torch
+            ok, why = peer_access_ok(torch, world)
+            shard = "p2p" if ok else "chunks"
+            log(f"N={world}: --shard {shard} ({why})")
+    if shard == "chunks":
+        return main_chunks(a, world, rank, local, log, variant_id, slimwork)
+    if shard == "p2p":
+        return main_p2p(a, world, rank, local, log, variant_id, slimwork)
 
     import torch
 
@@ -329,6 +453,7 @@ def main():
     launches = 0
     per_root_ms = {}
     balg_total, kernel_ms_total, n_bfs = 0.0, 0.0, 0
+    first_stats = None
     t_wall0 = time.time()
     for s in range(a.steps):
         tot = 0.0
@@ -342,8 +467,8 @@ def main():
             kernel_ms_total += kms
             n_bfs += 1
             per_root_ms.setdefault(root, []).append(ms)
-            if s == 0:
-                last_stats = stats
+            if first_stats is None:  # the step's first root (mine[0])
+                first_stats = stats
         step_ms.append(tot)
     barrier()
     wall_s = time.time() - t_wall0
@@ -369,7 +494,7 @@ def main():
     # ---- roofline of the dominant kernel ------------------------------------
     peak, peak_src = hbm_peak()
     achieved = balg_total / (kernel_ms_total * 1e-3) / 1e9
-    traffic, traffic_src = profiled_traffic()
+    traffic, traffic_src = profiled_traffic(a)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "bfs32_kernel", "peak_source": peak_src,
@@ -434,29 +559,10 @@ def main():
            "single_call": {"value": round(single_tot / single_max / 1e9, 3), "unit": "GTEPS",
                            "note": "one ssb_bfs_spmv call per root, same outputs"}}
 
-    # ---- Graph500-style validation of every root (device, untimed) ----------
+    # ---- parity of every root of the step (device, untimed) -----------------
     validation = None
     if not a.no_validate:
-        t0 = time.time()
-        bad, first = 0, None
-        compat = variant_id == 3  # the bench runs the reference's sel-max encoding
-        for root in mine:
-            db.run(root, opts)
-            dd, pp = db.fetch(True, pin_d, pin_p)
-            rep = ssb.validate_bfs(g, root, dd, pp if len(pp) else None, selmax_compat=compat)
-            if rep is not None:
-                bad += 1
-                first = first or f"root {root}: {rep}"
-        # the device queue BFS (independent of the SlimSell path) for the first root
-        t = ssb.bfs_traditional(g, mine[0])
-        db.run(mine[0], opts)
-        dd, _ = db.fetch(False, pin_d, pin_p)
-        validation = {"roots": len(mine), "roots_failed": bad, "first_failure": first,
-                      "checks": "ssb_validate_bfs: Graph500 edge checks + parent-tree checks "
-                                "(cli.cpp:73-112)" + (", sel-max compat parents of levels 0-1 skipped"
-                                                       if compat else ""),
-                      "dist_equal_queue_bfs_first_root": bool(np.array_equal(dd, t.dist)),
-                      "seconds": round(time.time() - t0, 2)}
+        validation = validate_roots(ssb, torch, a, g, r, db, opts, mine, variant_id, pin_d, pin_p)
         log(f"validation: {validation}")
 
     # ---- CPU baseline: the reference library on this host, one root ---------
@@ -486,13 +592,9 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(max_ms, 3),
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": DATA[a.graph],
-        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor,
-                   "C": 32, "sigma": "n", "semiring": a.variant, "slimwork": slimwork,
-                   "slimchunk_len": a.slimchunk, "roots_per_step": len(roots),
-                   "root_rule": "pick_roots stream (cli.cpp:114-134) rejecting degree 0",
-                   "parallelism": f"root-parallel x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (col = %.2f GB int32 >> 126 MB)" % (4 * r.n_cells / 1e9),
-                   "n": r.n, "m": m, "n_cells": r.n_cells, "iterations": len(last_stats)},
+        "config": config_of(a, slimwork, len(roots), f"root-parallel x{world}" if world > 1 else "single GPU"),
+        "graph_info": {"n": r.n, "m": m, "n_cells": r.n_cells, "col_gb_int32": round(4 * r.n_cells / 1e9, 2),
+                       "iterations_first_root": len(first_stats), "first_root": mine[0]},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "validation": validation,
         "gpu_launches": int(launches),
@@ -502,7 +604,7 @@ def main():
                    "gen_s": round(t_gen, 3), "build_s": round(t_build, 3)},
         "per_iteration_first_root": [{"k": s.iteration, "ms": round(s.elapsed_ns / 1e6, 4),
                                       "cols": s.columns_processed, "frontier": s.frontier_size,
-                                      "skipped": s.chunks_skipped} for s in last_stats],
+                                      "skipped": s.chunks_skipped} for s in first_stats],
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -511,7 +613,7 @@ def main():
         dist.destroy_process_group()
 
 
-def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
+def main_chunks(a, world, rank, local, log, variant_id, slimwork):
     """Chunk-range sharding: every rank sweeps its contiguous,
     cell-balanced chunk range of every BFS; one NCCL all-gather of the owned
     frontier words per iteration (paper_2010_09913_b200.sharding)."""
@@ -592,10 +694,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
         "warmup": a.warmup, "ms_per_step": round(max_ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": DATA[a.graph],
-        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
-                   "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
-                   "roots_per_step": len(roots), "parallelism": f"chunk-range shards x{world}",
-                   "l2": "inputs larger than L2"},
+        "config": config_of(a, slimwork, len(roots), f"chunk-range shards x{world}, NCCL frontier all-gather"),
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "chunk-sharded mode reports device time only"},
@@ -610,7 +709,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork, workload):
         dist.destroy_process_group()
 
 
-def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
+def main_p2p(a, world, rank, local, log, variant_id, slimwork):
     """Chunk-range sharding with the frontier exchange FUSED into the BFS
     kernel (sharding.P2PShard): each rank's owned frontier words go straight
     into the peers' windows over NVLink and the ranks meet at an in-kernel
@@ -719,11 +818,9 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(max_ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": DATA[a.graph],
-        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
-                   "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
-                   "roots_per_step": len(roots), "parallelism": par, "l2": "inputs larger than L2",
-                   "cells_per_rank_max": max(x.range_cells for x in (reprs if emu > 1 else [r])),
-                   "n_cells": r.n_cells},
+        "config": config_of(a, slimwork, len(roots), par,
+                            cells_per_rank_max=max(x.range_cells for x in (reprs if emu > 1 else [r])),
+                            n_cells=r.n_cells),
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "p2p-sharded mode reports device time only"},
@@ -738,40 +835,111 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork, workload):
         dist.destroy_process_group()
 
 
-def main_reference(a, world, rank, local, log, variant_id, slimwork, cores, workload):
-    """The reference's own CPU bfs_spmv (oracle/_ref) on this host."""
+def lscpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def main_reference(a, world, rank, local, log, variant_id, slimwork, cores):
+    """The reference's OWN path on this host (oracle/_ref: the unmodified
+    reference compiled from its sources): gen_kronecker / gen_erdos_renyi
+    (generator.cpp:15-89) -> build_slimsell (repr.cpp:84-131) -> bfs_spmv
+    (bfs.cpp:234-246), workers = all host threads, dynamic queue. Nothing of
+    this repo's device path is loaded in this process. Each timed step is one
+    root of the 64-root Graph500 list (cycled) — a bounded sample of the step
+    the GPU arm times. Under torchrun only rank 0 works."""
     if rank != 0:
         return
-    import paper_2010_09913_b200 as ssb
+    from oracle import Reference
 
-    ssb.set_device(local)
-    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
-    deg = r.degrees()
+    budget_s = float(os.environ.get("SSB_REF_BUDGET_S", "1650"))  # the driver's step limit is 30 min
+    T0 = time.time()
+    R = Reference()
+    t0 = time.time()
+    if a.graph == "er":
+        n_in = 1 << a.scale
+        g = R.gen_erdos_renyi(n_in, a.avg_degree / (n_in - 1), a.seed)
+    else:
+        g = R.gen_kronecker(a.scale, a.edgefactor, a.seed)
+    t_gen = time.time() - t0
+    deg = g.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
-    ref, rr = reference_repr(ssb, r, log)
-    del r
-    times, edges = [], []
+    t0 = time.time()
+    rr = R.build_slimsell(g, 32, g.n)
+    t_build = time.time() - t0
+    log(f"reference graph S{a.scale}: n={g.n} m={g.m} cells={rr.n_cells}; gen_kronecker {t_gen:.1f}s "
+        f"build_slimsell {t_build:.1f}s (single-threaded, the reference's own code)")
+    gold, cases = golden_entry(a)
+    t0 = time.time()
+    fnv = {k: rr.fnv(k) for k in ("col", "cs", "cl", "perm")}
+    fnv["edges"] = g.edges_fnv()
+    layout_check = None
+    if gold:
+        gl = gold.get("layout", {})
+        layout_check = all(fnv[k] == gl.get(f"{k}_fnv") for k in ("col", "cs", "cl", "perm")) and \
+            fnv["edges"] == gold.get("edges_fnv")
+    log(f"layout FNV {fnv} ({time.time() - t0:.1f}s); equal to tests/golden/golden_big.json: {layout_check}")
+
+    times, edges, ran = [], [], []
+    first_out = None
     for i in range(a.warmup + a.steps):
         root = roots[i % len(roots)]
-        out, t, wall = cpu_reference_run(ref, rr, root, variant_id, slimwork, a.slimchunk, cores)
+        if i >= a.warmup and times and time.time() - T0 + 2 * np.mean(times) + 120 > budget_s:
+            log(f"time budget: stopping after {len(times)} of {a.steps} timed roots")
+            break
+        out, t, wall = cpu_reference_run(R, rr, root, variant_id, slimwork, a.slimchunk, cores)
         log(f"reference root {root}: {t:.2f}s ({wall:.2f}s wall) iterations {out.iterations}")
+        if first_out is None:
+            first_out = (root, out)
         if i >= a.warmup:
             times.append(t)
             edges.append(m_cc_of(out.dist, deg))
+            ran.append(root)
     value = sum(edges) / sum(times) / 1e9
-    sample = (f"each step = 1 root of the {len(roots)}-root batch (roots cycled), full S{a.scale} graph; "
-              f"reference bfs_spmv workers={cores} dynamic_queue; layout materialised from the "
-              f"device-built (bit-identical) SlimSell arrays")
+    # the first root's output against the reference's recorded output
+    bit_same = None
+    root0, out0 = first_out  # root0 == roots[0]
+    mcc0 = m_cc_of(out0.dist, deg)
+    c = cases.get((root0, variant_id, slimwork, a.slimchunk))
+    if c is not None:
+        from paper_2010_09913_b200.fingerprint import ph64_np
+        bit_same = ph64_np(out0.dist) == c["dist_ph"] and (
+            c["parent_ph"] is None or ph64_np(out0.parent) == c["parent_ph"])
+    del out0, first_out
+    del rr
+    # the queue BFS (bfs_traditional, bfs.cpp:248-291), one thread: the
+    # Trad-BFS stand-in of BASELINE.md §3
+    trad = None
+    if time.time() - T0 + 200 < budget_s:
+        _, _, it, ts = R.bfs_traditional_timed(g, roots[0], want=False)
+        trad = {"value": round(mcc0 / ts / 1e9, 5) if ts > 0 else None,
+                "unit": "GTEPS", "threads": 1, "root": roots[0], "seconds": round(ts, 3), "iterations": it}
+        g.drop_csr()
+    sample = (f"each timed step = 1 root of the {len(roots)}-root Graph500 list (cycled; {len(ran)} timed "
+              f"after {a.warmup} warm-up roots), full S{a.scale} graph built by the reference itself "
+              f"(gen {t_gen:.0f}s + build_slimsell {t_build:.0f}s, untimed); reference bfs_spmv "
+              f"workers={cores} dynamic_queue; t = sum of IterStats.elapsed_ns (cli.cpp:46-50)")
     line = {
         "metric": METRIC, "value": round(value, 5), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(1e3 * float(np.mean(times)), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": workload, "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32,
-                   "sigma": "n", "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk},
+        "config": config_of(a, slimwork, len(roots), "single GPU" if world == 1 else f"root-parallel x{world}"),
         "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": cores, "kind": "reference",
-                         "sample": sample},
+                         "cpu_model": lscpu_model(), "sample": sample,
+                         "traditional_bfs_1_thread": trad},
         "e2e": {"value": round(value, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_path": {"gen_s": round(t_gen, 1), "build_slimsell_s": round(t_build, 1),
+                           "layout_fnv": fnv, "layout_equals_recorded_reference": layout_check,
+                           "first_root_equals_recorded_reference": bit_same,
+                           "timed_roots": len(ran), "wall_s": round(time.time() - T0, 1),
+                           "native_code": "oracle/_ref/libslimsell_ref.so only (no libslimsell_b200.so)"},
     }
     print(json.dumps(line), flush=True)
 

@@ -277,6 +277,22 @@ int ssb_bfs_traditional(ssb_edges* e, int64_t root, int64_t* dist, int64_t* pare
 #define SSB_VALIDATE_SELMAX_COMPAT 1
 int ssb_validate_bfs(ssb_edges* e, int64_t root, const int64_t* dist, const int64_t* parent,
                      int flags, int64_t* violations, char* report, int64_t report_cap);
+/* Bit-exact parents at any scale: ssb_validate_bfs plus, for every reached
+ * vertex, parent == the value the reference returns —
+ *   SSB_VALIDATE_MIN_PARENT_EXACT: the smallest original-id neighbour one level
+ *     closer, root self-parented (dp_transform semiring.cpp:159-187 ==
+ *     bfs_traditional bfs.cpp:248-291; tropical / real / boolean);
+ *   SSB_VALIDATE_SELMAX_EXACT: perm[max{inv_perm[u] : u ∈ N(v), d(u) = d(v)-1}]
+ *     (selmax_parents bfs.cpp:94-101); with SSB_VALIDATE_SELMAX_COMPAT the root
+ *     and its depth-1 vertices must hold perm[root] (the reference's root
+ *     encoding), else root.
+ * layout supplies perm / inv_perm (required for SELMAX_EXACT, may be NULL
+ * otherwise); it must be the layout the BFS ran on. O(m) device work. */
+#define SSB_VALIDATE_MIN_PARENT_EXACT 2
+#define SSB_VALIDATE_SELMAX_EXACT 4
+int ssb_validate_bfs_exact(ssb_edges* e, const ssb_graph* layout, int64_t root, const int64_t* dist,
+                           const int64_t* parent, int flags, int64_t* violations, char* report,
+                           int64_t report_cap);
 /* m_cc of the last run: Σ_{reached v} deg(v) / 2 (the GTEPS numerator). */
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc);
 

@@ -114,6 +114,8 @@ class Port:
         L.so_mix64.restype = C.c_uint64
         L.so_fnv1a64.argtypes = [C.c_void_p, C.c_int64]
         L.so_fnv1a64.restype = C.c_uint64
+        L.so_fnv1a64_i32.argtypes = [C.c_void_p, C.c_int64, C.c_uint64]
+        L.so_fnv1a64_i32.restype = C.c_uint64
 
     # -- generators / graph core ------------------------------------------
     def gen_kronecker_pairs(self, scale, ef, seed, init=(0.57, 0.19, 0.19, 0.05)):
@@ -237,6 +239,11 @@ class Port:
     def mix64(self, x):
         return self.lib.so_mix64(x)
 
+    def fnv_i32(self, a) -> str:
+        """fnv() of an int32 array's values as int64 (no widened copy)."""
+        a = np.ascontiguousarray(a, dtype=np.int32)
+        return format(self.lib.so_fnv1a64_i32(a.ctypes.data, a.shape[0], 0xCBF29CE484222325), "016x")
+
     def fnv(self, a) -> str:
         """FNV-1a-64 of an array's little-endian int64 bytes, as 16 hex digits."""
         a = np.ascontiguousarray(a, dtype=np.int64)
@@ -260,6 +267,17 @@ class RefGraph:
         self.ref.lib.ref_graph_edges(self.h, _p(uv))
         return uv
 
+    def edges_fnv(self) -> str:
+        return format(self.ref.lib.ref_graph_edges_fnv(self.h), "016x")
+
+    def degrees(self) -> np.ndarray:
+        deg = np.empty(self.n, dtype=np.int64)
+        self.ref.lib.ref_graph_degrees(self.h, _p(deg))
+        return deg
+
+    def drop_csr(self):
+        self.ref.lib.ref_graph_drop_csr(self.h)
+
     def csr(self):
         row = np.empty(self.n + 1, dtype=np.int64)
         col = np.empty(2 * self.m, dtype=np.int64)
@@ -280,6 +298,11 @@ class RefRepr:
         ref.lib.ref_repr_info(h, _p(info))
         (self.C, self.sigma, self.n, self.n_padded, self.n_chunks, self.nonzeros,
          self.n_cells, self.padding) = (int(v) for v in info)
+
+    def fnv(self, which: str) -> str:
+        """In-place FNV-1a-64 of col / cs / cl / perm / inv_perm."""
+        k = ("col", "cs", "cl", "perm", "inv_perm").index(which)
+        return format(self.ref.lib.ref_repr_fnv(self.h, k), "016x")
 
     def layout(self) -> Layout:
         col = np.empty(self.n_cells, dtype=np.int64)
@@ -334,6 +357,13 @@ class Reference:
         L.ref_bfs_traditional.argtypes = [vp, C.c_int64, _i64p, _i64p, _i64p]
         L.ref_dp_transform.argtypes = [vp, _i64p, _i64p]
         L.ref_selftest.argtypes = [C.c_uint64, C.c_int, C.c_char_p, C.c_int64]
+        L.ref_graph_edges_fnv.argtypes = [vp]
+        L.ref_graph_edges_fnv.restype = C.c_uint64
+        L.ref_graph_degrees.argtypes = [vp, _i64p]
+        L.ref_graph_drop_csr.argtypes = [vp]
+        L.ref_repr_fnv.argtypes = [vp, C.c_int]
+        L.ref_repr_fnv.restype = C.c_uint64
+        L.ref_bfs_traditional_timed.argtypes = [vp, C.c_int64, _i64p, _i64p, _i64p, _i64p]
 
     def _check(self, rc):
         if rc:
@@ -414,6 +444,16 @@ class Reference:
         it = np.zeros(1, dtype=np.int64)
         self._check(self.lib.ref_bfs_traditional(g.h, root, _p(dist), _p(parent), _p(it)))
         return dist, parent, int(it[0])
+
+    def bfs_traditional_timed(self, g: RefGraph, root, want=True):
+        """bfs_traditional plus Σ IterStats.elapsed_ns (seconds)."""
+        n = g.n
+        dist = np.empty(n, dtype=np.int64) if want else None
+        parent = np.empty(n, dtype=np.int64) if want else None
+        it = np.zeros(1, dtype=np.int64)
+        ns = np.zeros(1, dtype=np.int64)
+        self._check(self.lib.ref_bfs_traditional_timed(g.h, root, _p(dist), _p(parent), _p(it), _p(ns)))
+        return dist, parent, int(it[0]), float(ns[0]) * 1e-9
 
     def dp_transform(self, g: RefGraph, d):
         parent = np.empty(g.n, dtype=np.int64)

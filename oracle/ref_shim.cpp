@@ -136,6 +136,38 @@ void ref_graph_csr(void* g, int64_t* row, int64_t* col) {
 
 void ref_graph_free(void* g) { delete static_cast<RefGraph*>(g); }
 
+// FNV-1a-64 over little-endian int64 bytes (the golden-vector fingerprint),
+// computed in place so an S26 graph / layout is hashed without a 17 GB copy.
+static uint64_t fnv_i64(const int64_t* a, size_t count, uint64_t h = 0xcbf29ce484222325ULL) {
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(a);
+  for (size_t i = 0; i < count * 8; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+// graph.hpp:42 Graph::edges() as the flattened (u, v) int64 pairs
+uint64_t ref_graph_edges_fnv(void* g) {
+  const auto& e = static_cast<RefGraph*>(g)->g.edges();
+  static_assert(sizeof(e[0]) == 16, "pair<int64,int64>");
+  return fnv_i64(reinterpret_cast<const int64_t*>(e.data()), e.size() * 2);
+}
+
+// deg[v] = |N(v)| over the normalised edge set (the CSR row lengths of
+// graph.cpp:212-232, without materialising the CSR).
+void ref_graph_degrees(void* g, int64_t* deg) {
+  const auto& G = static_cast<RefGraph*>(g)->g;
+  std::memset(deg, 0, sizeof(int64_t) * size_t(G.num_vertices()));
+  for (auto [u, v] : G.edges()) {
+    ++deg[u];
+    ++deg[v];
+  }
+}
+
+// Drops the cached CsrView (to_csr) to give its memory back between phases.
+void ref_graph_drop_csr(void* g) { static_cast<RefGraph*>(g)->csr.reset(); }
+
 // graph.hpp:55-59 from_edge_list / from_matrix_market
 int ref_from_edge_list(const char* text, int64_t len, int directive, void** out) {
   return guarded([&] {
@@ -207,6 +239,14 @@ void ref_repr_export(void* r, int64_t* col, int64_t* cs, int64_t* cl, int64_t* p
 }
 
 void ref_repr_free(void* r) { delete static_cast<SlimSellRepr*>(r); }
+
+// FNV of one SlimSellRepr array in place: which = 0 col, 1 cs, 2 cl, 3 perm, 4 inv_perm.
+uint64_t ref_repr_fnv(void* r, int which) {
+  const auto* s = static_cast<SlimSellRepr*>(r);
+  const std::vector<int64_t>* v[] = {&s->col, &s->cs, &s->cl, &s->perm, &s->inv_perm};
+  if (which < 0 || which > 4) return 0;
+  return fnv_i64(v[which]->data(), v[which]->size());
+}
 
 // repr.hpp:90 spmv_step (chunk range form); out must hold n_padded values
 // (rows outside the range are left untouched, as in the reference).
@@ -297,6 +337,21 @@ int ref_bfs_traditional(void* g, int64_t root, int64_t* dist, int64_t* parent,
     std::memcpy(dist, res.dist.data(), res.dist.size() * 8);
     std::memcpy(parent, res.parent.data(), res.parent.size() * 8);
     *iterations = res.iterations;
+  });
+}
+
+// As ref_bfs_traditional, plus elapsed_ns = sum of its IterStats.elapsed_ns
+// (the timed part of the queue BFS, bfs.cpp:264-287).
+int ref_bfs_traditional_timed(void* g, int64_t root, int64_t* dist, int64_t* parent,
+                              int64_t* iterations, int64_t* elapsed_ns) {
+  return guarded([&] {
+    BfsResult res = bfs_traditional(static_cast<RefGraph*>(g)->get_csr(), root);
+    if (dist) std::memcpy(dist, res.dist.data(), res.dist.size() * 8);
+    if (parent) std::memcpy(parent, res.parent.data(), res.parent.size() * 8);
+    *iterations = res.iterations;
+    int64_t t = 0;
+    for (const IterStats& s : res.per_iter) t += s.elapsed_ns;
+    *elapsed_ns = t;
   });
 }
 

@@ -19,6 +19,21 @@ uint64_t so_mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+/* FNV-1a-64 of int32 values as the little-endian int64 bytes of their
+ * sign-extended values, continuing from h (pass 0xcbf29ce484222325 first):
+ * fingerprints a device-resident int32 col against the reference's int64 col
+ * without a 2x host copy. Test infrastructure. */
+uint64_t so_fnv1a64_i32(const int32_t* a, int64_t count, uint64_t h) {
+  for (int64_t i = 0; i < count; ++i) {
+    const uint64_t v = (uint64_t)(int64_t)a[i];
+    for (int b = 0; b < 8; ++b) {
+      h ^= (v >> (8 * b)) & 0xffu;
+      h *= 0x100000001b3ULL;
+    }
+  }
+  return h;
+}
+
 uint64_t so_fnv1a64(const void* data, int64_t nbytes) {
   const unsigned char* p = (const unsigned char*)data;
   uint64_t h = 0xcbf29ce484222325ULL;

@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         "ssb_bfs_columns_swept": (C.c_int, [vp, i64p]),
         "ssb_bfs_traditional": (C.c_int, [vp, C.c_int64, i64p, i64p, C.POINTER(IterStatsC), C.c_int64, i64p]),
         "ssb_validate_bfs": (C.c_int, [vp, C.c_int64, i64p, i64p, C.c_int, i64p, C.c_char_p, C.c_int64]),
+        "ssb_validate_bfs_exact": (C.c_int, [vp, vp, C.c_int64, i64p, i64p, C.c_int, i64p, C.c_char_p,
+                                             C.c_int64]),
         "ssb_bfs_shard_begin": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.c_int64, C.c_int64]),
         "ssb_bfs_shard_step": (C.c_int, [vp, C.POINTER(IterStatsC), C.c_void_p]),
         "ssb_bfs_shard_exchange": (C.c_int, [vp, C.c_void_p, C.c_int64]),

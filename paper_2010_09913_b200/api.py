@@ -472,18 +472,37 @@ def bfs_traditional(g: Graph, root: int) -> BfsResult:  # bfs.hpp:86, bfs.cpp:24
     return BfsResult(dist[:n], parent[:n], k, per)
 
 
-def validate_bfs(g: Graph, root: int, dist, parent=None, selmax_compat: bool = False):
+VALIDATE_SELMAX_COMPAT, VALIDATE_MIN_PARENT_EXACT, VALIDATE_SELMAX_EXACT = 1, 2, 4
+
+
+def validate_bfs(g: Graph, root: int, dist, parent=None, selmax_compat: bool = False,
+                 exact: str | None = None, layout: "SlimSellRepr | None" = None):
     """cli.cpp:73-112 (the parent-tree checks of verify_against_oracle) plus the
     Graph500 edge checks, on the device. Returns None when valid, else a report
-    (the first few violations) — the reference's optional<string>."""
+    (the first few violations) — the reference's optional<string>.
+
+    exact="min": every parent must be the smallest original-id neighbour one
+    level closer (dp_transform / bfs_traditional; tropical, real, boolean).
+    exact="selmax": every parent must be the reference's sel-max value
+    perm[max position of a neighbour one level closer], with the root encoding
+    (perm[root] at levels 0-1) when selmax_compat; needs
+    the layout the BFS ran on. Together with the edge checks this pins dist
+    and parent bit for bit at any scale."""
     dist = np.ascontiguousarray(dist, dtype=np.int64)
     par = None if parent is None or len(parent) == 0 else np.ascontiguousarray(parent, dtype=np.int64)
     if dist.shape[0] != g.num_vertices() or (par is not None and par.shape[0] != g.num_vertices()):
         raise InvalidArgument("dist/parent length must equal the vertex count")
+    flags = VALIDATE_SELMAX_COMPAT if selmax_compat else 0
+    if exact == "min":
+        flags |= VALIDATE_MIN_PARENT_EXACT
+    elif exact == "selmax":
+        flags |= VALIDATE_SELMAX_EXACT
+    elif exact is not None:
+        raise InvalidArgument("exact must be None, 'min' or 'selmax'")
     bad = np.zeros(1, np.int64)
     buf = C.create_string_buffer(1024)
-    _check(_L.lib().ssb_validate_bfs(g._h, root, _p(dist), _p(par), 1 if selmax_compat else 0,
-                                     _p(bad), buf, 1024))
+    _check(_L.lib().ssb_validate_bfs_exact(g._h, layout._h if layout is not None else None, root, _p(dist),
+                                           _p(par), flags, _p(bad), buf, 1024))
     if int(bad[0]) == 0:
         return None
     return f"{int(bad[0])} violation(s):\n" + buf.value.decode()

@@ -144,7 +144,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #define SSB_PF_AHEAD 1  // in-loop prefetch distance, in 2 KB loop iterations (A/B: 1 best)
 #endif
 constexpr int32_t kPfAhead = SSB_PF_AHEAD;
-#ifndef SSB_PF_HEAD
 #ifndef SSB_TLIST64
 #define SSB_TLIST64 1
 #endif
@@ -156,6 +155,7 @@ typedef int64_t ssb_tentry;
 #else
 typedef int32_t ssb_tentry;
 #endif
+#ifndef SSB_PF_HEAD
 #define SSB_PF_HEAD 0  // steps (512 B) of each unit prefetched when its task starts
 #endif
 constexpr int32_t kPfHeadSteps = SSB_PF_HEAD;
@@ -920,13 +920,20 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       uint32_t vis = 0, realm = 0;
       int64_t ubase = 0;  // the unit's first cell in col (loaded once per task)
       bool skip = false;
+      // A shared task (dsh > 0) is walked by 2^dsh warps at once; sub-task d
+      // owns the units in lanes l with l mod 2^dsh == d. Ownership must not
+      // depend on visited: a sibling may finalise a chunk (and rewrite its
+      // visited word) before this warp reads it. Only the owner reads
+      // visited for its decisions — it does so before its own unit can
+      // arrive, so it always sees the value the iteration started with.
+      const bool mine = dsh == 0 || (lane & ((1 << dsh) - 1)) == sub;
       if (has) {
         U = a.units[u];
         ubase = a.cs[U.chunk] + int64_t(U.col_begin) * 32;
         vis = a.visited[U.chunk];
         realm = U.chunk == a.n_chunks - 1 ? a.last_real : 0xffffffffu;
         skip = a.slimwork && vis == realm;  // should_skip_chunk
-        if (U.col_begin == 0 && sub == 0) {
+        if (U.col_begin == 0 && mine) {
           if (skip) {
             ++c_skip;
             Fn[U.chunk] = 0u;
@@ -939,9 +946,6 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         }
       }
       const uint32_t open_all = __ballot_sync(0xffffffffu, has && !skip);
-      // this sub-task's units: the d-th open unit of the task, d mod D == sub
-      const bool mine = dsh == 0 ||
-          (int32_t(__popc(open_all & ((1u << lane) - 1u))) & ((1 << dsh) - 1)) == sub;
       if (!mine) skip = true;
       // every lane prefetches the head (in sweep order) of its unit into L2
       if (kPfHeadSteps > 0 && has && !skip && U.col_len > 0) {
@@ -964,7 +968,10 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       uint32_t longs = __ballot_sync(0xffffffffu, is_long);
       uint32_t active = __ballot_sync(0xffffffffu, has && !skip && !is_long);
       {
-        const bool all_skipped = open_all == 0u;
+        // Retirement needs every unit's skip state, which only the unit's
+        // owner reads reliably: shared tasks (few active tasks, late
+        // iterations) are never retired; they mark themselves "not skipped".
+        const bool all_skipped = dsh == 0 && open_all == 0u;
         const uint32_t firsts = __ballot_sync(0xffffffffu, has && U.col_begin == 0);
         if (!kBuf) {
           if (lane == 0 && sub == 0) {

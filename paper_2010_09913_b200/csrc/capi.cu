@@ -406,12 +406,19 @@ int ssb_bfs_traditional(ssb_edges* e, int64_t root, int64_t* dist, int64_t* pare
 
 int ssb_validate_bfs(ssb_edges* e, int64_t root, const int64_t* dist, const int64_t* parent,
                      int flags, int64_t* violations, char* report, int64_t report_cap) {
+  return ssb_validate_bfs_exact(e, nullptr, root, dist, parent, flags,
+                                violations, report, report_cap);
+}
+
+int ssb_validate_bfs_exact(ssb_edges* e, const ssb_graph* layout, int64_t root, const int64_t* dist,
+                           const int64_t* parent, int flags, int64_t* violations, char* report,
+                           int64_t report_cap) {
   return guarded([&] {
     need(e, "edges");
     need(dist, "dist");
     need(violations, "violations");
     std::string text;
-    *violations = ssb::validate_bfs(*e, root, dist, parent, flags, text);
+    *violations = ssb::validate_bfs(*e, root, dist, parent, flags, text, layout);
     if (report && report_cap > 0) {
       const size_t k = std::min<size_t>(text.size(), size_t(report_cap - 1));
       std::memcpy(report, text.data(), k);

@@ -34,8 +34,11 @@ class Pool {
     for (auto& t : th_) t.join();
   }
   int size() const { return int(th_.size()) + 1; }
-  // f(w) on every worker w in [0, size()); the caller runs w = 0
+  // f(w) on every worker w in [0, size()); the caller runs w = 0. One job at
+  // a time: concurrent callers (e.g. one host thread per GPU, ctypes drops
+  // the GIL) queue on run_mu_ instead of overwriting each other's job.
   void run(const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> serial(run_mu_);
     {
       std::lock_guard<std::mutex> l(mu_);
       job_ = &f;
@@ -67,6 +70,7 @@ class Pool {
     }
   }
   std::vector<std::thread> th_;
+  std::mutex run_mu_;
   std::mutex mu_;
   std::condition_variable cv_, done_;
   const std::function<void(int)>* job_ = nullptr;

@@ -248,5 +248,5 @@ void parse_matrix_market(std::string_view text, std::vector<int64_t>& uv, int64_
 int64_t bfs_traditional(ssb_edges& e, int64_t root, int64_t* dist, int64_t* parent,
                         std::vector<ssb_iter_stats>& per_iter);
 int64_t validate_bfs(ssb_edges& e, int64_t root, const int64_t* dist, const int64_t* parent,
-                     int flags, std::string& report_text);
+                     int flags, std::string& report_text, const ssb_graph* layout = nullptr);
 }  // namespace ssb

@@ -149,6 +149,7 @@ enum : int32_t {
   kVRootParent = 6,      // root not self-parented
   kVParentRange = 7,     // parent outside [0, n) or not a neighbour
   kVParentLevel = 8,     // parent not one level closer
+  kVParentExact = 9,     // parent differs from the reference's deterministic rule
 };
 
 struct Violations {
@@ -203,7 +204,8 @@ __global__ void check_vertices_kernel(const int64_t* __restrict__ row, const int
       continue;
     }
     // the reference's sel-max root encoding gives the
-    // root and its depth-1 vertices the parent perm[root]: not checked
+    // root and its depth-1 vertices the parent perm[root]: not a tree edge
+    // (exact_parent_kernel checks that value when asked to)
     if ((flags & SSB_VALIDATE_SELMAX_COMPAT) && d <= 1) continue;
     if (d == 0) {
       if (p != v) report(out, kVRootParent, v, p);
@@ -214,6 +216,52 @@ __global__ void check_vertices_kernel(const int64_t* __restrict__ row, const int
       continue;
     }
     if (dist[p] != d - 1) report(out, kVParentLevel, v, p);
+  }
+}
+
+// The exact parent every reference variant returns (one warp per vertex,
+// the neighbour list scanned 32 at a time — hub rows hold 1M neighbours):
+//   min rule  (tropical / real / boolean, dp_transform semiring.cpp:159-187,
+//             == bfs_traditional's first discoverer):
+//             the smallest ORIGINAL-id neighbour one level closer;
+//   sel-max   (selmax_parents bfs.cpp:94-101, App. A.3):
+//             perm[max{inv_perm[u] : u ∈ N(v), d(u) = d(v) − 1}], and with
+//             the reference's root encoding (compat) perm[root] at levels 0-1.
+// The root is its own parent (min rule, sel-max without compat). Reached
+// vertices only; unreached ones are checked by check_vertices_kernel.
+__global__ void exact_parent_kernel(const int64_t* __restrict__ row, const int32_t* __restrict__ col,
+                                    int64_t n, int64_t root, const int64_t* __restrict__ dist,
+                                    const int64_t* __restrict__ parent, const int32_t* __restrict__ perm,
+                                    const int32_t* __restrict__ inv_perm, int flags, Violations* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const bool sel = (flags & SSB_VALIDATE_SELMAX_EXACT) != 0;
+  const bool compat = sel && (flags & SSB_VALIDATE_SELMAX_COMPAT) != 0;
+  for (int64_t v = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+    const int64_t d = dist[v];
+    if (d == INT64_MAX) continue;
+    int64_t want;
+    if (compat && d <= 1) {
+      want = perm[root];
+    } else if (d == 0) {
+      want = v;
+    } else {
+      // min rule: smallest id; sel-max: largest position (-1 = none found)
+      int64_t best = sel ? -1 : INT64_MAX;
+      for (int64_t e = row[v] + lane; e < row[v + 1]; e += 32) {
+        const int32_t u = col[e];
+        if (dist[u] != d - 1) continue;
+        if (sel) best = max(best, int64_t(inv_perm[u]));
+        else best = min(best, int64_t(u));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int64_t b = __shfl_xor_sync(0xffffffffu, best, o);
+        best = sel ? max(best, b) : min(best, b);
+      }
+      want = sel ? (best < 0 ? -2 : int64_t(perm[best])) : (best == INT64_MAX ? -2 : best);
+    }
+    if (lane == 0 && parent[v] != want) report(out, kVParentExact, v, want);
   }
 }
 
@@ -350,7 +398,7 @@ int64_t bfs_traditional(ssb_edges& e, int64_t root, int64_t* dist, int64_t* pare
 }
 
 int64_t validate_bfs(ssb_edges& e, int64_t root, const int64_t* dist, const int64_t* parent,
-                     int flags, std::string& report_text) {
+                     int flags, std::string& report_text, const ssb_graph* layout) {
   if (root < 0 || root >= e.n)
     fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(e.n) + ")");
   DevCsr& c = device_csr(e);
@@ -365,6 +413,20 @@ int64_t validate_bfs(ssb_edges& e, int64_t root, const int64_t* dist, const int6
   check_vertices_kernel<<<grid_for(n), 256, 0, s>>>(c.row.p, c.col.p, n, root, dd.p,
                                                     parent ? pp.p : nullptr, flags, vv.p);
   SSB_CUDA(cudaGetLastError());
+  if (parent && (flags & (SSB_VALIDATE_SELMAX_EXACT | SSB_VALIDATE_MIN_PARENT_EXACT))) {
+    if ((flags & SSB_VALIDATE_SELMAX_EXACT) && (flags & SSB_VALIDATE_MIN_PARENT_EXACT))
+      fail(SSB_EINVAL, "SSB_VALIDATE_SELMAX_EXACT and SSB_VALIDATE_MIN_PARENT_EXACT exclude each other");
+    const int32_t *perm = nullptr, *inv = nullptr;
+    if (flags & SSB_VALIDATE_SELMAX_EXACT) {
+      if (!layout) fail(SSB_EINVAL, "SSB_VALIDATE_SELMAX_EXACT needs the layout (perm / inv_perm)");
+      if (layout->n != n) fail(SSB_EINVAL, "layout and edge set have different vertex counts");
+      perm = layout->perm.p;
+      inv = layout->inv_perm.p;
+    }
+    exact_parent_kernel<<<grid_for(n * 32), 256, 0, s>>>(c.row.p, c.col.p, n, root, dd.p, pp.p, perm, inv,
+                                                         flags, vv.p);
+    SSB_CUDA(cudaGetLastError());
+  }
   Violations h{};
   SSB_CUDA(cudaMemcpyAsync(&h, vv.p, sizeof(h), cudaMemcpyDeviceToHost, s));
   e.sc.sync();
@@ -377,7 +439,8 @@ int64_t validate_bfs(ssb_edges& e, int64_t root, const int64_t* dist, const int6
                                "unreached but parent set",
                                "root not self-parented",
                                "parent is not a neighbor",
-                               "parent not one level closer"};
+                               "parent not one level closer",
+                               "parent differs from the reference rule; expected"};
   for (int i = 0; i < int(std::min<unsigned long long>(h.count, 4)); ++i) {
     char buf[160];
     const int32_t code = h.first_code[i];

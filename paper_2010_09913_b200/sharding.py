@@ -237,6 +237,11 @@ class P2PShard:
         rc = L.lib().ssb_bfs_p2p(self.r._h, int(root), C.byref(o), st, cap, k.ctypes.data_as(L.i64p),
                                  C.byref(ms))
         _check(rc)
+        if int(k[0]) > cap:  # every rank reruns the same root: the group stays in step
+            cap = int(k[0])
+            st = (L.IterStatsC * cap)()
+            _check(L.lib().ssb_bfs_p2p(self.r._h, int(root), C.byref(o), st, cap,
+                                       k.ctypes.data_as(L.i64p), C.byref(ms)))
         return int(k[0]), float(ms.value), _stats_list(st, int(k[0]))
 
     def fetch(self, want_parents: bool, dist: np.ndarray, parent: np.ndarray) -> None:
@@ -267,11 +272,15 @@ def run_p2p_group(reprs, ranges, root: int, opts, fetch: bool = True):
     rc = L.lib().ssb_bfs_p2p_group(hs, world, rg.ctypes.data_as(L.i64p), cnt.ctypes.data_as(L.i64p),
                                    int(root), C.byref(o), st, cap, k.ctypes.data_as(L.i64p), C.byref(ms))
     _check(rc)
-    if not fetch:
+    if int(k[0]) > cap:  # deeper than the first buffer: rerun once with room for every record
+        cap = int(k[0])
+        st = (L.IterStatsC * cap)()
+        _check(L.lib().ssb_bfs_p2p_group(hs, world, rg.ctypes.data_as(L.i64p), cnt.ctypes.data_as(L.i64p),
+                                         int(root), C.byref(o), st, cap, k.ctypes.data_as(L.i64p),
+                                         C.byref(ms)))
+    if not fetch:  # the BFS only (results stay on the devices)
         return None, None, _stats_list(st, int(k[0])), float(ms.value)
     n = reprs[0].n
-    if not fetch:  # the BFS only (results stay on the devices)
-        return None, None, per_iter
     dist = np.full(n, KINF, dtype=np.int64)
     parent = np.full(n, -1, dtype=np.int64)
     want = bool(opts.want_parents) and int(opts.variant) == 3

@@ -1,0 +1,198 @@
+"""GPU parity at the BENCHMARK configurations (BASELINE.json configs 2-4).
+
+The expected values are the unmodified reference's own outputs, recorded by
+tests/golden/make_golden_big.py into tests/golden/golden_big.json (layout
+FNVs, the Graph500 root lists, and per root the reference bfs_spmv's
+IterStats plus dist / parent fingerprints). On top, every root goes through
+the device's exact validator (ssb_validate_bfs_exact: Graph500 edge checks +
+every parent equal to the reference's deterministic rule), which pins dist and
+parent bit for bit without a host oracle.
+
+* config 2: Kronecker S22, C=32, σ=n, all four semirings, 16 Graph500 roots,
+  SlimWork on and off, SlimChunk L=2048 (128 BFS);
+* config 3: Kronecker S26, sel-max + SlimWork + L=2048, all 64 Graph500
+  roots of the bench + root 30,478,752, tropical parents
+  against the reference's queue BFS;
+* config 4: Erdős–Rényi 2^26, avg degree 16, sel-max, 16 roots.
+"""
+import gc
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIG = os.path.join(HERE, "golden", "golden_big.json")
+KEYS = ("iteration", "chunks_processed", "chunks_skipped", "subchunks_processed", "columns_processed",
+        "frontier_size")
+
+
+@pytest.fixture(scope="module")
+def big():
+    if not os.path.exists(BIG):
+        pytest.skip("tests/golden/golden_big.json missing")
+    with open(BIG) as f:
+        return json.load(f)
+
+
+def rows(stats):
+    return [[getattr(s, k) for k in KEYS] for s in stats]
+
+
+def ph(a):
+    import torch
+
+    from paper_2010_09913_b200.fingerprint import ph64_torch
+    return ph64_torch(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+
+
+def check_layout(port, r, lay, col_i32=True):
+    assert (r.n_cells, r.padding) == (lay["n_cells"], lay["padding"])
+    col = r.col32()
+    assert port.fnv_i32(col) == lay["col_fnv"], "col differs from the reference's build_slimsell"
+    del col
+    assert port.fnv(r.cs) == lay["cs_fnv"]
+    assert port.fnv(r.cl) == lay["cl_fnv"]
+    assert port.fnv(r.perm) == lay["perm_fnv"]
+    assert port.fnv(r.inv_perm) == lay["inv_perm_fnv"]
+
+
+def opts(ssb, v, sw, L):
+    return ssb.BfsOptions(variant=ssb.Variant(v), slimwork=sw, slimchunk_len=L)
+
+
+def run_case(ssb, g, r, db, c, exact_roots):
+    """One recorded reference case through the device: counters, dist and
+    parent fingerprints equal; exact validator when asked."""
+    o = opts(ssb, c["variant"], c["slimwork"], c["L"])
+    k, _, stats, rc = db.run(c["root"], o)
+    assert rc == 0 and k == c["iterations"], (c["root"], k, c["iterations"])
+    assert rows(stats) == c["stats"], f"IterStats differ for root {c['root']}"
+    want_par = c["parent_ph"] is not None
+    dist, par = db.fetch(want_par)
+    assert ph(dist) == c["dist_ph"], f"dist differs for root {c['root']}"
+    if want_par:
+        assert ph(par) == c["parent_ph"], f"parent differs for root {c['root']}"
+    if c["root"] in exact_roots and want_par:
+        rep = ssb.validate_bfs(g, c["root"], dist, par, selmax_compat=c["variant"] == 3,
+                               exact="selmax" if c["variant"] == 3 else "min", layout=r)
+        assert rep is None, rep
+
+
+def test_config2_s22_all_semirings_slimwork_on_off(ssb, port, big):
+    from paper_2010_09913_b200.fingerprint import graph500_roots
+    e = big["kron22"]
+    g = ssb.gen_kronecker(22, 16, 1)
+    assert (g.num_vertices(), g.num_edges()) == (e["n"], e["m"])
+    assert port.fnv(g.edges()) == e["edges_fnv"]
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    check_layout(port, r, e["layout"])
+    assert graph500_roots(r.degrees(), 16, 1) == e["roots"]
+    db = ssb.DeviceBfs(r)
+    assert len(e["cases"]) == 16 * 4 * 2
+    for c in e["cases"]:
+        run_case(ssb, g, r, db, c, exact_roots=set(e["roots"]))
+
+
+def test_config3_s26_selmax_64_roots_bit_exact(ssb, port, big):
+    from paper_2010_09913_b200.fingerprint import graph500_roots
+    e = big.get("kron26")
+    if not e:
+        pytest.skip("no S26 record")
+    g = ssb.gen_kronecker(26, 16, 1)
+    assert (g.num_vertices(), g.num_edges()) == (e["n"], e["m"])
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    check_layout(port, r, e["layout"])
+    assert graph500_roots(r.degrees(), 64, 1) == e["roots"]
+    db = ssb.DeviceBfs(r)
+    exact = set(e["roots"][:8]) | {30478752}
+    for c in e["cases"]:
+        run_case(ssb, g, r, db, c, exact_roots=exact)
+    # root 30,478,752 sweeps 5,746,402,784 cells in 7 iterations
+    c = next(x for x in e["cases"] if x["root"] == 30478752 and x["variant"] == 3)
+    assert c["iterations"] == 7 and 32 * sum(s[4] for s in c["stats"]) == 5746402784
+    # tropical / real / boolean parents: the reference's queue BFS (== dp_transform)
+    for t in e["traditional"]:
+        for v in (0, 2):
+            db.run(t["root"], opts(ssb, v, True, 2048))
+            dist, par = db.fetch(True)
+            assert ph(dist) == t["dist_ph"] and ph(par) == t["parent_ph"]
+        rep = ssb.validate_bfs(g, t["root"], dist, par, exact="min")
+        assert rep is None, rep
+    del db, r, g
+    gc.collect()
+
+
+def test_config4_er26_selmax_bit_exact(ssb, port, big):
+    from paper_2010_09913_b200.fingerprint import graph500_roots
+    e = big.get("er26")
+    if not e:
+        pytest.skip("no ER 2^26 record")
+    n = 1 << 26
+    g = ssb.gen_erdos_renyi(n, 16.0 / (n - 1), 1)
+    assert (g.num_vertices(), g.num_edges()) == (e["n"], e["m"])
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    check_layout(port, r, e["layout"])
+    assert graph500_roots(r.degrees(), len(e["roots"]), 1) == e["roots"]
+    db = ssb.DeviceBfs(r)
+    for c in e["cases"]:
+        run_case(ssb, g, r, db, c, exact_roots=set(e["roots"][:4]))
+    t = e["traditional"][0]
+    db.run(t["root"], opts(ssb, 0, True, 2048))
+    dist, par = db.fetch(True)
+    assert ph(dist) == t["dist_ph"] and ph(par) == t["parent_ph"]
+    del db, r, g
+    gc.collect()
+
+
+def test_exact_validator_rejects_valid_but_different_parents(ssb, port):
+    """A parent that is a neighbour one level up (valid for cli.cpp:73-112) but
+    not the one the reference returns must fail the exact check, and the
+    sel-max root encoding must be enforced at levels 0-1."""
+    g = ssb.gen_kronecker(14, 16, 1)
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    csr = ssb.to_csr(g)
+    deg = np.diff(csr.row)
+    root = int(np.argmax(deg))
+    res = ssb.bfs_spmv(r, root, opts(ssb, 3, True, 64))
+    dist, par = res.dist.copy(), res.parent.copy()
+    assert ssb.validate_bfs(g, root, dist, par, selmax_compat=True, exact="selmax", layout=r) is None
+    # a level >= 2 vertex with two candidate parents: swap in the other one
+    inv = r.inv_perm
+    for v in np.nonzero(dist == 2)[0]:
+        nb = csr.col[csr.row[v]:csr.row[v + 1]]
+        cand = nb[dist[nb] == 1]
+        if len(cand) >= 2:
+            alt = int(cand[np.argmin(inv[cand])])
+            assert alt != par[v]
+            bad = par.copy()
+            bad[v] = alt
+            assert ssb.validate_bfs(g, root, dist, bad, selmax_compat=True) is None  # tree-valid
+            rep = ssb.validate_bfs(g, root, dist, bad, selmax_compat=True, exact="selmax", layout=r)
+            assert rep is not None and "reference rule" in rep
+            break
+    else:
+        pytest.fail("no level-2 vertex with two candidate parents")
+    # compat: depth-1 parents are perm[root]; the corrected value root fails
+    v1 = int(np.nonzero(dist == 1)[0][0])
+    if int(r.perm[root]) != root:
+        bad = par.copy()
+        bad[v1] = root
+        assert ssb.validate_bfs(g, root, dist, bad, selmax_compat=True, exact="selmax", layout=r) is not None
+    # min rule: tropical parents from the device equal the smallest-id rule; a
+    # larger valid neighbour fails
+    res = ssb.bfs_spmv(r, root, opts(ssb, 0, True, 64), csr)
+    assert ssb.validate_bfs(g, root, res.dist, res.parent, exact="min") is None
+    bad = res.parent.copy()
+    for v in np.nonzero(res.dist == 2)[0]:
+        nb = csr.col[csr.row[v]:csr.row[v + 1]]
+        cand = nb[res.dist[nb] == 1]
+        if len(cand) >= 2:
+            bad[v] = int(cand.max())
+            break
+    assert ssb.validate_bfs(g, root, res.dist, bad, exact="min") is not None
+    with pytest.raises(ssb.InvalidArgument):
+        ssb.validate_bfs(g, root, dist, par, exact="selmax")  # needs the layout
