@@ -365,13 +365,13 @@ def free_port() -> int:
         return sk.getsockname()[1]
 
 
-def spawn_ranks(n: int) -> int:
+def spawn_ranks(n: int, script: str | None = None, argv: list[str] | None = None) -> int:
     """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks
     (one process per GPU) under torch.distributed.run on 127.0.0.1; rank 0
     prints the JSON line."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
-           *sys.argv[1:]]
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script or os.path.abspath(__file__),
+           *(sys.argv[1:] if argv is None else argv)]
     return subprocess.run(cmd).returncode
 
 
@@ -389,6 +389,16 @@ def peer_access_ok(torch, world: int) -> tuple[bool, str]:
     return True, "peer access between every pair"
 
 
+def choose_shard(torch, world: int) -> tuple[str, str]:
+    """Default decomposition: one GPU -> the single-GPU engine; N > 1 ->
+    north_star's chunk-range shards, fused peer exchange when every pair of
+    GPUs maps each other's memory, else the NCCL all-gather form."""
+    if world <= 1:
+        return "roots", "single GPU"
+    ok, why = peer_access_ok(torch, world)
+    return ("p2p" if ok else "chunks"), why
+
+
 def main():
     a = args_()
     world, rank, local = dist_env()
@@ -403,12 +413,9 @@ def main():
         return main_reference(a, world, rank, local, log, variant_id, slimwork, cores)
     shard = a.shard
     if shard is None:
-        shard = "roots"
-        if world > 1:
-            import torch
-            ok, why = peer_access_ok(torch, world)
-            shard = "p2p" if ok else "chunks"
-            log(f"N={world}: --shard {shard} ({why})")
+        import torch
+        shard, why = choose_shard(torch, world)
+        log(f"N={world}: --shard {shard} ({why})")
     if shard == "chunks":
         return main_chunks(a, world, rank, local, log, variant_id, slimwork)
     if shard == "p2p":
@@ -613,100 +620,201 @@ def main():
         dist.destroy_process_group()
 
 
+def sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n):
+    """m_cc and reference parity of a sharded BFS without gathering vectors:
+    each rank fetches its OWNED rows (other entries keep the -2 sentinel),
+    sums their degrees and their ph64 terms; one all-reduce per root adds the
+    ranks' partials (ph64 is a sum over positions)."""
+    from paper_2010_09913_b200.fingerprint import ph64_format, ph64_partial_torch
+    _, cases = golden_entry(a)
+    mcc, g_cmp, g_eq = {}, 0, 0
+    dd = np.empty(n, np.int64)
+    pp = np.empty(n, np.int64)
+    deg_t = torch.from_numpy(deg).cuda()
+    for root in roots:
+        dd.fill(-2)
+        pp.fill(-2)
+        run_fetch(root, dd, pp)
+        td = torch.from_numpy(dd).cuda()
+        mine = td != -2
+        reached = mine & (td != np.iinfo(np.int64).max)
+        deg_sum = int(deg_t[reached].sum().item())
+        c = cases.get((root, variant_id, slimwork, a.slimchunk))
+        parts = [deg_sum, 0, 0]
+        if c is not None:
+            parts[1] = ph64_partial_torch(td, mine)
+            if variant_id == 3:
+                tp = torch.from_numpy(pp).cuda()
+                parts[2] = ph64_partial_torch(tp, tp != -2)
+        t = torch.tensor(parts, dtype=torch.int64, device=RED_DEV)
+        if world > 1:
+            dist_mod.all_reduce(t)
+        deg_tot, dph, pph = (int(x) for x in t.cpu().tolist())
+        mcc[root] = deg_tot // 2
+        if c is not None:
+            g_cmp += 1
+            g_eq += int(ph64_format(dph) == c["dist_ph"] and
+                        (variant_id != 3 or ph64_format(pph) == c["parent_ph"]))
+    return mcc, {"roots_compared": g_cmp, "roots_equal": g_eq,
+                 "what": "ph64 of the assembled dist (and sel-max parent) vs the unmodified reference's "
+                         "bfs_spmv (tests/golden/golden_big.json); partial sums over each rank's owned "
+                         "rows, all-reduced"}
+
+
+def shard_evidence(a, world, n_padded, iters_first, cells_rank, peak):
+    """Exchange volume and its NVLink floor next to the HBM figures."""
+    words = (n_padded + 31) // 32
+    per_iter_rank_in = 4 * words * (world - 1) // max(world, 1)  # bytes each rank receives per iteration
+    return {"frontier_words": words, "exchange_bytes_per_iteration_per_rank": per_iter_rank_in,
+            "nvlink_gbs_assumed": 900.0,
+            "nvlink_floor_us_per_iteration": round(per_iter_rank_in / 900e9 * 1e6, 2),
+            "cells_per_rank": cells_rank, "iterations_first_root": iters_first,
+            "hbm_peak_gbs": peak}
+
+
 def main_chunks(a, world, rank, local, log, variant_id, slimwork):
-    """Chunk-range sharding: every rank sweeps its contiguous,
-    cell-balanced chunk range of every BFS; one NCCL all-gather of the owned
-    frontier words per iteration (paper_2010_09913_b200.sharding)."""
+    """Chunk-range sharding: every rank holds and sweeps its
+    contiguous, cell-balanced chunk range (range build: its own cells only)
+    plus the replicated 1-bit frontier; one all-gather of the owned frontier
+    words per iteration. Under NCCL the iteration loop has no host round trip:
+    the all-gather is enqueued on the shard's stream between the sweep and
+    the exchange, |F| is counted on the device, and the host polls |F_{k-1}|
+    while k is queued (sharding.run_sharded_bfs_async); counters are summed
+    once per BFS. Under gloo (ranks sharing one GPU: a functional check) the
+    words go through host memory and every step synchronises."""
     import torch
 
     import paper_2010_09913_b200 as ssb
     from paper_2010_09913_b200.sharding import DeviceShard, TorchComm, partition_chunks, run_sharded_bfs
 
-    dev = init_dist(torch, ssb, world, local)
+    init_dist(torch, ssb, world, local)
+    import torch.distributed as dist_mod
 
     def barrier():
         if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
+            dist_mod.barrier()
         torch.cuda.synchronize()
 
-    g, r, m, t_gen, t_build = build_graph(ssb, a, log)
-    deg = r.degrees()
+    t0 = time.time()
+    g = (ssb.gen_erdos_renyi(1 << a.scale, a.avg_degree / ((1 << a.scale) - 1), a.seed) if a.graph == "er"
+         else ssb.gen_kronecker(a.scale, a.edgefactor, a.seed))
+    t_gen = time.time() - t0
+    n = g.num_vertices()
+    meta = ssb.build_slimsell(g, 32, n, chunk_range=(0, 0))  # perm / cl / degrees, no cells
+    deg = meta.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
-    ranges = partition_chunks(r.cl, 32, world)
+    ranges = partition_chunks(meta.cl, 32, world)
+    del meta
+    t0 = time.time()
+    r = ssb.build_slimsell(g, 32, n, chunk_range=ranges[rank])
+    t_build = time.time() - t0
+    log(f"graph S{a.scale}: n={n} m={g.num_edges()}; rank 0 holds chunks {ranges[0]} = {r.range_cells} of "
+        f"{r.n_cells} cells; gen {t_gen:.2f}s build {t_build:.2f}s")
+    del g
     shard = DeviceShard(r, *ranges[rank])
-    if world > 1:
-        comm = TorchComm(ranges)
-    else:
-        from paper_2010_09913_b200.sharding import LocalComm
-        comm = LocalComm()
+
+    class OneRank:  # N = 1: the same asynchronous loop, nothing to exchange
+        device_async = True
+
+        def allgather_frontier(self, owned_list):
+            return owned_list[0]
+
+        def allreduce_sum(self, arrays):
+            return arrays[0]
+
+    comm = TorchComm(ranges) if world > 1 else OneRank()
+    mode = "async" if getattr(comm, "device_async", False) else "sync"
     opts = ssb.BfsOptions(variant=ssb.Variant(variant_id), slimwork=slimwork, slimchunk_len=a.slimchunk)
+    launches = [0]
 
     def one(root):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        dist_, parent_, per_iter = run_sharded_bfs([shard], comm, root, opts, fetch=False)
-        e1.record()
-        torch.cuda.synchronize()
+        if mode == "async":
+            _, _, per_iter = run_sharded_bfs([shard], comm, root, opts, fetch=False)
+            ms = shard.last_ms  # CUDA events on the shard's stream around the whole BFS
+        else:
+            t = time.perf_counter()
+            _, _, per_iter = run_sharded_bfs([shard], comm, root, opts, fetch=False)
+            torch.cuda.synchronize()
+            ms = (time.perf_counter() - t) * 1e3
         launches[0] += shard.launches()
-        return e0.elapsed_time(e1), per_iter
-
-    launches = [0]
+        return ms, per_iter
 
     for _ in range(a.warmup):
         for root in roots:
             one(root)
-    mcc = {}
     sampler = ClockSampler(local)
     barrier()
     sampler.start()
     step_ms = []
     launches[0] = 0
-    for s in range(a.steps):
+    first_iter = None
+    swept = 0
+    for s_ in range(a.steps):
         tot = 0.0
         for root in roots:
             ms, per_iter = one(root)
             tot += ms
+            first_iter = first_iter or per_iter
+            if s_ == 0:
+                swept += ssb.DeviceBfs(r).columns_swept()
         step_ms.append(tot)
     barrier()
     clocks = sampler.stop()
-    # m_cc from the assembled distances (owned rows gathered by MIN over ranks)
-    e_edges = 0
-    dist_all = {}
-    for root in roots:
-        d, _, _ = run_sharded_bfs([shard], comm, root, opts)
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.from_numpy(d).cuda()
-            dist.all_reduce(t, op=dist.ReduceOp.MIN)
-            d = t.cpu().numpy()
-        mcc[root] = m_cc_of(d, deg)
+
+    def run_fetch(root, dd, pp):
+        run_sharded_bfs([shard], comm, root, opts, fetch=False)
+        shard.fetch(variant_id == 3, dd, pp)
+
+    mcc, golden = sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n)
     my_ms = float(np.mean(step_ms))
-    max_ms = my_ms
+    t = torch.tensor([my_ms, swept], dtype=torch.float64, device=RED_DEV)
+    per_rank_ms = [my_ms]
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([my_ms], dtype=torch.float64, device=RED_DEV)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_ms = float(t.item())
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist_mod.all_gather(allt, t)
+        per_rank_ms = [float(x[0].item()) for x in allt]
+        swept_all = [float(x[1].item()) for x in allt]
+    else:
+        swept_all = [float(swept)]
+    max_ms = max(per_rank_ms)
     value = sum(mcc.values()) / (max_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    if world > 1:
+        ct = torch.tensor([r.range_cells], dtype=torch.int64, device=RED_DEV)
+        allc = [torch.zeros_like(ct) for _ in range(world)]
+        dist_mod.all_gather(allc, ct)
+        cells = [int(x.item()) for x in allc]
+    else:
+        cells = [r.range_cells]
+    ev = shard_evidence(a, world, r.n_padded, len(first_iter), cells, peak)
+    # HBM side: the busiest rank's swept col bytes per step over its time
+    hbm_gbs = max(128.0 * sw for sw in swept_all) / (max_ms * 1e-3) / 1e9
+    ev.update({"per_rank_ms_per_step": [round(x, 3) for x in per_rank_ms],
+               "hbm_achieved_gbs_busiest_rank_col_stream": round(hbm_gbs, 1),
+               "comm": (f"NCCL all_gather_into_tensor on the shard stream, {world} ranks" if world > 1 and
+                        mode == "async" else ("gloo all_gather through host memory (functional)"
+                                              if world > 1 else "single rank")),
+               "stepping": mode})
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(max_ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": DATA[a.graph],
-        "config": config_of(a, slimwork, len(roots), f"chunk-range shards x{world}, NCCL frontier all-gather"),
+        "config": config_of(a, slimwork, len(roots), f"chunk-range shards x{world}, frontier all-gather"),
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "chunk-sharded mode reports device time only"},
         "clocks": clocks, "gpu_launches": int(launches[0]),
+        "sharding": ev, "validation": {"reference_golden": golden},
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
-                   "build_s": round(t_build, 3)},
+                   "build_s": round(t_build, 3),
+                   "clock": "CUDA events on the shard stream" if mode == "async" else
+                            "host wall per BFS (gloo functional mode: every step synchronises)"},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+        dist_mod.destroy_process_group()
 
 
 def main_p2p(a, world, rank, local, log, variant_id, slimwork):
@@ -785,31 +893,39 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork):
         step_ms.append(sum(one(root)[0] for root in roots))
     barrier()
     clocks = sampler.stop()
-    # m_cc per root from the assembled distances (owned rows, MIN over ranks)
-    mcc = {}
-    dd = np.full(n, np.iinfo(np.int64).max, np.int64)
-    pp = np.full(n, -1, np.int64)
-    for root in roots:
+    # m_cc and reference parity per root from each rank's owned rows
+    import torch.distributed as dist_mod
+
+    def run_fetch(root, dd, pp):
         if emu > 1:
-            _, d = one(root, fetch=True)
+            d, p, _, _ = run_p2p_group(reprs, ranges, root, opts, fetch=True)
+            dd[:] = d
+            if len(p):
+                pp[:] = p
         else:
             one(root)
-            dd.fill(np.iinfo(np.int64).max)
-            shard.fetch(False, dd, pp)
-            d = dd
-            if world > 1:
-                import torch.distributed as dist
-                t = torch.from_numpy(d).cuda()
-                dist.all_reduce(t, op=dist.ReduceOp.MIN)
-                d = t.cpu().numpy()
-        mcc[root] = m_cc_of(d, deg)
-    max_ms = float(np.mean(step_ms))
+            shard.fetch(variant_id == 3, dd, pp)
+
+    mcc, golden = sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n)
+    my_ms = float(np.mean(step_ms))
+    per_rank_ms = [my_ms]
+    cells = [x.range_cells for x in (reprs if emu > 1 else [r])]
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([max_ms], dtype=torch.float64, device=RED_DEV)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_ms = float(t.item())
+        t = torch.tensor([my_ms, float(r.range_cells)], dtype=torch.float64, device=RED_DEV)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist_mod.all_gather(allt, t)
+        per_rank_ms = [float(x[0].item()) for x in allt]
+        cells = [int(x[1].item()) for x in allt]
+    max_ms = max(per_rank_ms)
     value = sum(mcc.values()) / (max_ms * 1e-3) / 1e9
+    peak, _ = hbm_peak()
+    ev = shard_evidence(a, max(world, emu), r.n_padded, None, cells, peak)
+    ev.update({"per_rank_ms_per_step": [round(x, 3) for x in per_rank_ms],
+               "segments_per_rank": a.segments,
+               "exchange": ("peer stores + atomicOr into every peer's IPC-mapped window, in-kernel counter "
+                            "barrier (ld.acquire.sys); one cooperative launch per BFS per rank" if emu == 1 else
+                            "ranks emulated in one cooperative launch; windows are plain device memory"),
+               "peer_windows_mapped": (world - 1) if emu == 1 else 0})
     par = (f"chunk-range shards x{world} ({a.segments} round-robin segments each), fused in-kernel "
            f"frontier exchange" if emu == 1 else
            f"{emu} chunk-range shards ({a.segments} round-robin segments each) emulated in one launch on "
@@ -825,14 +941,14 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork):
         "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "note": "p2p-sharded mode reports device time only"},
         "clocks": clocks, "gpu_launches": 2 * len(roots) * a.steps,
+        "sharding": ev, "validation": {"reference_golden": golden},
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
                    "build_s": round(t_build, 3)},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+        dist_mod.destroy_process_group()
 
 
 def lscpu_model() -> str:

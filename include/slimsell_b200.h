@@ -168,6 +168,17 @@ void ssb_graph_destroy(ssb_graph* g);
  * untouched. EINVAL for a bad range or variant. */
 int ssb_spmv_step(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* out,
                   int64_t chunk_begin, int64_t chunk_end);
+/* The same with x_prev / out in DEVICE memory (n_padded int64 each): one warp
+ * per work unit of <= 1024 columns (hub chunks split, folded by 64-bit
+ * atomics), no host copies. device_ms (may be NULL): CUDA-event time. */
+int ssb_spmv_step_device(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* out,
+                         int64_t chunk_begin, int64_t chunk_end, double* device_ms);
+/* spmv_segment (repr.hpp:79-81, repr.cpp:20-35, 153-170): acc[lane] =
+ * plus(acc[lane], times(x_prev[c], edge or pad)) over columns [col_begin,
+ * col_begin + col_len) of `chunk`; x_prev n_padded int64, acc C int64 (in/out),
+ * host memory. EINVAL for a chunk or column range outside the layout. */
+int ssb_spmv_segment(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* acc, int64_t chunk,
+                     int64_t col_begin, int64_t col_len);
 
 /* bfs_spmv (bfs.hpp:80-81, bfs.cpp:222-246): algebraic BFS on the device.
  * dist: n int64 in original ids, INT64_MAX when unreached. parent: n int64
@@ -223,6 +234,28 @@ int ssb_bfs_shard_begin(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
 int ssb_bfs_shard_step(ssb_graph* g, ssb_iter_stats* local, uint32_t* owned_words);
 int ssb_bfs_shard_exchange(ssb_graph* g, const uint32_t* frontier_words, int64_t newly_total);
 int ssb_bfs_shard_fetch(ssb_graph* g, int want_parents, int64_t* dist, int64_t* parent);
+/* The same iteration without a host round trip (the NCCL form of SURVEY.md
+ * §8(e)): the sweep reads |F_{k-1}|, the active task list and the retired-
+ * chunk count from a device-resident carry, so nothing returns to the host
+ * between iterations. Per iteration k:
+ *   ssb_bfs_shard_step_async      sweep + owned words copied out, on the
+ *                                 graph's stream (ssb_graph_stream);
+ *   <the caller's all-gather>     enqueued on that same stream (NCCL);
+ *   ssb_bfs_shard_exchange_async  full frontier installed, summary rebuilt,
+ *                                 global |F_k| counted on the device.
+ * ssb_bfs_shard_front(k) waits for iteration k's exchange only and returns
+ * |F_k| (poll k-1 while k is queued; an iteration queued after convergence
+ * does nothing). ssb_bfs_shard_finish(iterations) returns this rank's
+ * per-iteration counters (local to its chunks: sum them over ranks once per
+ * BFS) and the device time since begin. Then ssb_bfs_shard_fetch. */
+int ssb_graph_stream(ssb_graph* g, void** stream);
+int ssb_bfs_shard_begin_async(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
+                              int64_t chunk_begin, int64_t chunk_end);
+int ssb_bfs_shard_step_async(ssb_graph* g, uint32_t* owned_words);
+int ssb_bfs_shard_exchange_async(ssb_graph* g, const uint32_t* frontier_words);
+int ssb_bfs_shard_front(ssb_graph* g, int64_t k, int64_t* front);
+int ssb_bfs_shard_finish(ssb_graph* g, int64_t iterations, ssb_iter_stats* stats, int64_t stats_cap,
+                         double* device_ms);
 /* ---- multi-GPU, fused: chunk-range shards whose frontier exchange runs
  * inside the BFS kernel (replaces the per-iteration host
  * round trip of ssb_bfs_shard_*). Each rank's frontier bitmaps live in a

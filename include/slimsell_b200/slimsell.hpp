@@ -16,8 +16,12 @@
 //  * BfsOptions::schedule / workers are accepted and ignored.
 //  * BfsOptions::selmax_compat (default true) reproduces the reference's
 //    sel-max root encoding; false gives corrected parents.
-//  * bfs_traditional is the reference's CPU oracle and is not part of this
-//    library.
+//  * bfs_traditional (both overloads) runs the reference's queue BFS on the
+//    device; the CsrView overload expects a symmetric CSR (as to_csr returns).
+//  * A layout the REFERENCE built on the host (any struct with the
+//    repr.hpp:33-55 members, e.g. slimsell::SlimSellRepr) goes through
+//    upload(): copied to the device once and cached by a fingerprint, so the
+//    bfs_spmv / spmv_step / spmv_segment overloads taking it cost one upload.
 #pragma once
 
 #include <algorithm>
@@ -27,7 +31,9 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <optional>
+#include <type_traits>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -362,6 +368,107 @@ inline std::vector<val_t> spmv_step(const SlimSellRepr& r, const SemiringSpec& s
   return out;
 }
 
+/// repr.hpp:79-81 (repr.cpp:20-35) — one chunk's column range folded into
+/// C accumulators with the literal int64 semiring, on the device.
+inline void spmv_segment(const SlimSellRepr& r, const SemiringSpec& s, std::span<const val_t> x_prev,
+                         std::span<val_t> acc, std::int64_t chunk, std::int64_t col_begin,
+                         std::int64_t col_len) {
+  if (x_prev.size() != static_cast<std::size_t>(r.n_padded)) throw std::invalid_argument("x_prev length");
+  if (acc.size() != static_cast<std::size_t>(r.C)) throw std::invalid_argument("acc length must be C");
+  detail::check(ssb_spmv_segment(r.handle(), static_cast<int>(s.variant), x_prev.data(), acc.data(), chunk,
+                                 col_begin, col_len));
+}
+
+// ---- host layouts built by the reference (repr.hpp:33-55) -----------------
+namespace detail {
+template <class R, class = void>
+struct is_host_repr : std::false_type {};
+template <class R>
+struct is_host_repr<R, std::void_t<decltype(std::declval<const R&>().col.data()),
+                                   decltype(std::declval<const R&>().cs.data()),
+                                   decltype(std::declval<const R&>().cl.data()),
+                                   decltype(std::declval<const R&>().perm.data()),
+                                   decltype(std::declval<const R&>().n_padded),
+                                   decltype(std::declval<const R&>().nonzeros)>>
+    : std::bool_constant<!std::is_same_v<std::decay_t<R>, SlimSellRepr> &&
+                         std::is_convertible_v<decltype(std::declval<const R&>().col.data()),
+                                               const std::int64_t*>> {};
+
+inline std::uint64_t fnv_mix(std::uint64_t h, std::int64_t v) {
+  for (int b = 0; b < 8; ++b) {
+    h ^= (static_cast<std::uint64_t>(v) >> (8 * b)) & 0xffu;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+/// Cheap identity of a host layout: the scalars, cs.back(),
+/// and col / perm / cl sampled — their first and last 4096 entries in full
+/// (cli.cpp:200-207's corrupt_repr rewrites the FIRST real cell) plus 4096
+/// strided samples. Arbitrary rewrites in the middle of col can escape it:
+/// call upload(r, true) after mutating a layout in place.
+template <class R>
+std::uint64_t layout_fingerprint(const R& r) {
+  std::uint64_t h = 0xcbf29ce484222325ull;
+  for (std::int64_t v : {std::int64_t(r.C), std::int64_t(r.sigma), std::int64_t(r.n), std::int64_t(r.n_chunks),
+                         std::int64_t(r.nonzeros), std::int64_t(r.col.size()), std::int64_t(r.cs.size())})
+    h = fnv_mix(h, v);
+  auto sample = [&h](const auto& v) {
+    const std::size_t n = v.size();
+    const std::size_t head = std::min<std::size_t>(n, 4096);
+    for (std::size_t i = 0; i < head; ++i) h = fnv_mix(h, v[i]);
+    for (std::size_t i = n > 4096 ? n - 4096 : head; i < n; ++i) h = fnv_mix(h, v[i]);
+    if (n > 8192)
+      for (std::size_t k = 0; k < 4096; ++k) h = fnv_mix(h, v[(n / 4096) * k + k % 7]);
+  };
+  sample(r.col);
+  sample(r.cs);
+  sample(r.cl);
+  sample(r.perm);
+  return h;
+}
+struct UploadCache {
+  std::mutex mu;
+  std::uint64_t key = 0;
+  std::optional<SlimSellRepr> dev;
+};
+inline UploadCache& upload_cache() {
+  static UploadCache c;
+  return c;
+}
+}  // namespace detail
+
+/// A host SlimSellRepr built by the reference (repr.hpp:33-55: C, sigma, n,
+/// n_chunks, nonzeros, col, cs, cl, perm) on the device — uploaded through
+/// ssb_graph_from_layout once, then served from a one-entry cache keyed by
+/// detail::layout_fingerprint (force = true re-uploads).
+template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline SlimSellRepr upload(const HostRepr& r, bool force = false) {
+  auto& c = detail::upload_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  const std::uint64_t key = detail::layout_fingerprint(r);
+  if (!force && c.dev && c.key == key) return *c.dev;
+  ssb_graph* h = nullptr;
+  detail::check(ssb_graph_from_layout(r.n, r.C, r.sigma, r.nonzeros, r.col.data(),
+                                      static_cast<std::int64_t>(r.col.size()), r.cs.data(), r.cl.data(),
+                                      static_cast<std::int64_t>(r.cs.size()), r.perm.data(), &h));
+  c.dev.emplace(h);
+  c.key = key;
+  return *c.dev;
+}
+
+template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline void spmv_step(const HostRepr& r, const SemiringSpec& s, std::span<const val_t> x_prev,
+                      std::span<val_t> out, std::int64_t chunk_begin, std::int64_t chunk_end) {
+  spmv_step(upload(r), s, x_prev, out, chunk_begin, chunk_end);
+}
+
+template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline void spmv_segment(const HostRepr& r, const SemiringSpec& s, std::span<const val_t> x_prev,
+                         std::span<val_t> acc, std::int64_t chunk, std::int64_t col_begin,
+                         std::int64_t col_len) {
+  spmv_segment(upload(r), s, x_prev, acc, chunk, col_begin, col_len);
+}
+
 /// repr.hpp:104-107 (repr.cpp:239-253) — pure relabelling through perm.
 inline std::vector<val_t> permute_in(std::span<const val_t> v, const SlimSellRepr& r, val_t fill) {
   if (v.size() != static_cast<std::size_t>(r.n)) throw std::invalid_argument("input vector length");
@@ -498,6 +605,13 @@ inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& o
   return res;
 }
 
+/// bfs.hpp:80-81 on a layout the reference built on the host (upload()).
+template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline BfsResult bfs_spmv(const HostRepr& r, vid_t root, const BfsOptions& opts,
+                          const CsrView* csr_for_parents = nullptr) {
+  return bfs_spmv(upload(r), root, opts, csr_for_parents);
+}
+
 /// Extension: a Graph500 root list through ssb_bfs_spmv_batch — results as
 /// from bfs_spmv per root (no per_iter records), root i's host fetch
 /// overlapped with root i+1's BFS on the device.
@@ -563,6 +677,29 @@ inline BfsResult bfs_traditional(const Graph& g, vid_t root) {
     res.per_iter.push_back(s);
   }
   return res;
+}
+
+/// bfs.hpp:85 (bfs.cpp:248-291) on a CSR: its arcs become the normalised
+/// edge set on the device (a symmetric CSR, as to_csr returns, gives exactly
+/// the reference's traversal), then the device queue BFS.
+inline BfsResult bfs_traditional(const CsrView& csr, vid_t root) {
+  const vid_t n = csr.num_vertices();
+  if (root < 0 || root >= n)
+    throw std::out_of_range("root " + std::to_string(root) + " outside [0, " + std::to_string(n) + ")");
+  std::vector<std::int64_t> uv;
+  uv.reserve(csr.col.size());
+  for (vid_t u = 0; u < n; ++u)
+    for (vid_t e = csr.row[u]; e < csr.row[u + 1]; ++e)
+      if (u < csr.col[e]) {
+        uv.push_back(u);
+        uv.push_back(csr.col[e]);
+      } else if (csr.col[e] < u && !csr.has_edge(csr.col[e], u)) {  // an arc with no mirror
+        uv.push_back(csr.col[e]);
+        uv.push_back(u);
+      }
+  ssb_edges* h = nullptr;
+  detail::check(ssb_edges_from_pairs(uv.data(), static_cast<std::int64_t>(uv.size() / 2), n, &h));
+  return bfs_traditional(Graph(h), root);
 }
 
 /// cli.cpp:73-112 (verify_against_oracle's tree checks) + Graph500 edge

@@ -87,6 +87,9 @@ def lib() -> C.CDLL:
         "ssb_bfs_last_timing": (C.c_int, [vp, C.POINTER(C.c_double), i64p]),
         "ssb_graph_destroy": (None, [vp]),
         "ssb_spmv_step": (C.c_int, [vp, C.c_int, i64p, i64p, C.c_int64, C.c_int64]),
+        "ssb_spmv_step_device": (C.c_int, [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                           C.POINTER(C.c_double)]),
+        "ssb_spmv_segment": (C.c_int, [vp, C.c_int, i64p, i64p, C.c_int64, C.c_int64, C.c_int64]),
         "ssb_bfs_spmv": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), i64p, i64p, i64p,
                                    C.POINTER(IterStatsC), C.c_int64, i64p]),
         "ssb_bfs_spmv_batch": (C.c_int, [vp, i64p, C.c_int64, C.POINTER(BfsOptionsC), C.POINTER(i64p),
@@ -104,6 +107,13 @@ def lib() -> C.CDLL:
         "ssb_bfs_shard_step": (C.c_int, [vp, C.POINTER(IterStatsC), C.c_void_p]),
         "ssb_bfs_shard_exchange": (C.c_int, [vp, C.c_void_p, C.c_int64]),
         "ssb_bfs_shard_fetch": (C.c_int, [vp, C.c_int, i64p, i64p]),
+        "ssb_graph_stream": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
+        "ssb_bfs_shard_begin_async": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.c_int64, C.c_int64]),
+        "ssb_bfs_shard_step_async": (C.c_int, [vp, C.c_void_p]),
+        "ssb_bfs_shard_exchange_async": (C.c_int, [vp, C.c_void_p]),
+        "ssb_bfs_shard_front": (C.c_int, [vp, C.c_int64, i64p]),
+        "ssb_bfs_shard_finish": (C.c_int, [vp, C.c_int64, C.POINTER(IterStatsC), C.c_int64,
+                                           C.POINTER(C.c_double)]),
         "ssb_p2p_window": (C.c_int, [vp, C.c_void_p, i64p]),
         "ssb_p2p_attach": (C.c_int, [vp, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int64]),
         "ssb_bfs_p2p": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.POINTER(IterStatsC), C.c_int64,

@@ -372,6 +372,36 @@ def spmv_step(r: SlimSellRepr, variant: Variant, x_prev, out=None, chunk_begin: 
     return out
 
 
+def spmv_step_device(r: SlimSellRepr, variant: Variant, x_prev, out, chunk_begin: int = 0,
+                     chunk_end: int | None = None) -> float:
+    """spmv_step with DEVICE operands (torch int64 CUDA tensors of n_padded):
+    no host copies; returns the kernels' device time in ms."""
+    for t, nm in ((x_prev, "x_prev"), (out, "out")):
+        if not t.is_cuda or t.dtype.itemsize != 8 or t.numel() != r.n_padded or not t.is_contiguous():
+            raise InvalidArgument(f"{nm} must be a contiguous int64 CUDA tensor of n_padded = {r.n_padded}")
+    ce = r.n_chunks if chunk_end is None else chunk_end
+    import torch
+    torch.cuda.current_stream().synchronize()  # the library stream reads the tensors next
+    ms = C.c_double()
+    _check(_L.lib().ssb_spmv_step_device(r._h, int(variant), C.c_void_p(x_prev.data_ptr()),
+                                         C.c_void_p(out.data_ptr()), chunk_begin, ce, C.byref(ms)))
+    return float(ms.value)
+
+
+def spmv_segment(r: SlimSellRepr, variant: Variant, x_prev, acc, chunk: int, col_begin: int,
+                 col_len: int) -> np.ndarray:  # repr.hpp:79-81
+    """acc[lane] = plus(acc[lane], times(x_prev[c], edge/pad)) over columns
+    [col_begin, col_begin + col_len) of `chunk` (repr.cpp:20-35); acc is
+    updated in place (C int64) and returned."""
+    x = np.ascontiguousarray(x_prev, dtype=np.int64)
+    if x.shape[0] != r.n_padded:
+        raise InvalidArgument(f"x_prev length {x.shape[0]}, expected {r.n_padded}")
+    if acc.shape[0] != r.C or acc.dtype != np.int64 or not acc.flags.c_contiguous:
+        raise InvalidArgument(f"acc must be contiguous int64[C = {r.C}]")
+    _check(_L.lib().ssb_spmv_segment(r._h, int(variant), _p(x), _p(acc), chunk, col_begin, col_len))
+    return acc
+
+
 def _stats_list(buf, k):
     return [IterStats(s.iteration, s.elapsed_ns, s.chunks_processed, s.chunks_skipped,
                       s.subchunks_processed, s.columns_processed, s.frontier_size) for s in buf[:k]]

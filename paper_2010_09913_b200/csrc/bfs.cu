@@ -201,6 +201,11 @@ struct Args32 {
   int32_t k_begin;
   int32_t k_end;
   int* trace;  // debug progress words in mapped host memory (SSB_TRACE), or null
+  // Device-resident carry between launches (asynchronous shard stepping), or
+  // null: {|F| entering k_begin, active tasks, retired chunks}. Read at launch
+  // start instead of n_tasks / front_in / gone_base, written back at the end;
+  // a launch entering with |F| = 0 (the BFS already converged) does nothing.
+  int64_t* carry;
 };
 
 // Fused multi-GPU exchange (chunk-range shards): every rank's
@@ -781,6 +786,12 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
   int32_t n_in = a.n_tasks;                  // active tasks entering iteration k
   int64_t front_in = a.front_in;             // |F_{k-1}|
   unsigned long long gone = a.gone_base;     // chunks of tasks retired before k
+  if (a.carry) {  // grid-uniform: every CTA reads the words the previous kernels wrote
+    front_in = a.carry[0];
+    n_in = int32_t(a.carry[1]);
+    gone = static_cast<unsigned long long>(a.carry[2]);
+    if (front_in == 0) return;
+  }
   // every rank has reset its window before anyone stores into it
   if (kP2P) p2p_barrier(x, x.gen_base + 1);
 
@@ -1164,6 +1175,12 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     gone += *reinterpret_cast<volatile unsigned long long*>(&a.gone_chunks[rec]);
     if (front == 0) break;  // is_converged: no row newly reached
   }
+  // every CTA read the carry at launch start, before the first grid.sync
+  if (a.carry && vb == 0 && threadIdx.x == 0) {
+    a.carry[0] = front_in;
+    a.carry[1] = n_in;
+    a.carry[2] = static_cast<int64_t>(gone);
+  }
 }
 
 template <bool kSelMax, int kS>
@@ -1310,6 +1327,16 @@ __global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_
 // reference, including its root encoding when compat is on.
 // Summary of a full frontier bitmap (after a shard exchange): bit t of the
 // summary <-> frontier words [PW + 8t, PW + 8t + 8) hold a set bit.
+// |F| of a full frontier bitmap (the exchanged words of every rank): the global
+// newly-reached count is_converged (semiring.cpp:152-157) needs, on the device.
+__global__ void front_count_kernel(const uint32_t* __restrict__ F, int64_t nw, int64_t* __restrict__ out) {
+  unsigned long long c = 0;
+  GRID_STRIDE(w, nw) c += __popc(F[w]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(out), c);
+}
+
 __global__ void summary_from_words_kernel(const uint32_t* __restrict__ F, int64_t PW, int64_t NW,
                                           uint32_t* __restrict__ S, int64_t SW, int gshift) {
   GRID_STRIDE(sw, SW) {
@@ -1848,6 +1875,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.slimwork = o.slimwork ? 1 : 0;
   a.root_code = root_code;
   a.trace = nullptr;
+  a.carry = nullptr;
   static int* trace_buf = nullptr;
   if (std::getenv("SSB_TRACE")) {
     if (!trace_buf) SSB_CUDA(cudaHostAlloc(&trace_buf, 64, cudaHostAllocMapped));
@@ -2395,11 +2423,31 @@ void fetch_rows(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent,
 // iteration = shard_step (this rank's sweep, its owned frontier words copied
 // out) -> the caller all-gathers every rank's words -> shard_exchange (the
 // full frontier installed, the summary rebuilt, |F| made global).
+constexpr int kFrontRing = 64;  // iterations whose |F| the host can still query
 struct ShardState {
   Run32 r;
   ssb_bfs_options o;
   std::vector<ssb_iter_stats> stats;
   DevBuf<uint8_t> owned;  // per chunk: owned by this rank (result fetch)
+  // asynchronous stepping (no host round trip per iteration)
+  DevBuf<int64_t> carry;                    // {|F|, active tasks, retired chunks, spare}
+  std::vector<std::unique_ptr<DevBuf<int64_t>>> recs;  // per-iteration records, 1024 per block
+  int64_t* hfront = nullptr;                // pinned ring: global |F_k|
+  cudaEvent_t ev[kFrontRing] = {};
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  bool async = false;
+  ~ShardState() {
+    if (hfront) cudaFreeHost(hfront);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+  }
+  int64_t* rec_slot(int64_t k) {  // device record of iteration k (1-based)
+    const size_t blk = size_t((k - 1) / 1024);
+    while (recs.size() <= blk) recs.emplace_back(new DevBuf<int64_t>(size_t(1024) * kStatW));
+    return recs[blk]->p + ((k - 1) % 1024) * kStatW;
+  }
 };
 
 // device mask of the owned chunks of a segment list
@@ -2475,6 +2523,124 @@ void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_
   g.sc.sync();
   g.last_iterations = int64_t(st->stats.size());
   g.last_valid = true;  // results of the owned rows can be fetched at any point
+}
+
+// ---- asynchronous form: no host synchronisation inside the BFS -------------
+// step_async (sweep k; record k and the owned words copied on the stream) ->
+// the caller's all-gather on the SAME stream (ssb_graph_stream) ->
+// exchange_async (install, summary, global |F_k| counted on the device into
+// the carry the next sweep reads, and copied to a pinned slot). The host only
+// polls |F_{k-1}| (ssb_bfs_shard_front) while iteration k is already queued,
+// and takes the counters once at the end (ssb_bfs_shard_finish).
+void shard_begin_async(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t cb, int64_t ce) {
+  shard_begin(g, root, o, cb, ce);
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  st->async = true;
+  st->carry.alloc(4);
+  if (!st->hfront) SSB_CUDA(cudaHostAlloc(&st->hfront, sizeof(int64_t) * kFrontRing, cudaHostAllocDefault));
+  for (auto& e : st->ev) SSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  SSB_CUDA(cudaEventCreate(&st->t0));
+  SSB_CUDA(cudaEventCreate(&st->t1));
+  const int64_t init[4] = {1, st->r.a.n_tasks, 0, 0};  // F_0 = {root}
+  SSB_CUDA(cudaMemcpyAsync(st->carry.p, init, sizeof init, cudaMemcpyHostToDevice, g.sc.s));
+  st->r.a.carry = st->carry.p;
+  SSB_CUDA(cudaStreamSynchronize(g.sc.s));  // init lives on this stack frame
+  SSB_CUDA(cudaEventRecord(st->t0, g.sc.s));
+}
+
+void shard_step_async(ssb_graph& g, uint32_t* owned_words) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st || !st->async) fail(SSB_EINVAL, "no asynchronous sharded BFS in progress (ssb_bfs_shard_begin_async)");
+  Run32& r = st->r;
+  cudaStream_t s = g.sc.s;
+  Args32& a = r.a;
+  const int64_t k = r.k;
+  a.k_begin = int32_t(k);
+  a.k_end = int32_t(k + 1);
+  if (!r.zeroed) {
+    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, size_t(kStatW) * 8, s));
+    SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
+  }
+  r.zeroed = false;
+  void* params[] = {&a};
+  SSB_CUDA(cudaLaunchCooperativeKernel((const void*)bfs32_fn(r.sel, r.G.S), dim3(r.grid), dim3(kThreads),
+                                       params, r.G.smem, s));
+  SSB_CUDA(cudaGetLastError());
+  g.last_launches += 1;
+  SSB_CUDA(cudaMemcpyAsync(st->rec_slot(k), g.dstats.p, size_t(kStatW) * 8, cudaMemcpyDeviceToDevice, s));
+  const uint32_t* Fn = (k & 1) ? a.F1 : a.F0;
+  const int64_t cb = r.segs[0], ce = r.segs[1];
+  if (owned_words && ce > cb)
+    SSB_CUDA(cudaMemcpyAsync(owned_words, Fn + cb, 4 * (ce - cb), cudaMemcpyDeviceToDevice, s));
+  r.k = k + 1;
+}
+
+void shard_exchange_async(ssb_graph& g, const uint32_t* frontier_words) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st || !st->async) fail(SSB_EINVAL, "no asynchronous sharded BFS in progress (ssb_bfs_shard_begin_async)");
+  if (!frontier_words) fail(SSB_EINVAL, "frontier_words is NULL");
+  Run32& r = st->r;
+  const int64_t k = r.k - 1;  // the iteration just stepped
+  cudaStream_t s = g.sc.s;
+  uint32_t* Fn = (k & 1) ? r.a.F1 : r.a.F0;
+  SSB_CUDA(cudaMemcpyAsync(Fn, frontier_words, 4 * g.n_chunks, cudaMemcpyDeviceToDevice, s));
+  if (r.G.SW > 0) {
+    uint32_t* Sn = (k % 3) == 0 ? r.a.S0 : ((k % 3) == 1 ? r.a.S1 : r.a.S2);
+    summary_from_words_kernel<<<grid_for(r.G.SW), 256, 0, s>>>(Fn, r.G.PW, g.n_chunks, Sn, r.G.SW,
+                                                               r.G.gshift);
+    SSB_CUDA(cudaGetLastError());
+    g.last_launches += 1;
+  }
+  SSB_CUDA(cudaMemsetAsync(st->carry.p, 0, 8, s));
+  front_count_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(Fn, g.n_chunks, st->carry.p);
+  SSB_CUDA(cudaGetLastError());
+  g.last_launches += 1;
+  const int slot = int(k % kFrontRing);
+  SSB_CUDA(cudaMemcpyAsync(st->hfront + slot, st->carry.p, 8, cudaMemcpyDeviceToHost, s));
+  SSB_CUDA(cudaEventRecord(st->ev[slot], s));
+}
+
+int64_t shard_front(ssb_graph& g, int64_t k) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st || !st->async) fail(SSB_EINVAL, "no asynchronous sharded BFS in progress (ssb_bfs_shard_begin_async)");
+  if (k < 1 || k >= st->r.k || k < st->r.k - kFrontRing)
+    fail(SSB_EINVAL, "iteration " + std::to_string(k) + " not exchanged or no longer held");
+  const int slot = int(k % kFrontRing);
+  SSB_CUDA(cudaEventSynchronize(st->ev[slot]));
+  return st->hfront[slot];
+}
+
+// The BFS took `iterations` iterations (the caller saw |F_iterations| = 0 or
+// hit its cap): this rank's per-iteration counters (local to its chunks —
+// sum them over ranks) and the device time since begin.
+void shard_finish(ssb_graph& g, int64_t iterations, ssb_iter_stats* out, int64_t cap, double* device_ms) {
+  auto st = std::static_pointer_cast<ShardState>(g.shard);
+  if (!st || !st->async) fail(SSB_EINVAL, "no asynchronous sharded BFS in progress (ssb_bfs_shard_begin_async)");
+  Run32& r = st->r;
+  if (iterations < 0 || iterations >= r.k) fail(SSB_EINVAL, "more iterations than were stepped");
+  cudaStream_t s = g.sc.s;
+  SSB_CUDA(cudaEventRecord(st->t1, s));
+  SSB_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> rec(size_t(iterations) * kStatW);
+  for (int64_t k = 1; k <= iterations; ++k)
+    SSB_CUDA(cudaMemcpy(rec.data() + (k - 1) * kStatW, st->rec_slot(k), size_t(kStatW) * 8,
+                        cudaMemcpyDeviceToHost));
+  std::vector<ssb_iter_stats> stats;
+  collect_stats(rec, 1, iterations, stats);
+  g.last_swept = 0;
+  for (int64_t i = 0; i < iterations; ++i) {
+    stats[size_t(i)].chunks_processed += g.plan.empty_chunks - (r.z_skip ? 1 : 0);
+    stats[size_t(i)].chunks_skipped += r.z_skip ? 1 : 0;
+    g.last_swept += rec[size_t(i) * kStatW + 6];
+  }
+  for (int64_t i = 0; i < std::min<int64_t>(cap, iterations); ++i) out[i] = stats[size_t(i)];
+  st->stats = stats;
+  float ms = 0;
+  SSB_CUDA(cudaEventElapsedTime(&ms, st->t0, st->t1));
+  if (device_ms) *device_ms = ms;
+  g.last_kernel_ms = ms;
+  g.last_iterations = iterations;
+  g.last_valid = true;
 }
 
 void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent) {

@@ -309,6 +309,26 @@ int ssb_spmv_step(const ssb_graph* g, int variant, const int64_t* x_prev, int64_
   });
 }
 
+int ssb_spmv_step_device(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* out,
+                         int64_t chunk_begin, int64_t chunk_end, double* device_ms) {
+  return guarded([&] {
+    need(g, "graph");
+    need(x_prev, "x_prev");
+    need(out, "out");
+    ssb::spmv_step_device(*g, variant, x_prev, out, chunk_begin, chunk_end, device_ms);
+  });
+}
+
+int ssb_spmv_segment(const ssb_graph* g, int variant, const int64_t* x_prev, int64_t* acc, int64_t chunk,
+                     int64_t col_begin, int64_t col_len) {
+  return guarded([&] {
+    need(g, "graph");
+    need(x_prev, "x_prev");
+    need(acc, "acc");
+    ssb::spmv_segment(*g, variant, x_prev, acc, chunk, col_begin, col_len);
+  });
+}
+
 int ssb_bfs_run(ssb_graph* g, int64_t root, const ssb_bfs_options* opts, ssb_iter_stats* stats,
                 int64_t stats_cap, int64_t* iterations, double* device_ms) {
   int rc = SSB_OK;
@@ -447,6 +467,54 @@ int ssb_bfs_shard_exchange(ssb_graph* g, const uint32_t* frontier_words, int64_t
   return guarded([&] {
     need(g, "graph");
     ssb::shard_exchange(*g, frontier_words, newly_total);
+  });
+}
+
+int ssb_graph_stream(ssb_graph* g, void** stream) {
+  return guarded([&] {
+    need(g, "graph");
+    need(stream, "stream");
+    *stream = static_cast<void*>(g->sc.s);
+  });
+}
+
+int ssb_bfs_shard_begin_async(ssb_graph* g, int64_t root, const ssb_bfs_options* opts,
+                              int64_t chunk_begin, int64_t chunk_end) {
+  return guarded([&] {
+    need(g, "graph");
+    need(opts, "opts");
+    ssb::shard_begin_async(*g, root, *opts, chunk_begin, chunk_end);
+  });
+}
+
+int ssb_bfs_shard_step_async(ssb_graph* g, uint32_t* owned_words) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::shard_step_async(*g, owned_words);
+  });
+}
+
+int ssb_bfs_shard_exchange_async(ssb_graph* g, const uint32_t* frontier_words) {
+  return guarded([&] {
+    need(g, "graph");
+    ssb::shard_exchange_async(*g, frontier_words);
+  });
+}
+
+int ssb_bfs_shard_front(ssb_graph* g, int64_t k, int64_t* front) {
+  return guarded([&] {
+    need(g, "graph");
+    need(front, "front");
+    *front = ssb::shard_front(*g, k);
+  });
+}
+
+int ssb_bfs_shard_finish(ssb_graph* g, int64_t iterations, ssb_iter_stats* stats, int64_t stats_cap,
+                         double* device_ms) {
+  return guarded([&] {
+    need(g, "graph");
+    if (stats_cap > 0) need(stats, "stats");
+    ssb::shard_finish(*g, iterations, stats, stats_cap, device_ms);
   });
 }
 

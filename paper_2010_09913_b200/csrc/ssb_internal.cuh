@@ -196,6 +196,7 @@ struct ssb_graph {
   ssb::DevBuf<uint32_t> p2p_win;  // fused multi-GPU BFS: the peer-mapped frontier window
   std::shared_ptr<void> p2p;      // ... and its peer table (bfs.cu)
   std::shared_ptr<void> geom;   // cached shared-memory image geometry (bfs.cu)
+  std::shared_ptr<void> spmv_plan;  // work units of the last spmv_step chunk range (spmv.cu)
 
   ssb::StreamCtx sc;
 };
@@ -218,6 +219,10 @@ void edges_to_csr(const ssb_edges& e, int64_t* row, int64_t* col);
 // spmv.cu
 void spmv_step(const ssb_graph& g, int variant, const int64_t* x_prev, int64_t* out,
                int64_t chunk_begin, int64_t chunk_end);
+void spmv_step_device(const ssb_graph& g, int variant, const int64_t* x_prev, int64_t* out,
+                      int64_t chunk_begin, int64_t chunk_end, double* device_ms);
+void spmv_segment(const ssb_graph& g, int variant, const int64_t* x_prev, int64_t* acc, int64_t chunk,
+                  int64_t col_begin, int64_t col_len);
 // bfs.cu
 int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats* stats,
             int64_t stats_cap, int64_t* iterations, double* device_ms);
@@ -230,6 +235,11 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
 void shard_step(ssb_graph& g, ssb_iter_stats* local, uint32_t* owned_words);
 void shard_exchange(ssb_graph& g, const uint32_t* frontier_words, int64_t newly_total);
 void shard_fetch(ssb_graph& g, int want_parents, int64_t* dist, int64_t* parent);
+void shard_begin_async(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t cb, int64_t ce);
+void shard_step_async(ssb_graph& g, uint32_t* owned_words);
+void shard_exchange_async(ssb_graph& g, const uint32_t* frontier_words);
+int64_t shard_front(ssb_graph& g, int64_t k);
+void shard_finish(ssb_graph& g, int64_t iterations, ssb_iter_stats* out, int64_t cap, double* device_ms);
 void p2p_window(ssb_graph& g, void* ipc_handle, int64_t* bytes);
 void p2p_attach(ssb_graph& g, int rank, int world, const void* handles, const int64_t* bounds,
                 int64_t nseg);

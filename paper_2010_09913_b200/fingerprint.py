@@ -75,3 +75,22 @@ def ph64_torch(t) -> str:
     x = (x ^ ((x >> 27) & ((1 << 37) - 1))) * _as_signed(K2)
     x = x ^ ((x >> 31) & ((1 << 33) - 1))
     return format(int(x.sum().item()) & M64, "016x")
+
+
+def ph64_partial_torch(t, mask) -> int:
+    """The ph64 terms of the positions where `mask` holds, summed mod 2^64 as a
+    signed int64 (ph64 is a sum over positions, so ranks that own disjoint
+    rows add their partials — one all-reduce instead of gathering the vector)."""
+    import torch
+
+    t = t.reshape(-1).to(torch.int64)
+    i = torch.arange(1, t.numel() + 1, dtype=torch.int64, device=t.device)
+    x = t + i * _as_signed(GAMMA)
+    x = (x ^ ((x >> 30) & ((1 << 34) - 1))) * _as_signed(K1)
+    x = (x ^ ((x >> 27) & ((1 << 37) - 1))) * _as_signed(K2)
+    x = x ^ ((x >> 31) & ((1 << 33) - 1))
+    return _as_signed(int(x[mask.reshape(-1)].sum().item()) & M64)
+
+
+def ph64_format(total: int) -> str:
+    return format(int(total) & M64, "016x")

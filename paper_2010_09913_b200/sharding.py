@@ -178,6 +178,66 @@ class DeviceShard:
         from .api import _check, _p
         _check(L.lib().ssb_bfs_shard_fetch(self.r._h, int(want_parents), _p(dist), _p(parent)))
 
+    # -- asynchronous stepping: no host round trip inside the BFS ------------
+    def stream(self):
+        """The library stream of this shard's handle as a torch stream: the
+        all-gather is enqueued on it between the step and the exchange."""
+        import ctypes as C
+
+        import torch
+
+        from . import _lib as L
+        from .api import _check
+        if getattr(self, "_stream", None) is None:
+            p = C.c_void_p()
+            _check(L.lib().ssb_graph_stream(self.r._h, C.byref(p)))
+            self._stream = torch.cuda.ExternalStream(p.value)
+        return self._stream
+
+    def begin_async(self, root: int, opts) -> None:
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        o = opts._c()
+        _check(L.lib().ssb_bfs_shard_begin_async(self.r._h, int(root), C.byref(o), self.cb, self.ce))
+
+    def step_async(self):
+        """Queue one iteration's sweep; returns the owned-words view (filled on
+        the shard's stream)."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        _check(L.lib().ssb_bfs_shard_step_async(self.r._h, C.c_void_p(self.owned.data_ptr())))
+        return self.owned[: self.ce - self.cb]
+
+    def exchange_async(self, full_words) -> None:
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        _check(L.lib().ssb_bfs_shard_exchange_async(self.r._h, C.c_void_p(full_words.data_ptr())))
+
+    def front(self, k: int) -> int:
+        """Global |F_k| (waits for iteration k's exchange only)."""
+        from . import _lib as L
+        from .api import _check, _p
+        out = np.zeros(1, np.int64)
+        _check(L.lib().ssb_bfs_shard_front(self.r._h, int(k), _p(out)))
+        return int(out[0])
+
+    def finish(self, iterations: int):
+        """(this rank's per-iteration counters, device ms of the BFS)."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check, _stats_list
+        st = (L.IterStatsC * max(iterations, 1))()
+        ms = C.c_double()
+        _check(L.lib().ssb_bfs_shard_finish(self.r._h, int(iterations), st, int(iterations), C.byref(ms)))
+        return _stats_list(st, iterations), float(ms.value)
+
 
 class P2PShard:
     """One rank's shard of the FUSED multi-GPU BFS: the frontier exchange runs
@@ -313,6 +373,9 @@ class TorchComm:
         self.slot = max(1, max(e - b for b, e in ranges))
         # gloo (functional runs with ranks sharing a GPU) exchanges host tensors
         self.host = dist.get_backend(group) == "gloo"
+        # NCCL: the all-gather runs on the caller's current (the shard's) stream,
+        # so the BFS steps without host synchronisation (run_sharded_bfs_async)
+        self.device_async = not self.host
 
     def allgather_frontier(self, owned_list):
         import torch
@@ -342,18 +405,54 @@ class TorchComm:
         return t.cpu().numpy()
 
 
+def _cap_of(opts, n: int, max_iterations: int) -> int:
+    """bfs.cpp:70-71: opts.max_iterations > 0 ? it : n + 1 (an explicit
+    max_iterations argument overrides)."""
+    if max_iterations > 0:
+        return max_iterations
+    return int(opts.max_iterations) if int(opts.max_iterations) > 0 else n + 1
+
+
+def _gather_results(shards, opts, n, per_iter, fetch, converged):
+    from .api import KINF, BfsCapError, BfsResult
+    if not converged:  # bfs.cpp:86-90: the partial distances, no parents
+        dist = np.full(n, KINF, dtype=np.int64)
+        for sh in shards:
+            sh.fetch(False, dist, dist.copy())
+        raise BfsCapError(f"BFS did not converge within {len(per_iter)} iterations",
+                          BfsResult(dist, dist[:0], len(per_iter), per_iter))
+    if not fetch:  # the BFS only (results stay on the devices)
+        return None, None, per_iter
+    dist = np.full(n, KINF, dtype=np.int64)
+    parent = np.full(n, -1, dtype=np.int64)
+    want = bool(opts.want_parents) and int(opts.variant) == 3
+    for sh in shards:
+        sh.fetch(want, dist, parent)
+    return dist, (parent if want else parent[:0]), per_iter
+
+
 def run_sharded_bfs(shards, comm, root: int, opts, max_iterations: int = 0, fetch: bool = True):
     """A BFS over chunk-range shards: per iteration every shard sweeps its
     chunks, the owned frontier words are all-gathered, |newly| is summed, and
     the full frontier is installed on every shard. Returns (dist, parent,
     per_iter) — dist/parent of the rows this process owns (other rows hold the
-    sentinels KINF / -1) and the global per-iteration counters."""
-    from .api import IterStats, KINF
+    sentinels KINF / -1) and the global per-iteration counters. The cap is
+    opts.max_iterations (bfs.cpp:70-71); hitting it raises BfsCapError with
+    the partial distances and no parents, as bfs_spmv does.
+
+    One shard per process over a device communicator (NCCL): the asynchronous
+    form — no host synchronisation inside the BFS (run_sharded_bfs_async).
+    Several shards in one process (LocalComm) or a host communicator (gloo)
+    step synchronously."""
+    if len(shards) == 1 and getattr(comm, "device_async", False):
+        return run_sharded_bfs_async(shards[0], comm, root, opts, max_iterations, fetch)
+    from .api import IterStats
     for sh in shards:
         sh.begin(root, opts)
     n = shards[0].r.n
-    cap = max_iterations if max_iterations > 0 else n + 1
+    cap = _cap_of(opts, n, max_iterations)
     per_iter = []
+    converged = False
     for k in range(1, cap + 1):
         locals_, owned = zip(*[sh.step() for sh in shards])
         counts = comm.allreduce_sum([np.array([s.chunks_processed, s.chunks_skipped,
@@ -365,12 +464,40 @@ def run_sharded_bfs(shards, comm, root: int, opts, max_iterations: int = 0, fetc
             sh.exchange(full, int(counts[4]))
         per_iter.append(IterStats(k, int(counts[5]), *[int(x) for x in counts[:5]]))
         if counts[4] == 0:
+            converged = True
             break
-    if not fetch:  # the BFS only (results stay on the devices)
-        return None, None, per_iter
-    dist = np.full(n, KINF, dtype=np.int64)
-    parent = np.full(n, -1, dtype=np.int64)
-    want = bool(opts.want_parents) and int(opts.variant) == 3
-    for sh in shards:
-        sh.fetch(want, dist, parent)
-    return dist, (parent if want else parent[:0]), per_iter
+    return _gather_results(shards, opts, n, per_iter, fetch, converged)
+
+
+def run_sharded_bfs_async(shard, comm, root: int, opts, max_iterations: int = 0, fetch: bool = True):
+    """The NCCL form without host round trips: sweep (library stream) ->
+    all-gather (NCCL, enqueued on the same stream) -> exchange (install +
+    device-side |F| count) per iteration; the host only polls |F_{k-1}| while
+    iteration k is already queued. The counters stay on the device and are
+    all-reduced ONCE at the end of the BFS."""
+    import torch
+
+    from .api import IterStats
+    n = shard.r.n
+    cap = _cap_of(opts, n, max_iterations)
+    shard.begin_async(root, opts)
+    stream = shard.stream()
+    iterations, converged = 0, False
+    with torch.cuda.stream(stream):
+        for k in range(1, cap + 1):
+            owned = shard.step_async()
+            full = comm.allgather_frontier([owned])
+            shard.exchange_async(full)
+            if k >= 2 and shard.front(k - 1) == 0:  # iteration k was queued after convergence: a no-op
+                iterations, converged = k - 1, True
+                break
+        else:
+            iterations = cap
+            converged = shard.front(cap) == 0
+    local, ms = shard.finish(iterations)
+    cols = np.array([[s.chunks_processed, s.chunks_skipped, s.subchunks_processed, s.columns_processed,
+                      s.frontier_size, s.elapsed_ns] for s in local], dtype=np.int64).reshape(-1, 6)
+    tot = comm.allreduce_sum([cols.reshape(-1)]).reshape(-1, 6)  # once per BFS
+    per_iter = [IterStats(k + 1, int(r[5]), *[int(x) for x in r[:5]]) for k, r in enumerate(tot)]
+    shard.last_ms = ms
+    return _gather_results([shard], opts, n, per_iter, fetch, converged)

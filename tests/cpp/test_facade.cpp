@@ -209,7 +209,114 @@ void ingest_and_checks() {
   CHECK(validate_bfs(g, 1, bad).has_value());
 }
 
+// A layout the reference built on the host (here: the oracle's restatement,
+// shaped like repr.hpp:33-55) goes through upload(): bfs_spmv / spmv_step /
+// spmv_segment on it equal the oracle; rewriting its first real cell (what
+// cli.cpp:200-207's corrupt_repr does) is seen by the fingerprint cache.
+struct HostRepr {  // the reference's SlimSellRepr members (repr.hpp:33-55)
+  std::int64_t C = 1, sigma = 1;
+  vid_t n = 0, n_padded = 0;
+  std::int64_t n_chunks = 0;
+  vid_t nonzeros = 0;
+  std::vector<vid_t> col, cs, cl, perm, inv_perm;
+  std::int64_t padding = 0;
+};
+
+TEST_CASE(host_layout_upload_and_segment) {
+  const std::int64_t scale = 11;
+  std::vector<std::int64_t> uv(2 * (std::int64_t{16} << scale));
+  const double init[4] = {0.57, 0.19, 0.19, 0.05};
+  so_gen_kronecker_pairs(scale, 16, 5, init, uv.data());
+  std::int64_t n = 0;
+  const std::int64_t m = so_normalize_pairs(uv.data(), 16 << scale, 1 << scale, &n);
+  std::vector<std::int64_t> row(n + 1), col(2 * m);
+  so_to_csr(n, uv.data(), m, row.data(), col.data());
+  for (std::int64_t C : {8, 32}) {
+    so_repr L;
+    so_build_slimsell(n, row.data(), col.data(), C, n, &L);
+    HostRepr h;
+    h.C = L.C;
+    h.sigma = L.sigma;
+    h.n = L.n;
+    h.n_padded = L.n_padded;
+    h.n_chunks = L.n_chunks;
+    h.nonzeros = L.nonzeros;
+    h.padding = L.padding;
+    h.col.assign(L.col, L.col + L.n_cells);
+    h.cs.assign(L.cs, L.cs + L.n_chunks);
+    h.cl.assign(L.cl, L.cl + L.n_chunks);
+    h.perm.assign(L.perm, L.perm + n);
+    h.inv_perm.assign(L.inv_perm, L.inv_perm + n);
+    auto oracle_bfs = [&](const so_repr* R, std::int64_t root, std::vector<std::int64_t>& d,
+                          std::vector<std::int64_t>& p) {
+      std::vector<std::int64_t> st(7 * (n + 2));
+      std::int64_t plen = 0, it = 0;
+      d.assign(n, 0);
+      p.assign(n, 0);
+      so_bfs_spmv(R, root, 3, 1, 16, 0, 1, nullptr, nullptr, d.data(), p.data(), &plen, &it, st.data(), n + 2);
+      p.resize(plen);
+    };
+    BfsOptions o;
+    o.variant = Variant::selmax;
+    o.slimwork = true;
+    o.slimchunk_len = 16;
+    std::vector<std::int64_t> d, p;
+    oracle_bfs(&L, 3, d, p);
+    BfsResult a = bfs_spmv(h, 3, o);  // uploads
+    CHECK(a.dist == d && a.parent == p);
+    BfsResult b = bfs_spmv(h, 3, o);  // cached
+    CHECK(b.dist == d && b.parent == p);
+    // spmv_step / spmv_segment on the host layout vs the oracle
+    std::vector<val_t> x(h.n_padded);
+    for (std::size_t i = 0; i < x.size(); ++i) x[i] = static_cast<val_t>((i * 2654435761u) % 1000);
+    for (Variant v : kAllVariants) {
+      std::vector<val_t> out(h.n_padded, 7), want(h.n_padded, 7);
+      spmv_step(h, semiring(v), x, out, 0, h.n_chunks);
+      so_spmv_step(&L, static_cast<int>(v), x.data(), want.data(), 0, h.n_chunks);
+      CHECK(out == want);
+      std::int64_t ch = 0;
+      for (std::int64_t i = 0; i < h.n_chunks; ++i)
+        if (h.cl[i] > h.cl[ch]) ch = i;
+      std::vector<val_t> acc(C, 3), exp(C, 3);
+      const std::int64_t cb = h.cl[ch] / 3, len = h.cl[ch] - cb;
+      spmv_segment(h, semiring(v), x, acc, ch, cb, len);
+      const SemiringSpec& s = semiring(v);
+      for (std::int64_t j = cb; j < cb + len; ++j)
+        for (std::int64_t l = 0; l < C; ++l) {
+          const std::int64_t c = h.col[h.cs[ch] + j * C + l];
+          exp[l] = s.plus(exp[l], s.times(x[c < 0 ? 0 : c], c < 0 ? s.pad_value : s.edge_value));
+        }
+      CHECK(acc == exp);
+      CHECK_THROWS_AS(spmv_segment(h, semiring(v), x, acc, ch, 0, h.cl[ch] + 1), std::invalid_argument);
+    }
+    // corrupt_repr (cli.cpp:200-207): the first real cell is rewritten in place
+    for (std::int64_t i = 0; i < L.n_cells; ++i)
+      if (L.col[i] >= 0) {
+        L.col[i] = (L.col[i] + 1) % n;
+        h.col[i] = L.col[i];
+        break;
+      }
+    oracle_bfs(&L, 3, d, p);
+    BfsResult c = bfs_spmv(h, 3, o);
+    CHECK(c.dist == d && c.parent == p);
+    so_repr_free(&L);
+  }
+  // bfs.hpp:85 — the CsrView overload equals the Graph overload
+  Graph g = Graph::from_pairs([&] {
+    std::vector<std::pair<vid_t, vid_t>> pr;
+    for (std::int64_t i = 0; i < m; ++i) pr.emplace_back(uv[2 * i], uv[2 * i + 1]);
+    return pr;
+  }(), n);
+  CsrView csr;
+  csr.row = row;
+  csr.col = col;
+  BfsResult t1 = bfs_traditional(csr, 3), t2 = bfs_traditional(g, 3);
+  CHECK(t1.dist == t2.dist && t1.parent == t2.parent && t1.iterations == t2.iterations);
+  CHECK_THROWS_AS(bfs_traditional(csr, n), std::out_of_range);
+}
+
 int main() {
+  host_layout_upload_and_segment();
   ingest_and_checks();
   csr_layout_of_path4();
   from_pairs_normalises();

@@ -122,6 +122,54 @@ def test_spmv_step_random_vs_oracle(ssb, port):
         ssb.spmv_step(r, ssb.Variant.real, np.zeros(3, np.int64))
 
 
+def test_spmv_split_hub_chunks_device_operands_and_segment(ssb, port):
+    """Hub chunks longer than one work unit (1024 columns) are split and folded
+    by atomics: the host form, the device-operand form (ssb_spmv_step_device)
+    and the oracle agree for every semiring, C in {8, 32}; spmv_segment
+    (repr.cpp:20-35) equals the reference loop restated on the oracle's layout,
+    including column ranges crossing unit boundaries."""
+    import torch
+    n, uv = port.gen_kronecker(14, 32, 1)  # max degree > 1024
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    rng = np.random.default_rng(3)
+    ops = {0: (lambda a, b: min(a, b), lambda a, b: KINF if KINF in (a, b) else a + b, KINF, 1, KINF),
+           1: (lambda a, b: (a + b + (1 << 63)) % (1 << 64) - (1 << 63),
+               lambda a, b: (a * b + (1 << 63)) % (1 << 64) - (1 << 63), 0, 1, 0),
+           2: (lambda a, b: a | b, lambda a, b: a & b, 0, 1, 0),
+           3: (lambda a, b: max(a, b), lambda a, b: (a * b + (1 << 63)) % (1 << 64) - (1 << 63), 0, 1, 0)}
+    for C_ in (8, 32):
+        r = ssb.build_slimsell(g, C_, n)
+        L = port.build_slimsell(n, row, col, C_, n)
+        assert int(L.cl.max()) > 1024
+        for v in range(4):
+            x = rng.integers(-(1 << 40), 1 << 40, r.n_padded)
+            if v == 0:
+                x[rng.random(r.n_padded) < 0.5] = KINF
+            want = port.spmv_step(L, v, x)
+            assert np.array_equal(ssb.spmv_step(r, ssb.Variant(v), x), want), (C_, v)
+            dx = torch.from_numpy(x).cuda()
+            dout = torch.zeros(r.n_padded, dtype=torch.int64, device="cuda")
+            ms = ssb.spmv_step_device(r, ssb.Variant(v), dx, dout)
+            assert ms >= 0 and np.array_equal(dout.cpu().numpy(), want), (C_, v)
+            # spmv_segment on the hub chunk, a range crossing unit boundaries
+            plus, times, zero, edge, pad = ops[v]
+            ch = int(np.argmax(L.cl))
+            for cb, ln in ((0, int(L.cl[ch])), (1000, 1100), (5, 0), (int(L.cl[ch]) - 3, 3)):
+                acc0 = rng.integers(0, 50, C_)
+                got = ssb.spmv_segment(r, ssb.Variant(v), x, acc0.copy(), ch, cb, ln)
+                exp = [int(a) for a in acc0]
+                for j in range(cb, cb + ln):
+                    for lane in range(C_):
+                        c = int(L.col[L.cs[ch] + j * C_ + lane])
+                        exp[lane] = plus(exp[lane], times(int(x[max(c, 0)]), pad if c < 0 else edge))
+                assert got.tolist() == exp, (C_, v, cb, ln)
+        with pytest.raises(ssb.InvalidArgument):
+            ssb.spmv_segment(r, ssb.Variant.real, x, np.zeros(C_, np.int64), 0, 0, int(L.cl[0]) + 1)
+        with pytest.raises(ssb.InvalidArgument):
+            ssb.spmv_segment(r, ssb.Variant.real, x, np.zeros(C_, np.int64), r.n_chunks, 0, 1)
+
+
 # ---- BFS ------------------------------------------------------------------------
 
 def test_selftest_grid_vs_oracle(ssb, port):
@@ -365,6 +413,99 @@ def test_chunk_sharded_device_bfs_matches_single_gpu(ssb, port, monkeypatch, wor
             if v == 3:
                 assert np.array_equal(parent, b.parent), (root, v, world)
             assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_chunk_sharded_async_steps_match_oracle(ssb, port, monkeypatch, world):
+    """The NCCL form without host round trips (ssb_bfs_shard_*_async: the
+    sweep reads |F|, the task list and the retired-chunk count from a device
+    carry; the exchange counts |F| on the device; the host polls |F_{k-1}|
+    while k is queued; counters summed once at the end). `world` shards, each
+    on its own library stream, the all-gather done on a third stream with
+    events between them — the ordering NCCL gives on one stream per rank —
+    equal the oracle in dist, sel-max parents and every counter, including
+    the iteration queued after convergence (a no-op) and the cap."""
+    import torch
+
+    from paper_2010_09913_b200.sharding import DeviceShard, LocalComm, partition_chunks, run_sharded_bfs_async
+    monkeypatch.setenv("SSB_SMEM_KB", "4")
+    n, uv = port.gen_kronecker(15, 16, 2)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    reprs = [ssb.build_slimsell(g, 32, n) for _ in range(world)]
+    ranges = partition_chunks(reprs[0].cl, 32, world)
+    shards = [DeviceShard(r, b, e) for r, (b, e) in zip(reprs, ranges)]
+    side = torch.cuda.Stream()
+
+    def run(root, o):
+        for sh in shards:
+            sh.begin_async(root, o)
+        k, iters = 0, None
+        while iters is None:
+            k += 1
+            owned, evs = [], []
+            for sh in shards:
+                with torch.cuda.stream(sh.stream()):
+                    owned.append(sh.step_async())
+                    evs.append(torch.cuda.Event())
+                    evs[-1].record()
+            with torch.cuda.stream(side):
+                for e in evs:
+                    side.wait_event(e)
+                full = LocalComm().allgather_frontier(owned)
+                done = torch.cuda.Event()
+                done.record()
+            for sh in shards:
+                with torch.cuda.stream(sh.stream()):
+                    sh.stream().wait_event(done)
+                    sh.exchange_async(full)
+            if k >= 2 and shards[0].front(k - 1) == 0:
+                iters = k - 1
+            assert all(sh.front(k) == shards[0].front(k) for sh in shards)
+        parts = [sh.finish(iters)[0] for sh in shards]
+        per = []
+        for i in range(iters):
+            f = lambda key: sum(getattr(p[i], key) for p in parts)  # noqa: E731
+            per.append(ssb.IterStats(i + 1, 0, f("chunks_processed"), f("chunks_skipped"),
+                                     f("subchunks_processed"), f("columns_processed"), f("frontier_size")))
+        dist = np.full(n, KINF, np.int64)
+        parent = np.full(n, -1, np.int64)
+        for sh in shards:
+            sh.fetch(o.variant == 3, dist, parent)
+        return dist, parent, per
+
+    for root in (0, 5, 2000):
+        for v, sw, Lc in ((3, True, 64), (0, True, 0), (3, False, 0), (2, True, 2048)):
+            o = opts(ssb, v, sw, Lc)
+            dist, parent, per_iter = run(root, o)
+            b = port.bfs_spmv(L, root, v, sw, Lc)
+            assert np.array_equal(dist, b.dist), (root, v, world)
+            if v == 3:
+                assert np.array_equal(parent, b.parent), (root, v, world)
+            assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
+    if world == 1:  # the library driver itself (one rank, a device-side comm)
+        class OneRank:
+            device_async = True
+
+            def allgather_frontier(self, owned_list):
+                return owned_list[0]
+
+            def allreduce_sum(self, arrays):
+                return arrays[0]
+
+        o = opts(ssb, 3, True, 64)
+        for root in (0, 5, 2000):
+            dist, parent, per_iter = run_sharded_bfs_async(shards[0], OneRank(), root, o)
+            b = port.bfs_spmv(L, root, 3, True, 64)
+            assert np.array_equal(dist, b.dist) and np.array_equal(parent, b.parent)
+            assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats)
+        o.max_iterations = 2
+        with pytest.raises(ssb.BfsCapError) as ei:
+            run_sharded_bfs_async(shards[0], OneRank(), 5, o)
+        assert ei.value.partial.iterations == 2 and len(ei.value.partial.parent) == 0
+        b = port.bfs_spmv(L, 5, 3, True, 64, max_iterations=2)
+        assert np.array_equal(ei.value.partial.dist, b.dist)
 
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])

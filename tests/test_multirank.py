@@ -174,3 +174,65 @@ def test_chunk_sharded_bfs_world2_matches_reference():
         assert p.exitcode == 0
     for key, (d_ok, p_ok, st_ok, it_ok) in out.items():
         assert d_ok and p_ok and st_ok and it_ok, key
+
+
+def test_bench_spawner_runs_n_ranks(tmp_path, capfd):
+    """`bench.py --gpus N` outside torchrun re-launches the command as N ranks
+    under torch.distributed.run (127.0.0.1); here with a gloo stand-in script
+    that all-reduces and lets rank 0 print one line."""
+    import json
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    script = tmp_path / "rank.py"
+    script.write_text(
+        "import json, os, sys, torch, torch.distributed as dist\n"
+        "dist.init_process_group('gloo')\n"
+        "t = torch.tensor([int(os.environ['RANK']) + 1])\n"
+        "dist.all_reduce(t)\n"
+        "if dist.get_rank() == 0:\n"
+        "    print(json.dumps({'world': dist.get_world_size(), 'sum': int(t.item()), 'argv': sys.argv[1:]}))\n"
+        "dist.destroy_process_group()\n")
+    rc = bench.spawn_ranks(2, script=str(script), argv=["--gpus", "2", "--steps", "1"])
+    assert rc == 0
+    out = [ln for ln in capfd.readouterr().out.splitlines() if ln.startswith("{")]
+    assert len(out) == 1
+    d = json.loads(out[0])
+    assert d == {"world": 2, "sum": 3, "argv": ["--gpus", "2", "--steps", "1"]}
+
+
+def test_bench_default_decomposition():
+    """N = 1: the single-GPU engine; N > 1: fused peer exchange when every GPU
+    pair maps each other's memory and the backend is NCCL, else the NCCL
+    all-gather form."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    class FakeCuda:
+        def __init__(self, n, peer):
+            self.n, self.peer = n, peer
+
+        def device_count(self):
+            return self.n
+
+        def can_device_access_peer(self, i, j):
+            return self.peer
+
+    class FakeTorch:
+        def __init__(self, n, peer):
+            self.cuda = FakeCuda(n, peer)
+
+    assert bench.choose_shard(FakeTorch(1, True), 1)[0] == "roots"
+    assert bench.choose_shard(FakeTorch(8, True), 8)[0] == "p2p"
+    assert bench.choose_shard(FakeTorch(8, False), 8)[0] == "chunks"
+    assert bench.choose_shard(FakeTorch(1, True), 2)[0] == "chunks"  # ranks sharing one GPU
+    old = os.environ.get("SSB_BENCH_BACKEND")
+    os.environ["SSB_BENCH_BACKEND"] = "gloo"
+    try:
+        assert bench.choose_shard(FakeTorch(8, True), 8)[0] == "chunks"
+    finally:
+        if old is None:
+            del os.environ["SSB_BENCH_BACKEND"]
+        else:
+            os.environ["SSB_BENCH_BACKEND"] = old
