@@ -1329,9 +1329,12 @@ __global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_
 // summary <-> frontier words [PW + 8t, PW + 8t + 8) hold a set bit.
 // |F| of a full frontier bitmap (the exchanged words of every rank): the global
 // newly-reached count is_converged (semiring.cpp:152-157) needs, on the device.
-__global__ void front_count_kernel(const uint32_t* __restrict__ F, int64_t nw, int64_t* __restrict__ out) {
+// Only chunks with cells count: a newly reached row has a neighbour, and the
+// words of cell-less chunks (isolated rows, never swept) are not maintained.
+__global__ void front_count_kernel(const uint32_t* __restrict__ F, const int32_t* __restrict__ cl, int64_t nw,
+                                   int64_t* __restrict__ out) {
   unsigned long long c = 0;
-  GRID_STRIDE(w, nw) c += __popc(F[w]);
+  GRID_STRIDE(w, nw) c += cl[w] > 0 ? __popc(F[w]) : 0;
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(out), c);
@@ -2592,7 +2595,7 @@ void shard_exchange_async(ssb_graph& g, const uint32_t* frontier_words) {
     g.last_launches += 1;
   }
   SSB_CUDA(cudaMemsetAsync(st->carry.p, 0, 8, s));
-  front_count_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(Fn, g.n_chunks, st->carry.p);
+  front_count_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(Fn, g.cl.p, g.n_chunks, st->carry.p);
   SSB_CUDA(cudaGetLastError());
   g.last_launches += 1;
   const int slot = int(k % kFrontRing);

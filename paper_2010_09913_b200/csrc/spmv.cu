@@ -31,7 +31,7 @@ template <int V>
 struct Ops;
 template <>
 struct Ops<SSB_TROPICAL> {
-  static constexpr int64_t zero = kInf, edge = 1, pad = kInf;
+  static constexpr int64_t zero = kInf, edge = 1, pad = kInf, ident = kInf;
   __device__ static int64_t plus(int64_t a, int64_t b) { return a < b ? a : b; }
   __device__ static int64_t times(int64_t a, int64_t b) {
     return (a == kInf || b == kInf) ? kInf : a + b;
@@ -42,7 +42,7 @@ struct Ops<SSB_TROPICAL> {
 };
 template <>
 struct Ops<SSB_REAL> {
-  static constexpr int64_t zero = 0, edge = 1, pad = 0;
+  static constexpr int64_t zero = 0, edge = 1, pad = 0, ident = 0;
   // two's-complement wrap, as the reference's int64 add/mul on x86-64
   __device__ static int64_t plus(int64_t a, int64_t b) {
     return int64_t(uint64_t(a) + uint64_t(b));
@@ -56,7 +56,7 @@ struct Ops<SSB_REAL> {
 };
 template <>
 struct Ops<SSB_BOOLEAN> {
-  static constexpr int64_t zero = 0, edge = 1, pad = 0;
+  static constexpr int64_t zero = 0, edge = 1, pad = 0, ident = 0;
   __device__ static int64_t plus(int64_t a, int64_t b) { return a | b; }
   __device__ static int64_t times(int64_t a, int64_t b) { return a & b; }
   __device__ static void fold(int64_t* p, int64_t v) {
@@ -65,7 +65,9 @@ struct Ops<SSB_BOOLEAN> {
 };
 template <>
 struct Ops<SSB_SELMAX> {
-  static constexpr int64_t zero = 0, edge = 1, pad = 0;
+  // zero = 0 is the semiring's (non-negative) zero; a unit's partial starts
+  // at the true identity of max so arbitrary int64 inputs fold exactly
+  static constexpr int64_t zero = 0, edge = 1, pad = 0, ident = INT64_MIN;
   __device__ static int64_t plus(int64_t a, int64_t b) { return a > b ? a : b; }
   __device__ static int64_t times(int64_t a, int64_t b) {
     return int64_t(uint64_t(a) * uint64_t(b));
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(256) spmv_units_kernel(const int32_t* __restri
       const int64_t l = l0 + lane;
       if (l >= C) break;
       const int32_t* cells = base + l;
-      int64_t acc = O::zero;
+      int64_t acc = O::ident;
       int32_t j = 0;
       for (; j + 4 <= u.col_len; j += 4) {  // four columns' loads in flight
         int32_t c[4];
