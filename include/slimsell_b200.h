@@ -45,6 +45,8 @@ extern "C" {
 
 typedef struct ssb_edges ssb_edges; /* normalised Graph on the device (graph.hpp:31-51) */
 typedef struct ssb_graph ssb_graph; /* SlimSellRepr on the device (repr.hpp:33-55) */
+typedef struct ssb_ctx ssb_ctx;     /* the devices of a single-process multi-GPU job */
+typedef struct ssb_sharded ssb_sharded; /* a SlimSellRepr sharded over a context's devices */
 
 /* SlimSellRepr scalar fields (repr.hpp:33-45). n_cells = |col| = Σ C·cl of
  * the whole layout. A handle built for chunk segments
@@ -326,6 +328,33 @@ int ssb_validate_bfs(ssb_edges* e, int64_t root, const int64_t* dist, const int6
 int ssb_validate_bfs_exact(ssb_edges* e, const ssb_graph* layout, int64_t root, const int64_t* dist,
                            const int64_t* parent, int flags, int64_t* violations, char* report,
                            int64_t report_cap);
+/* ---- single-process multi-device (SURVEY.md §8(b) ssb_ctx_create) --------
+ * A context names the ranks' devices. All distinct: peer access is enabled
+ * between every pair (ECUDA if a pair has no peer path) and each BFS runs one
+ * cooperative launch per device, the frontier exchange fused over NVLink peer
+ * stores (the ssb_bfs_p2p path with raw peer pointers instead of IPC). All the
+ * same device: the ranks run as ONE cooperative launch there (the emulated
+ * group of ssb_bfs_p2p_group). Mixed lists are EINVAL.
+ * ssb_ctx_build: the layout (C = 32) sharded into segments_per_rank
+ * round-robin, cell-balanced chunk segments per rank; rank i
+ * holds only its segments' cells, on its device. e may live on any device of
+ * the context and must be the CURRENT device's handle.
+ * ssb_sharded_bfs: bfs_spmv over the shards, outputs as ssb_bfs_spmv (dist in
+ * original ids; sel-max parents when want_parents, parent_len = n, else 0;
+ * counters summed over the ranks). ERANGE bad root, ECAP at the cap.
+ * ssb_sharded_info: ranks, n, cells and segments per rank (arrays of n_ranks,
+ * may be NULL). */
+int ssb_ctx_create(int n_ranks, const int* device_ids, ssb_ctx** out);
+void ssb_ctx_destroy(ssb_ctx* ctx);
+int ssb_ctx_build(ssb_ctx* ctx, const ssb_edges* e, int64_t C, int64_t sigma, int segments_per_rank,
+                  ssb_sharded** out);
+int ssb_sharded_info(const ssb_sharded* sh, int* n_ranks, int64_t* n, int64_t* cells_per_rank,
+                     int64_t* segments_per_rank);
+int ssb_sharded_bfs(ssb_sharded* sh, int64_t root, const ssb_bfs_options* opts, int64_t* dist,
+                    int64_t* parent, int64_t* parent_len, ssb_iter_stats* stats, int64_t stats_cap,
+                    int64_t* iterations, double* device_ms);
+void ssb_sharded_destroy(ssb_sharded* sh);
+
 /* m_cc of the last run: Σ_{reached v} deg(v) / 2 (the GTEPS numerator). */
 int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc);
 

@@ -702,6 +702,83 @@ inline BfsResult bfs_traditional(const CsrView& csr, vid_t root) {
   return bfs_traditional(Graph(h), root);
 }
 
+// ---- one process, several B200s (ssb_ctx_*) -------
+/// The devices of a single-process multi-GPU job: all distinct (peer access
+/// between every pair, the frontier exchange fused over NVLink) or all the
+/// same (the ranks emulated as one cooperative launch on it).
+class Context {
+ public:
+  explicit Context(const std::vector<int>& device_ids) {
+    ssb_ctx* h = nullptr;
+    detail::check(ssb_ctx_create(static_cast<int>(device_ids.size()), device_ids.data(), &h));
+    h_.reset(h, &ssb_ctx_destroy);
+    ranks_ = static_cast<int>(device_ids.size());
+  }
+  ssb_ctx* handle() const { return h_.get(); }
+  int ranks() const { return ranks_; }
+
+ private:
+  std::shared_ptr<ssb_ctx> h_;
+  int ranks_ = 0;
+};
+
+/// A SlimSellRepr sharded over a Context (segments_per_rank round-robin,
+/// cell-balanced chunk segments per rank; each rank holds only its cells).
+class ShardedRepr {
+ public:
+  ShardedRepr(const Context& ctx, const Graph& g, std::int64_t C, std::int64_t sigma, int segments_per_rank = 4)
+      : ctx_(ctx) {
+    ssb_sharded* h = nullptr;
+    detail::check(ssb_ctx_build(ctx.handle(), g.handle(), C, sigma, segments_per_rank, &h));
+    h_.reset(h, &ssb_sharded_destroy);
+    int nr = 0;
+    detail::check(ssb_sharded_info(h, &nr, &n_, nullptr, nullptr));
+    cells_.resize(static_cast<std::size_t>(nr));
+    detail::check(ssb_sharded_info(h, &nr, nullptr, cells_.data(), nullptr));
+  }
+  ssb_sharded* handle() const { return h_.get(); }
+  vid_t n() const { return n_; }
+  const std::vector<std::int64_t>& cells_per_rank() const { return cells_; }
+
+ private:
+  Context ctx_;  // keeps the context alive
+  std::shared_ptr<ssb_sharded> h_;
+  vid_t n_ = 0;
+  std::vector<std::int64_t> cells_;
+};
+
+/// bfs.hpp:80-81 over the shards of a context (sel-max parents when
+/// want_parents; the other variants return dist only).
+inline BfsResult bfs_spmv(const ShardedRepr& r, vid_t root, const BfsOptions& opts) {
+  ssb_bfs_options o{};
+  o.variant = static_cast<std::int32_t>(opts.variant);
+  o.slimwork = opts.slimwork;
+  o.slimchunk_len = opts.slimchunk_len;
+  o.max_iterations = opts.max_iterations;
+  o.want_parents = opts.want_parents && opts.variant == Variant::selmax;
+  o.selmax_compat = opts.selmax_compat;
+  BfsResult res;
+  res.dist.resize(r.n());
+  res.parent.resize(r.n());
+  std::int64_t plen = 0, iters = 0;
+  std::vector<ssb_iter_stats> st(std::min<std::int64_t>(r.n() + 2, 1 << 16));
+  const int rc = ssb_sharded_bfs(r.handle(), root, &o, res.dist.data(), res.parent.data(), &plen, st.data(),
+                                 static_cast<std::int64_t>(st.size()), &iters, nullptr);
+  if (rc != SSB_OK && rc != SSB_ECAP) detail::raise(rc);
+  res.parent.resize(plen);
+  res.iterations = iters;
+  for (std::int64_t i = 0; i < std::min<std::int64_t>(iters, static_cast<std::int64_t>(st.size())); ++i) {
+    const auto& s = st[i];
+    res.per_iter.push_back({s.iteration, s.elapsed_ns, s.chunks_processed, s.chunks_skipped,
+                            s.subchunks_processed, s.columns_processed, s.frontier_size});
+  }
+  if (rc == SSB_ECAP) {
+    res.parent.clear();
+    throw BfsCapError(ssb_last_error(), std::move(res));
+  }
+  return res;
+}
+
 /// cli.cpp:73-112 (verify_against_oracle's tree checks) + Graph500 edge
 /// checks, on the device. Empty optional = valid, else a diff report.
 inline std::optional<std::string> validate_bfs(const Graph& g, vid_t root, const BfsResult& run,

@@ -108,6 +108,13 @@ def lib() -> C.CDLL:
         "ssb_bfs_shard_exchange": (C.c_int, [vp, C.c_void_p, C.c_int64]),
         "ssb_bfs_shard_fetch": (C.c_int, [vp, C.c_int, i64p, i64p]),
         "ssb_graph_stream": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
+        "ssb_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+        "ssb_ctx_destroy": (None, [vp]),
+        "ssb_ctx_build": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]),
+        "ssb_sharded_info": (C.c_int, [vp, C.POINTER(C.c_int), i64p, i64p, i64p]),
+        "ssb_sharded_bfs": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), i64p, i64p, i64p,
+                                      C.POINTER(IterStatsC), C.c_int64, i64p, C.POINTER(C.c_double)]),
+        "ssb_sharded_destroy": (None, [vp]),
         "ssb_bfs_shard_begin_async": (C.c_int, [vp, C.c_int64, C.POINTER(BfsOptionsC), C.c_int64, C.c_int64]),
         "ssb_bfs_shard_step_async": (C.c_int, [vp, C.c_void_p]),
         "ssb_bfs_shard_exchange_async": (C.c_int, [vp, C.c_void_p]),

@@ -43,6 +43,7 @@
 #include <memory>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <type_traits>
 #include <unistd.h>
 
@@ -2986,6 +2987,246 @@ int64_t bfs_edges_traversed(ssb_graph& g) {
   SSB_CUDA(cudaMemcpyAsync(&v, acc.p, 8, cudaMemcpyDeviceToHost, s));
   g.sc.sync();
   return int64_t(v / 2);
+}
+
+
+// ---- single-process multi-device context (SURVEY.md §8(b) ssb_ctx_create) ----
+// One host thread drives every rank of a sharded layout:
+//  * distinct devices: peer access enabled between every pair; each rank's
+//    frontier window is a plain device pointer the peers store into over
+//    NVLink (no IPC), and every BFS runs one cooperative launch per rank —
+//    the same per-rank path as a multi-process job (bfs_p2p, n_local = 1),
+//    each launched from its own host thread because the ranks meet at an
+//    in-kernel barrier;
+//  * one device listed several times: the ranks run as ONE cooperative
+//    launch on it (the emulated group, bfs_p2p n_local > 1).
+
+// partition_chunks + the snake deal of partition_segments (sharding.py):
+// k·W contiguous pieces of near-equal C·cl + 1 weight, dealt 0..W-1, W-1..0, ...
+std::vector<std::vector<int64_t>> partition_segments_host(const std::vector<int32_t>& cl, int64_t C, int world,
+                                                          int k) {
+  const int64_t nc = int64_t(cl.size());
+  const int pieces = world * k;
+  std::vector<int64_t> cum(size_t(nc) + 1, 0);
+  for (int64_t i = 0; i < nc; ++i) cum[size_t(i + 1)] = cum[size_t(i)] + C * int64_t(cl[size_t(i)]) + 1;
+  std::vector<int64_t> bounds{0};
+  for (int r = 1; r < pieces; ++r) {
+    const int64_t target = cum.back() * r / pieces;
+    int64_t b = int64_t(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+    b = std::min(std::max(b, bounds.back()), nc);
+    bounds.push_back(b);
+  }
+  bounds.push_back(nc);
+  std::vector<std::vector<int64_t>> out(static_cast<size_t>(world));
+  for (int j = 0; j < pieces; ++j) {
+    const int rnd = j / world, pos = j % world;
+    const int r = rnd % 2 == 0 ? pos : world - 1 - pos;
+    out[size_t(r)].push_back(bounds[size_t(j)]);
+    out[size_t(r)].push_back(bounds[size_t(j + 1)]);
+  }
+  return out;
+}
+
+namespace {
+struct DeviceGuard {  // restores the caller's current device
+  int prev = 0;
+  DeviceGuard() { SSB_CUDA(cudaGetDevice(&prev)); }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// the normalised edge set on `dev` (a device-to-device copy of e's keys)
+std::unique_ptr<ssb_edges> edges_on(const ssb_edges& e, int src_dev, int dev) {
+  SSB_CUDA(cudaSetDevice(dev));
+  auto c = std::make_unique<ssb_edges>();
+  c->n = e.n;
+  c->m = e.m;
+  c->bits = e.bits;
+  c->keys.alloc(e.keys.n);
+  SSB_CUDA(cudaStreamSynchronize(e.sc.s));
+  if (e.keys.n) SSB_CUDA(cudaMemcpyPeer(c->keys.p, dev, e.keys.p, src_dev, e.keys.bytes()));
+  return c;
+}
+}  // namespace
+
+ssb_ctx* ctx_create(int n_ranks, const int* device_ids) {
+  if (n_ranks < 1 || n_ranks > kMaxRanks) fail(SSB_EINVAL, "ranks must be in [1, 8]");
+  int n_dev = 0;
+  SSB_CUDA(cudaGetDeviceCount(&n_dev));
+  auto c = std::make_unique<ssb_ctx>();
+  for (int i = 0; i < n_ranks; ++i) {
+    const int d = device_ids ? device_ids[i] : i;
+    if (d < 0 || d >= n_dev) fail(SSB_EINVAL, "device id " + std::to_string(d) + " not present");
+    c->devs.push_back(d);
+  }
+  bool all_same = true, all_distinct = true;
+  for (int i = 0; i < n_ranks; ++i)
+    for (int j = 0; j < n_ranks; ++j)
+      if (i != j) {
+        all_same = all_same && c->devs[size_t(i)] == c->devs[size_t(j)];
+        all_distinct = all_distinct && c->devs[size_t(i)] != c->devs[size_t(j)];
+      }
+  if (!all_same && !all_distinct)
+    fail(SSB_EINVAL, "ranks must be on distinct devices, or all on one device (emulated group)");
+  c->group = n_ranks > 1 && all_same;
+  if (n_ranks > 1 && all_distinct) {
+    DeviceGuard guard;
+    for (int i = 0; i < n_ranks; ++i)
+      for (int j = 0; j < n_ranks; ++j) {
+        if (i == j) continue;
+        int ok = 0;
+        SSB_CUDA(cudaDeviceCanAccessPeer(&ok, c->devs[size_t(i)], c->devs[size_t(j)]));
+        if (!ok)
+          fail(SSB_ECUDA, "device " + std::to_string(c->devs[size_t(i)]) + " cannot access device " +
+                              std::to_string(c->devs[size_t(j)]) + " (no peer path for the fused exchange)");
+        SSB_CUDA(cudaSetDevice(c->devs[size_t(i)]));
+        const cudaError_t rc = cudaDeviceEnablePeerAccess(c->devs[size_t(j)], 0);
+        if (rc == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else SSB_CUDA(rc);
+      }
+  }
+  return c.release();
+}
+
+ssb_sharded* ctx_build(ssb_ctx& c, const ssb_edges& e, int64_t C, int64_t sigma, int k) {
+  if (C != 32) fail(SSB_EINVAL, "the sharded BFS needs the C = 32 layout");
+  if (k < 1 || k > kMaxSeg) fail(SSB_EINVAL, "segments per rank must be in [1, 8]");
+  DeviceGuard guard;
+  const int world = int(c.devs.size());
+  const int src = guard.prev;  // e lives on the current device
+  auto sh = std::make_unique<ssb_sharded>();
+  sh->ctx = &c;
+  {
+    std::unique_ptr<ssb_graph> meta(build_range_from_edges(e, C, sigma, {0, 0}));  // cl for the partition
+    sh->segs = partition_segments_host(meta->cl_host, C, world, k);
+    sh->n = meta->n;
+  }
+  for (int i = 0; i < world; ++i) {
+    const int d = c.devs[size_t(i)];
+    const ssb_edges* ei = &e;
+    std::unique_ptr<ssb_edges> copy;
+    if (d != src) {
+      copy = edges_on(e, src, d);
+      ei = copy.get();
+    }
+    SSB_CUDA(cudaSetDevice(d));
+    sh->g.emplace_back(build_range_from_edges(*ei, C, sigma, sh->segs[size_t(i)]));
+  }
+  if (!c.group && world > 1) {
+    // windows: every rank's frontier window as a raw peer pointer
+    std::vector<uint32_t*> wins(static_cast<size_t>(world));
+    std::vector<WinGeom> wgs(static_cast<size_t>(world));
+    for (int i = 0; i < world; ++i) {
+      SSB_CUDA(cudaSetDevice(c.devs[size_t(i)]));
+      wins[size_t(i)] = p2p_window_alloc(*sh->g[size_t(i)], wgs[size_t(i)]);
+      SSB_CUDA(cudaMemset(wins[size_t(i)], 0, sh->g[size_t(i)]->p2p_win.bytes()));
+    }
+    for (int i = 0; i < world; ++i) {
+      auto h = std::make_shared<P2PHost>();
+      h->rank = i;
+      h->world = world;
+      h->wg = wgs[size_t(i)];
+      h->segs = check_segments(*sh->g[size_t(i)], sh->segs[size_t(i)].data(),
+                               int64_t(sh->segs[size_t(i)].size() / 2));
+      for (int r = 0; r < world; ++r) h->win[r] = wins[size_t(r)];
+      sh->g[size_t(i)]->p2p = h;
+    }
+  }
+  for (int i = 0; i < world; ++i) {
+    SSB_CUDA(cudaSetDevice(c.devs[size_t(i)]));
+    sh->g[size_t(i)]->sc.sync();
+  }
+  return sh.release();
+}
+
+int sharded_bfs(ssb_sharded& sh, int64_t root, const ssb_bfs_options& o, int64_t* dist, int64_t* parent,
+                int64_t* parent_len, ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations,
+                double* device_ms) {
+  if (o.variant < 0 || o.variant > 3) fail(SSB_EINVAL, "bad variant");
+  if (root < 0 || root >= sh.n)
+    fail(SSB_ERANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(sh.n) + ")");
+  DeviceGuard guard;
+  ssb_ctx& c = *sh.ctx;
+  const int world = int(c.devs.size());
+  std::vector<ssb_graph*> gs;
+  for (auto& g : sh.g) gs.push_back(g.get());
+  std::vector<std::vector<ssb_iter_stats>> st(static_cast<size_t>(world));
+  std::vector<int64_t> its(static_cast<size_t>(world), 0);
+  std::vector<double> ms(static_cast<size_t>(world), 0);
+  std::vector<int> rcs(static_cast<size_t>(world), SSB_OK);
+  std::vector<std::string> errs(static_cast<size_t>(world));
+  const int64_t cap = std::max<int64_t>(stats_cap, 0) + 64;
+  if (world == 1 || c.group) {
+    SSB_CUDA(cudaSetDevice(c.devs[0]));
+    std::vector<int64_t> bounds, counts;
+    for (auto& s : sh.segs) {
+      counts.push_back(int64_t(s.size() / 2));
+      bounds.insert(bounds.end(), s.begin(), s.end());
+    }
+    if (world == 1 && !gs[0]->p2p) {  // a single rank: attach its own window
+      WinGeom wg;
+      uint32_t* w = p2p_window_alloc(*gs[0], wg);
+      SSB_CUDA(cudaMemset(w, 0, gs[0]->p2p_win.bytes()));
+      auto h = std::make_shared<P2PHost>();
+      h->wg = wg;
+      h->segs = check_segments(*gs[0], sh.segs[0].data(), int64_t(sh.segs[0].size() / 2));
+      h->win[0] = w;
+      gs[0]->p2p = h;
+    }
+    st[0].resize(size_t(cap));
+    rcs[0] = bfs_p2p(gs.data(), world == 1 ? 1 : world, bounds.data(), counts.data(), root, o, st[0].data(),
+                     cap, &its[0], &ms[0]);
+  } else {
+    std::vector<std::thread> th;
+    for (int i = 0; i < world; ++i) {
+      st[size_t(i)].resize(size_t(cap));
+      th.emplace_back([&, i] {
+        try {
+          SSB_CUDA(cudaSetDevice(c.devs[size_t(i)]));
+          rcs[size_t(i)] = bfs_p2p(&gs[size_t(i)], 1, nullptr, nullptr, root, o, st[size_t(i)].data(), cap,
+                                   &its[size_t(i)], &ms[size_t(i)]);
+        } catch (const Error& ex) {
+          rcs[size_t(i)] = ex.code;
+          errs[size_t(i)] = ex.what();
+        } catch (const std::exception& ex) {
+          rcs[size_t(i)] = SSB_ECUDA;
+          errs[size_t(i)] = ex.what();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int i = 0; i < world; ++i)
+      if (rcs[size_t(i)] != SSB_OK && rcs[size_t(i)] != SSB_ECAP) fail(rcs[size_t(i)], errs[size_t(i)]);
+  }
+  const int64_t iters = its[0];
+  // counters: summed over the ranks (each returns its own chunks' counts)
+  if (stats) {
+    for (int64_t j = 0; j < std::min<int64_t>(stats_cap, iters); ++j) {
+      ssb_iter_stats a = st[0][size_t(j)];
+      for (int i = 1; i < (c.group ? 1 : world); ++i) {
+        const ssb_iter_stats& b = st[size_t(i)][size_t(j)];
+        a.chunks_processed += b.chunks_processed;
+        a.chunks_skipped += b.chunks_skipped;
+        a.subchunks_processed += b.subchunks_processed;
+        a.columns_processed += b.columns_processed;
+        a.frontier_size += b.frontier_size;
+        a.elapsed_ns = std::max(a.elapsed_ns, b.elapsed_ns);
+      }
+      stats[j] = a;
+    }
+  }
+  if (iterations) *iterations = iters;
+  if (device_ms) *device_ms = *std::max_element(ms.begin(), ms.end());
+  // results: each rank writes its owned rows (original ids)
+  const bool want = o.want_parents && o.variant == SSB_SELMAX && rcs[0] == SSB_OK;
+  for (int64_t v = 0; dist && v < sh.n; ++v) dist[v] = INT64_MAX;
+  if (want && parent)
+    for (int64_t v = 0; v < sh.n; ++v) parent[v] = -1;
+  for (int i = 0; i < world; ++i) {
+    SSB_CUDA(cudaSetDevice(c.devs[size_t(i)]));
+    if (dist) shard_fetch(*gs[size_t(i)], want && parent, dist, want && parent ? parent : nullptr);
+  }
+  if (parent_len) *parent_len = want && parent ? sh.n : 0;
+  return rcs[0];
 }
 
 }  // namespace ssb

@@ -590,4 +590,51 @@ int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc) {
   });
 }
 
+int ssb_ctx_create(int n_ranks, const int* device_ids, ssb_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = ssb::ctx_create(n_ranks, device_ids);
+  });
+}
+
+void ssb_ctx_destroy(ssb_ctx* c) { delete c; }
+
+int ssb_ctx_build(ssb_ctx* c, const ssb_edges* e, int64_t C, int64_t sigma, int segments_per_rank,
+                  ssb_sharded** out) {
+  return guarded([&] {
+    need(c, "ctx");
+    need(e, "edges");
+    need(out, "out");
+    *out = ssb::ctx_build(*c, *e, C, sigma, segments_per_rank);
+  });
+}
+
+int ssb_sharded_info(const ssb_sharded* sh, int* n_ranks, int64_t* n, int64_t* cells_per_rank,
+                     int64_t* segments_per_rank) {
+  return guarded([&] {
+    need(sh, "sharded");
+    if (n_ranks) *n_ranks = int(sh->g.size());
+    if (n) *n = sh->n;
+    for (size_t i = 0; i < sh->g.size(); ++i) {
+      if (cells_per_rank) cells_per_rank[i] = sh->g[i]->n_cells;
+      if (segments_per_rank) segments_per_rank[i] = int64_t(sh->segs[i].size() / 2);
+    }
+  });
+}
+
+int ssb_sharded_bfs(ssb_sharded* sh, int64_t root, const ssb_bfs_options* opts, int64_t* dist,
+                    int64_t* parent, int64_t* parent_len, ssb_iter_stats* stats, int64_t stats_cap,
+                    int64_t* iterations, double* device_ms) {
+  int rc = SSB_OK;
+  const int grc = guarded([&] {
+    need(sh, "sharded");
+    need(opts, "opts");
+    rc = ssb::sharded_bfs(*sh, root, *opts, dist, parent, parent_len, stats, stats_cap, iterations, device_ms);
+    if (rc == SSB_ECAP) g_last_error = "iteration cap reached before fixed point";
+  });
+  return grc != SSB_OK ? grc : rc;
+}
+
+void ssb_sharded_destroy(ssb_sharded* sh) { delete sh; }
+
 }  // extern "C"

@@ -201,7 +201,41 @@ struct ssb_graph {
   ssb::StreamCtx sc;
 };
 
+// Single-process multi-device context: one rank per entry
+// of devs (all distinct: peer-mapped fused exchange; all equal: the ranks
+// emulated as one cooperative launch on that device).
+struct ssb_ctx {
+  std::vector<int> devs;
+  bool group = false;
+};
+
+// A layout sharded over a context's ranks: rank i holds the cells of its
+// round-robin chunk segments on devs[i].
+struct ssb_sharded {
+  ssb_ctx* ctx = nullptr;
+  int64_t n = 0;
+  std::vector<std::vector<int64_t>> segs;  // per rank: [b0, e0, b1, e1, ...]
+  std::vector<std::unique_ptr<ssb_graph>> g;
+  ~ssb_sharded() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (size_t i = 0; i < g.size(); ++i) {  // free each shard on its own device
+      if (ctx && i < ctx->devs.size()) cudaSetDevice(ctx->devs[i]);
+      g[i].reset();
+    }
+    cudaSetDevice(prev);
+  }
+};
+
 namespace ssb {
+// bfs.cu: the context
+ssb_ctx* ctx_create(int n_ranks, const int* device_ids);
+ssb_sharded* ctx_build(ssb_ctx& c, const ssb_edges& e, int64_t C, int64_t sigma, int segments_per_rank);
+int sharded_bfs(ssb_sharded& sh, int64_t root, const ssb_bfs_options& o, int64_t* dist, int64_t* parent,
+                int64_t* parent_len, ssb_iter_stats* stats, int64_t stats_cap, int64_t* iterations,
+                double* device_ms);
+std::vector<std::vector<int64_t>> partition_segments_host(const std::vector<int32_t>& cl, int64_t C, int world,
+                                                          int k);
 // builder.cu
 ssb_graph* build_from_edges(const ssb_edges& e, int64_t C, int64_t sigma);
 ssb_graph* build_range_from_edges(const ssb_edges& e, int64_t C, int64_t sigma,

@@ -501,3 +501,97 @@ def run_sharded_bfs_async(shard, comm, root: int, opts, max_iterations: int = 0,
     per_iter = [IterStats(k + 1, int(r[5]), *[int(x) for x in r[:5]]) for k, r in enumerate(tot)]
     shard.last_ms = ms
     return _gather_results([shard], opts, n, per_iter, fetch, converged)
+
+
+# ---- one process, several devices (ssb_ctx_*) ------------------------------
+
+class Context:
+    """The devices of a single-process multi-GPU job (ssb_ctx_create): all
+    distinct — peer access between every pair, one cooperative launch per
+    device with the fused NVLink exchange; all the same — the ranks emulated
+    as one cooperative launch on that device."""
+
+    def __init__(self, device_ids):
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        ids = (C.c_int * len(device_ids))(*[int(d) for d in device_ids])
+        h = C.c_void_p()
+        _check(L.lib().ssb_ctx_create(len(device_ids), ids, C.byref(h)))
+        self._h = h
+        self.device_ids = list(device_ids)
+
+    def build(self, g, C_: int = 32, sigma: int | None = None, segments: int = 4) -> "ShardedLayout":
+        """The layout of g sharded over the ranks (segments round-robin chunk
+        segments per rank)."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        h = C.c_void_p()
+        _check(L.lib().ssb_ctx_build(self._h, g._h, int(C_), int(sigma if sigma is not None else
+                                                                 g.num_vertices()), int(segments), C.byref(h)))
+        return ShardedLayout(self, h)
+
+    def __del__(self):
+        try:
+            from . import _lib as L
+            L.lib().ssb_ctx_destroy(self._h)
+        except Exception:
+            pass
+
+
+class ShardedLayout:
+    def __init__(self, ctx: Context, handle):
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import _check
+        self.ctx, self._h = ctx, handle
+        world = len(ctx.device_ids)
+        nr = C.c_int()
+        n = np.zeros(1, np.int64)
+        cells = np.zeros(world, np.int64)
+        segs = np.zeros(world, np.int64)
+        _check(L.lib().ssb_sharded_info(self._h, C.byref(nr), n.ctypes.data_as(L.i64p),
+                                        cells.ctypes.data_as(L.i64p), segs.ctypes.data_as(L.i64p)))
+        self.n, self.cells_per_rank, self.segments_per_rank = int(n[0]), cells, segs
+
+    def bfs_spmv(self, root: int, opts=None):
+        """bfs_spmv (bfs.hpp:80-81) over the shards; BfsResult as bfs_spmv."""
+        import ctypes as C
+
+        from . import _lib as L
+        from .api import BfsCapError, BfsOptions, BfsResult, _p, _raise, _stats_list
+        opts = opts or BfsOptions()
+        o = opts._c()
+        n = self.n
+        dist = np.empty(max(n, 1), np.int64)
+        parent = np.empty(max(n, 1), np.int64)
+        plen = np.zeros(1, np.int64)
+        it = np.zeros(1, np.int64)
+        ms = C.c_double()
+        cap = min(max(n + 2, 2), 1 << 12)
+        while True:
+            st = (L.IterStatsC * cap)()
+            rc = L.lib().ssb_sharded_bfs(self._h, int(root), C.byref(o), _p(dist), _p(parent), _p(plen), st, cap,
+                                         _p(it), C.byref(ms))
+            if rc not in (L.SSB_OK, L.SSB_ECAP):
+                _raise(rc)
+            if int(it[0]) <= cap:
+                break
+            cap = int(it[0])
+        k = int(it[0])
+        self.last_ms = float(ms.value)
+        res = BfsResult(dist[:n].copy(), parent[: int(plen[0])].copy(), k, _stats_list(st, k))
+        if rc == L.SSB_ECAP:
+            raise BfsCapError(L.lib().ssb_last_error().decode(), BfsResult(res.dist, res.dist[:0], k, res.per_iter))
+        return res
+
+    def __del__(self):
+        try:
+            from . import _lib as L
+            L.lib().ssb_sharded_destroy(self._h)
+        except Exception:
+            pass

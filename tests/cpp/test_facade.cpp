@@ -315,7 +315,35 @@ TEST_CASE(host_layout_upload_and_segment) {
   CHECK_THROWS_AS(bfs_traditional(csr, n), std::out_of_range);
 }
 
+// one process, several ranks (here all on device 0: the emulated group)
+TEST_CASE(context_sharded_bfs) {
+  Graph g = gen_kronecker(13, 16, 2);
+  SlimSellRepr r = build_slimsell(g, 32, g.num_vertices());
+  Context ctx({0, 0, 0});
+  ShardedRepr sh(ctx, g, 32, g.num_vertices(), 2);
+  std::int64_t cells = 0;
+  for (auto c : sh.cells_per_rank()) cells += c;
+  CHECK(cells == r.n_cells());
+  for (Variant v : {Variant::selmax, Variant::tropical}) {
+    BfsOptions o;
+    o.variant = v;
+    o.slimwork = true;
+    o.slimchunk_len = 32;
+    BfsResult a = bfs_spmv(sh, 11, o), b = bfs_spmv(r, 11, o);
+    CHECK(a.dist == b.dist && a.iterations == b.iterations);
+    if (v == Variant::selmax) CHECK(a.parent == b.parent);
+    bool same = a.per_iter.size() == b.per_iter.size();
+    for (std::size_t k = 0; same && k < a.per_iter.size(); ++k)
+      same = a.per_iter[k].columns_processed == b.per_iter[k].columns_processed &&
+             a.per_iter[k].chunks_skipped == b.per_iter[k].chunks_skipped &&
+             a.per_iter[k].frontier_size == b.per_iter[k].frontier_size;
+    CHECK(same);
+  }
+  CHECK_THROWS_AS(Context({0, 99}), std::invalid_argument);
+}
+
 int main() {
+  context_sharded_bfs();
   host_layout_upload_and_segment();
   ingest_and_checks();
   csr_layout_of_path4();

@@ -956,3 +956,53 @@ def test_edge_graphs_sharded_paths(ssb, port, edge_graphs, world):
                     if v == 3:
                         assert np.array_equal(parent, b.parent), key
                     assert dev_rows(ssb.BfsResult(dist, parent, len(per_iter), per_iter)) == port_rows(b.stats), key
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0]])
+def test_single_process_context_matches_single_gpu(ssb, port, devices):
+    """ssb_ctx_create / ssb_ctx_build / ssb_sharded_bfs: one host process
+    driving a sharded layout (round-robin segments, each rank holding only
+    its cells). On one B200 the ranks share device 0 and run as one
+    cooperative launch; the results equal the single-GPU engine and the
+    oracle in dist, sel-max parents and every counter."""
+    from paper_2010_09913_b200.sharding import Context
+    n, uv = port.gen_kronecker(16, 16, 3)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    ctx = Context(devices)
+    sh = ctx.build(g, 32, n, segments=3)
+    assert sum(sh.cells_per_rank) == L.n_cells and len(sh.cells_per_rank) == len(devices)
+    for root in (0, 9, 40000):
+        for v, sw, Lc in ((3, True, 64), (0, True, 0), (2, False, 2048)):
+            o = opts(ssb, v, sw, Lc)
+            res = sh.bfs_spmv(root, o)
+            b = port.bfs_spmv(L, root, v, sw, Lc)
+            assert np.array_equal(res.dist, b.dist), (root, v, devices)
+            if v == 3:
+                assert np.array_equal(res.parent, b.parent), (root, v, devices)
+            else:
+                assert len(res.parent) == 0
+            assert dev_rows(res) == port_rows(b.stats), (root, v, devices)
+    o = opts(ssb, 3, True, 64)
+    o.max_iterations = 2
+    with pytest.raises(ssb.BfsCapError):
+        sh.bfs_spmv(0, o)
+    with pytest.raises(ssb.OutOfRange):
+        sh.bfs_spmv(n, opts(ssb, 3, True, 64))
+    res = sh.bfs_spmv(9, opts(ssb, 3, True, 64))  # usable after the errors
+    assert np.array_equal(res.dist, port.bfs_spmv(L, 9, 3, True, 64).dist)
+
+
+def test_context_rejects_bad_device_lists(ssb):
+    import torch
+
+    from paper_2010_09913_b200.sharding import Context
+    nd = torch.cuda.device_count()
+    with pytest.raises(ssb.InvalidArgument):
+        Context([nd])  # not present
+    with pytest.raises(ssb.InvalidArgument):
+        Context([0] * 9)  # more than 8 ranks
+    if nd >= 2:
+        with pytest.raises(ssb.InvalidArgument):
+            Context([0, 0, 1])  # mixed
