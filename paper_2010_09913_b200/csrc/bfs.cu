@@ -228,6 +228,7 @@ struct P2PArgs {
   int64_t offArrive;           // uint64 arrival counter (cumulative)
   unsigned long long gen_base; // barrier generations completed before this launch
   unsigned long long arrivals; // CTAs per generation over all ranks
+  unsigned long long timeout_ns; // a peer missing for this long traps the kernel (0: wait forever)
   int32_t rank, world;
   int32_t nseg;                // owned chunk segments (round-robin partitions)
   int32_t wseg[2 * kMaxSeg];   // their frontier words [b, e) (= chunks, C = 32)
@@ -363,6 +364,9 @@ __device__ __forceinline__ void take_cells_direct(const int4 v, const Probe& pr,
   hit |= b;
 }
 
+#ifndef SSB_SPARSE_EXACT4
+#define SSB_SPARSE_EXACT4 0
+#endif
 #ifdef SSB_COUNT
 // debug counters (SSB_COUNT builds, one launch per iteration): open probes,
 // tail probes, exact lookups, exact hits, warp steps with a lookup
@@ -417,7 +421,7 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
   }
 #endif
   if (__any_sync(0xffffffffu, need)) {  // warp-uniform: no reconvergence bookkeeping
-    if (kEarly) {  // (A/B: the batched form does not help the sparse sweeps)
+    if (kEarly || SSB_SPARSE_EXACT4) {  // the four lookups of a step in flight together
       const uint32_t e = pr.exact4(c, need);
 #ifdef SSB_COUNT
       {
@@ -721,7 +725,13 @@ __device__ __forceinline__ void p2p_barrier(const P2PArgs& x, unsigned long long
       atomicAdd_system(reinterpret_cast<unsigned long long*>(x.win[r] + x.offArrive), 1ull);
     const unsigned long long* mine =
         reinterpret_cast<const unsigned long long*>(x.win[x.rank] + x.offArrive);
-    while (ld_acquire_sys(mine) < gen * x.arrivals) __nanosleep(64);
+    const uint64_t t0 = x.timeout_ns ? globaltimer() : 0;
+    while (ld_acquire_sys(mine) < gen * x.arrivals) {
+      __nanosleep(64);
+      // a rank that never arrives (died, or never launched) would hang every
+      // peer forever: fail the launch instead (the host sees an error)
+      if (x.timeout_ns && globaltimer() - t0 > x.timeout_ns) asm volatile("trap;");
+    }
   }
   __syncthreads();
   __threadfence();  // no stale L1 lines of the peers' words past this point
@@ -2713,6 +2723,7 @@ P2PArgs p2p_args(const ssb_graph& g, const P2PHost& h, const Geometry& G, unsign
   x.offSlots = h.wg.offSlots;
   x.offArrive = h.wg.offArrive;
   x.gen_base = h.gen;
+  x.timeout_ns = (unsigned long long)std::max(0, env_int("SSB_P2P_TIMEOUT_S", 60)) * 1000000000ull;
   x.arrivals = arrivals;
   x.rank = h.rank;
   x.world = h.world;

@@ -196,3 +196,50 @@ def test_exact_validator_rejects_valid_but_different_parents(ssb, port):
     assert ssb.validate_bfs(g, root, res.dist, bad, exact="min") is not None
     with pytest.raises(ssb.InvalidArgument):
         ssb.validate_bfs(g, root, dist, par, exact="selmax")  # needs the layout
+
+
+def test_config5_s28_exact_and_sharded_equal(ssb):
+    """Config 5's graph (Kronecker S28, 8.5e9 cells) on ONE B200 — the
+    reference needs ~210 GB of host RAM for it, so parity is the exact
+    validator (Graph500 edge checks + every parent equal to the reference's
+    sel-max rule) — and the fused multi-GPU decomposition of config 5 (8 ranks
+    x 4 round-robin segments, each holding only its cells) emulated in one
+    launch equals the single-GPU engine bit for bit."""
+    import torch
+
+    from paper_2010_09913_b200.fingerprint import graph500_roots
+    from paper_2010_09913_b200.sharding import partition_segments, run_p2p_group
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip("needs a 180 GB B200")
+    g = ssb.gen_kronecker(28, 16, 1)
+    n = g.num_vertices()
+    r = ssb.build_slimsell(g, 32, n)
+    roots = graph500_roots(r.degrees(), 2, 1)
+    db = ssb.DeviceBfs(r)
+    o = ssb.BfsOptions(variant=ssb.Variant.selmax, slimwork=True, slimchunk_len=2048)
+    single = {}
+    for root in roots:
+        k, _, stats, rc = db.run(root, o)
+        assert rc == 0
+        dist, par = db.fetch(True)
+        single[root] = (dist.copy(), par.copy(), rows(stats))
+    cl = r.cl
+    del db, r
+    gc.collect()
+    # config 5's decomposition, emulated: equal to the single-GPU engine
+    ranges = partition_segments(cl, 32, 8, 4)
+    reprs = [ssb.build_slimsell(g, 32, n, segments=sg) for sg in ranges]
+    d, p, per_iter, _ = run_p2p_group(reprs, ranges, roots[0], o, fetch=True)
+    assert np.array_equal(d, single[roots[0]][0]) and np.array_equal(p, single[roots[0]][1])
+    assert rows(per_iter) == single[roots[0]][2]
+    del reprs, d, p
+    gc.collect()
+    # the exact validator on the single-GPU results (layout rebuilt for perm)
+    r = ssb.build_slimsell(g, 32, n)
+    for root in roots:
+        dist, par, _ = single[root]
+        rep = ssb.validate_bfs(g, root, dist, par, selmax_compat=True, exact="selmax", layout=r)
+        assert rep is None, rep
+    del r, g
+    gc.collect()
