@@ -364,9 +364,6 @@ __device__ __forceinline__ void take_cells_direct(const int4 v, const Probe& pr,
   hit |= b;
 }
 
-#ifndef SSB_SPARSE_EXACT4
-#define SSB_SPARSE_EXACT4 0
-#endif
 #ifdef SSB_COUNT
 // debug counters (SSB_COUNT builds, one launch per iteration): open probes,
 // tail probes, exact lookups, exact hits, warp steps with a lookup
@@ -421,7 +418,7 @@ __device__ __forceinline__ void take_cells(const int4 v, const Probe& pr, uint32
   }
 #endif
   if (__any_sync(0xffffffffu, need)) {  // warp-uniform: no reconvergence bookkeeping
-    if (kEarly || SSB_SPARSE_EXACT4) {  // the four lookups of a step in flight together
+    if (kEarly) {  // (A/B: the batched form does not help the sparse sweeps; ER 2^26 k = 4-5 +5% slower)
       const uint32_t e = pr.exact4(c, need);
 #ifdef SSB_COUNT
       {
