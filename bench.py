@@ -661,6 +661,33 @@ def sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_f
                          "rows, all-reduced"}
 
 
+def sharded_e2e(torch, dist_mod, world, roots, run_fetch, mcc, variant_id, n):
+    """e2e of a sharded BFS through the public calls with HOST outputs: every
+    BFS of the step, then each rank's owned rows (int64 dist, + sel-max
+    parents) into pinned host arrays (ssb_bfs_shard_fetch: the unpermute
+    kernel writes them over PCIe); max over ranks."""
+    pd = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    pp = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+    run_fetch(roots[0], pd, pp)  # warm
+    if world > 1:
+        dist_mod.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for root in roots:
+        run_fetch(root, pd, pp)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=RED_DEV)
+    if world > 1:
+        dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+    per_row = 16 if variant_id == 3 else 8
+    return {"value": round(sum(mcc[x] for x in roots) / float(t.item()) / 1e9, 3), "unit": "GTEPS",
+            "h2d_bytes_per_step": 8 * len(roots), "d2h_bytes_per_step": per_row * n * len(roots),
+            "note": "every root's BFS, then each rank's owned rows (int64 dist" +
+                    (" + sel-max parent" if variant_id == 3 else "") + ") into pinned host arrays "
+                    "(ssb_bfs_shard_fetch); host wall clock, max over ranks"}
+
+
 def shard_evidence(a, world, n_padded, iters_first, cells_rank, peak):
     """Exchange volume and its NVLink floor next to the HBM figures."""
     words = (n_padded + 31) // 32
@@ -766,6 +793,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork):
         shard.fetch(variant_id == 3, dd, pp)
 
     mcc, golden = sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n)
+    e2e = sharded_e2e(torch, dist_mod, world, roots, run_fetch, mcc, variant_id, n)
     my_ms = float(np.mean(step_ms))
     t = torch.tensor([my_ms, swept], dtype=torch.float64, device=RED_DEV)
     per_rank_ms = [my_ms]
@@ -802,8 +830,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork):
         "data": DATA[a.graph],
         "config": config_of(a, slimwork, len(roots), f"chunk-range shards x{world}, frontier all-gather"),
         "roofline": None, "cpu_baseline": None,
-        "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                "note": "chunk-sharded mode reports device time only"},
+        "e2e": e2e,
         "clocks": clocks, "gpu_launches": int(launches[0]),
         "sharding": ev, "validation": {"reference_golden": golden},
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
@@ -907,6 +934,7 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork):
             shard.fetch(variant_id == 3, dd, pp)
 
     mcc, golden = sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n)
+    e2e = sharded_e2e(torch, dist_mod, world, roots, run_fetch, mcc, variant_id, n)
     my_ms = float(np.mean(step_ms))
     per_rank_ms = [my_ms]
     cells = [x.range_cells for x in (reprs if emu > 1 else [r])]
@@ -938,8 +966,7 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork):
                             cells_per_rank_max=max(x.range_cells for x in (reprs if emu > 1 else [r])),
                             n_cells=r.n_cells),
         "roofline": None, "cpu_baseline": None,
-        "e2e": {"value": None, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                "note": "p2p-sharded mode reports device time only"},
+        "e2e": e2e,
         "clocks": clocks, "gpu_launches": 2 * len(roots) * a.steps,
         "sharding": ev, "validation": {"reference_golden": golden},
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
