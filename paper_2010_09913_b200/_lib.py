@@ -37,10 +37,11 @@ class IterStatsC(C.Structure):
                                          "columns_processed", "frontier_size")]
 
 
-def build(verbose: bool = False) -> str:
-    """Compile libslimsell_b200.so for sm_100a (nvcc; no GPU needed)."""
-    out = subprocess.run(["make", "-s", "-C", CSRC, f"-j{min(8, os.cpu_count() or 1)}"],
-                         capture_output=not verbose, text=True)
+def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile libslimsell_b200.so for sm_100a (nvcc; no GPU needed).
+    force=True recompiles every source (make -B)."""
+    cmd = ["make", "-s", "-C", CSRC, f"-j{min(8, os.cpu_count() or 1)}"] + (["-B"] if force else [])
+    out = subprocess.run(cmd, capture_output=not verbose, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"building libslimsell_b200.so failed:\n{out.stdout}\n{out.stderr}")
     return LIB_PATH

@@ -1,6 +1,6 @@
 """e2e of ssb_bfs_spmv_batch (S26 sel-max, Graph500 roots, pinned int64
 outputs) for several shares of direct (DMA int64) fetch chunks
-(SSB_WIRE_DIRECT, read per fetch), each checked equal to the wire-only output."""
+(SSB_WIRE_DIRECT — an experiment that was reverted; only 0 exists now), each checked equal to the wire-only output."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -16,7 +16,7 @@ mcc = {}
 for x in roots:
     db.run(x, o); mcc[x] = db.edges_traversed()
 ref = None
-for pct in [0, 10, 20, 30, 40, 50, 0, 20, 30]:
+for pct in [int(x) for x in os.environ.get("PCTS", "0").split(",")]:
     os.environ["SSB_WIRE_DIRECT"] = str(pct)
     ssb.bfs_spmv_batch(r, roots[:2], o, None, [pins[i % 2][0] for i in range(2)], [pins[i % 2][1] for i in range(2)])
     t0 = time.perf_counter()
