@@ -345,6 +345,10 @@ int ssb_validate_bfs_exact(ssb_edges* e, const ssb_graph* layout, int64_t root, 
  * ssb_sharded_info: ranks, n, cells and segments per rank (arrays of n_ranks,
  * may be NULL). */
 int ssb_ctx_create(int n_ranks, const int* device_ids, ssb_ctx** out);
+/* The partition ssb_ctx_build uses (host only, no device): k·world contiguous
+ * chunk pieces of near-equal C·cl + 1 weight dealt to the ranks in snake
+ * order; bounds receives world·k pairs [b, e) rank by rank (2·world·k int64). */
+int ssb_partition_segments(const int32_t* cl, int64_t n_chunks, int64_t C, int world, int k, int64_t* bounds);
 void ssb_ctx_destroy(ssb_ctx* ctx);
 int ssb_ctx_build(ssb_ctx* ctx, const ssb_edges* e, int64_t C, int64_t sigma, int segments_per_rank,
                   ssb_sharded** out);

@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
         "ssb_bfs_shard_fetch": (C.c_int, [vp, C.c_int, i64p, i64p]),
         "ssb_graph_stream": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
         "ssb_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+        "ssb_partition_segments": (C.c_int, [i32p, C.c_int64, C.c_int64, C.c_int, C.c_int, i64p]),
         "ssb_ctx_destroy": (None, [vp]),
         "ssb_ctx_build": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]),
         "ssb_sharded_info": (C.c_int, [vp, C.POINTER(C.c_int), i64p, i64p, i64p]),

@@ -590,6 +590,19 @@ int ssb_bfs_edges_traversed(ssb_graph* g, int64_t* m_cc) {
   });
 }
 
+int ssb_partition_segments(const int32_t* cl, int64_t n_chunks, int64_t C, int world, int k, int64_t* bounds) {
+  return guarded([&] {
+    need(bounds, "bounds");
+    if (n_chunks > 0) need(cl, "cl");
+    if (world < 1 || k < 1) ssb::fail(SSB_EINVAL, "world and k must be >= 1");
+    const std::vector<int32_t> v(cl, cl + n_chunks);
+    const auto segs = ssb::partition_segments_host(v, C, world, k);
+    int64_t at = 0;
+    for (const auto& s : segs)
+      for (int64_t x : s) bounds[at++] = x;
+  });
+}
+
 int ssb_ctx_create(int n_ranks, const int* device_ids, ssb_ctx** out) {
   return guarded([&] {
     need(out, "out");

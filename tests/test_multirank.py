@@ -236,3 +236,45 @@ def test_bench_default_decomposition():
             del os.environ["SSB_BENCH_BACKEND"]
         else:
             os.environ["SSB_BENCH_BACKEND"] = old
+
+
+def test_native_partition_equals_python_partition():
+    """ssb_ctx_build's partition (C++, libslimsell_b200.so — host code, no
+    device needed) deals exactly the segments sharding.partition_segments
+    does, so a single-process context and a torch.distributed job shard a
+    layout identically."""
+    import ctypes as C
+
+    from paper_2010_09913_b200 import _lib as L
+    from paper_2010_09913_b200.sharding import partition_segments
+    rng = np.random.default_rng(7)
+    for nc in (1, 5, 1000, 77777):
+        cl = (rng.integers(0, 3000, nc) ** 2 // 3000)[::-1].astype(np.int32).copy()
+        for world, k in ((1, 1), (2, 4), (3, 2), (8, 4), (5, 3)):
+            out = np.zeros(2 * world * k, np.int64)
+            rc = L.lib().ssb_partition_segments(cl.ctypes.data_as(L.i32p), nc, 32, world, k,
+                                                out.ctypes.data_as(L.i64p))
+            assert rc == 0
+            py = partition_segments(cl, 32, world, k)
+            assert out.reshape(world, k, 2).tolist() == [[list(p) for p in sg] for sg in py], (nc, world, k)
+
+
+def test_fingerprints_numpy_torch_partial_and_roots(port):
+    """ph64 on the host (numpy) and on a torch device agree, partial sums over
+    disjoint rows add up to the whole (how sharded runs compare with the
+    reference), and graph500_roots follows the reference's pick_roots stream
+    (the oracle's so_pick_roots) with degree-0 vertices rejected."""
+    import torch
+
+    from paper_2010_09913_b200.fingerprint import (graph500_roots, ph64_format, ph64_np,
+                                                   ph64_partial_torch, ph64_torch)
+    v = np.random.default_rng(2).integers(-(1 << 62), 1 << 62, 300001).astype(np.int64)
+    v[::7] = np.iinfo(np.int64).max
+    t = torch.from_numpy(v)
+    assert ph64_np(v) == ph64_torch(t) == ph64_np(v, block=4096)
+    m = torch.from_numpy(np.random.default_rng(3).random(v.shape[0]) < 0.4)
+    assert ph64_format(ph64_partial_torch(t, m) + ph64_partial_torch(t, ~m)) == ph64_np(v)
+    n = 5000
+    deg = np.random.default_rng(4).integers(0, 3, n)
+    want = [int(x) for x in port.pick_roots(n, n, 1) if deg[x] > 0][:40]
+    assert graph500_roots(deg, 40, 1) == want
