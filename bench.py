@@ -70,6 +70,9 @@ def args_():
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--roots", type=int, default=64)
     ap.add_argument("--slimchunk", type=int, default=2048)
+    ap.add_argument("--chunk-height", type=int, default=32,
+                    help="SlimSell C (32 = the warp-wide engine; BASELINE config 1 uses C=8, sigma=C)")
+    ap.add_argument("--sigma", default="n", help="sorting scope: an integer, 'n' or 'C' (cli.cpp:156)")
     ap.add_argument("--variant", default="selmax", choices=["tropical", "real", "boolean", "selmax"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--graph", default="kronecker", choices=["kronecker", "er"],
@@ -95,6 +98,8 @@ def args_():
 from paper_2010_09913_b200.fingerprint import graph500_roots, ph64_torch  # noqa: E402  (loads no .so)
 
 GOLDEN_BIG = os.path.join(ROOT, "tests", "golden", "golden_big.json")
+L2_BYTES = 126 << 20
+L2_NOTE: dict = {}  # set by main() for layouts small enough to sit in L2
 ROOT_RULE = "pick_roots stream (cli.cpp:114-134) rejecting degree 0"
 
 
@@ -121,13 +126,14 @@ def config_of(a, slimwork, n_roots, parallelism, **extra):
     """The workload description both arms print (same keys, same values)."""
     gdesc = (f"erdos-renyi n=2^{a.scale} avg degree {a.avg_degree:g} seed {a.seed}" if a.graph == "er"
              else f"kronecker scale {a.scale} ef {a.edgefactor} seed {a.seed}")
-    cfg = {"workload": (f"{gdesc}, SlimSell C=32 sigma=n, {a.variant}, "
+    cfg = {"workload": (f"{gdesc}, SlimSell C={a.chunk_height} sigma={a.sigma}, "
+                        f"{a.variant}, "
                         f"slimwork={'on' if slimwork else 'off'}, slimchunk L={a.slimchunk}, "
                         f"{n_roots} Graph500 roots/step"),
-           "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": 32, "sigma": "n",
+           "graph": a.graph, "scale": a.scale, "edgefactor": a.edgefactor, "C": a.chunk_height, "sigma": a.sigma,
            "semiring": a.variant, "slimwork": slimwork, "slimchunk_len": a.slimchunk,
            "roots_per_step": n_roots, "root_rule": ROOT_RULE, "parallelism": parallelism,
-           "l2": "inputs larger than L2 (col >> 126 MB); no flush needed"}
+           "l2": L2_NOTE.get("note", "inputs larger than L2 (col >> 126 MB); no flush needed")}
     cfg.update(extra)
     return cfg
 
@@ -260,7 +266,9 @@ def build_graph(ssb, a, log):
     else:
         g = ssb.gen_kronecker(a.scale, a.edgefactor, a.seed)
     t1 = time.time()
-    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    n = g.num_vertices()
+    sigma = n if a.sigma == "n" else (a.chunk_height if a.sigma == "C" else int(a.sigma))
+    r = ssb.build_slimsell(g, a.chunk_height, sigma)
     t2 = time.time()
     m = g.num_edges()
     log(f"graph S{a.scale}: n={r.n} m={m} cells={r.n_cells} gen {t1 - t0:.2f}s build {t2 - t1:.2f}s")
@@ -416,6 +424,8 @@ def main():
         import torch
         shard, why = choose_shard(torch, world)
         log(f"N={world}: --shard {shard} ({why})")
+    if shard != "roots" and a.chunk_height != 32:
+        raise SystemExit("the sharded BFS needs the C = 32 layout")
     if shard == "chunks":
         return main_chunks(a, world, rank, local, log, variant_id, slimwork)
     if shard == "p2p":
@@ -462,9 +472,18 @@ def main():
     balg_total, kernel_ms_total, n_bfs = 0.0, 0.0, 0
     first_stats = None
     t_wall0 = time.time()
+    # layouts that fit L2 (config 1's S16) get it flushed before every BFS
+    flush = None
+    if 4 * r.n_cells < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+        L2_NOTE["note"] = (f"col = {4 * r.n_cells / 1e6:.1f} MB fits L2: a {2 * L2_BYTES >> 20} MB buffer is "
+                           "written before every timed BFS (outside its CUDA-event interval)")
     for s in range(a.steps):
         tot = 0.0
         for root in mine:
+            if flush is not None:
+                flush.fill_(s)
+                torch.cuda.synchronize()
             k, ms, stats, rc = db.run(root, opts)
             assert rc == 0, "BFS hit the iteration cap"
             kms, nl = db.last_timing()
@@ -504,7 +523,8 @@ def main():
     traffic, traffic_src = profiled_traffic(a)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "bfs32_kernel", "peak_source": peak_src,
+                "kernel": "bfs32_kernel" if r.C == 32 else "gen_chunk_kernel + gen_sweep_kernel (C != 32)",
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": round(balg_total / n_bfs),
                 "kernel_ms_per_launch": round(kernel_ms_total / n_bfs, 4),
                 "kernel_share_of_step": round(kernel_ms_total / max(sum(step_ms), 1e-9), 4)}
@@ -1014,7 +1034,11 @@ def main_reference(a, world, rank, local, log, variant_id, slimwork, cores):
     deg = g.degrees()
     roots = graph500_roots(deg, a.roots, a.seed)
     t0 = time.time()
-    rr = R.build_slimsell(g, 32, g.n)
+    sigma = g.n if a.sigma == "n" else (a.chunk_height if a.sigma == "C" else int(a.sigma))
+    rr = R.build_slimsell(g, a.chunk_height, sigma)
+    if 4 * rr.n_cells < 2 * L2_BYTES:  # the same config note as the B200 arm
+        L2_NOTE["note"] = (f"col = {4 * rr.n_cells / 1e6:.1f} MB fits L2: a {2 * L2_BYTES >> 20} MB buffer is "
+                           "written before every timed BFS (outside its CUDA-event interval)")
     t_build = time.time() - t0
     log(f"reference graph S{a.scale}: n={g.n} m={g.m} cells={rr.n_cells}; gen_kronecker {t_gen:.1f}s "
         f"build_slimsell {t_build:.1f}s (single-threaded, the reference's own code)")

@@ -1222,11 +1222,19 @@ struct ArgsG {
   uint8_t* skip;   // n_chunks
   int32_t* level;
   int32_t* parent;
-  unsigned long long* stats;  // one record
+  unsigned long long* stats;  // this iteration's record
+  const int* done;            // set once an earlier iteration of the batch found nothing new
   int32_t L, slimwork, root_code, k, selmax;
 };
 
+// is_converged (semiring.cpp:152-157) on the device: later iterations of the
+// same batch become no-ops
+__global__ void gen_done_kernel(const unsigned long long* stats, int* done) {
+  if (stats[0] == 0) *done = 1;
+}
+
 __global__ void gen_chunk_kernel(ArgsG a) {
+  if (*a.done) return;
   unsigned long long proc = 0, skp = 0, sub = 0, cols = 0;
   GRID_STRIDE(i, a.n_chunks) {
     bool s = false;
@@ -1249,19 +1257,49 @@ __global__ void gen_chunk_kernel(ArgsG a) {
   if (cols) atomicAdd(&a.stats[4], cols);
 }
 
-__global__ void gen_sweep_kernel(ArgsG a) {
+// Work units of the generic engine: a chunk's column range of at most
+// kGenUnitCols columns (hub chunks split across warps instead of one thread
+// per row walking a 5000-column row).
+struct GenUnit {
+  int32_t chunk, col_begin, col_len;
+};
+constexpr int32_t kGenUnitCols = 128;
+
+// One warp per unit; lane l (and l + 32, ... for C > 32) owns row l of the
+// chunk. The row's hit among the unit's columns is folded into hitbest[row]
+// with atomicMax: the largest frontier-neighbour position (sel-max's max,
+// bfs.cpp:94-101; any hit for the other semirings).
+__global__ void gen_units_kernel(ArgsG a, const GenUnit* __restrict__ units, int64_t n_units,
+                                 int32_t* __restrict__ hitbest) {
+  if (*a.done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_units; w += warps) {
+    const GenUnit u = units[w];
+    if (a.skip[u.chunk]) continue;
+    const int32_t* base = a.col + a.cs[u.chunk] + int64_t(u.col_begin) * a.C;
+    for (int64_t l = lane; l < a.C; l += 32) {
+      int32_t best = -1;
+      for (int32_t j = 0; j < u.col_len; ++j) {
+        const int32_t c = base[int64_t(j) * a.C + l];
+        if (c >= 0 && a.fcur[c]) best = c;  // columns ascend: the last hit is the largest
+      }
+      if (best >= 0) atomicMax(&hitbest[int64_t(u.chunk) * a.C + l], best);
+    }
+  }
+}
+
+// post_process_rows (semiring.cpp:90-124) per row, and the next frontier
+// for every row; hitbest is reset for the next iteration.
+__global__ void gen_final_kernel(ArgsG a, int32_t* __restrict__ hitbest) {
+  if (*a.done) return;
   unsigned long long front = 0;
   GRID_STRIDE(r, a.n_chunks * a.C) {
-    const int64_t ch = r / a.C, lane = r % a.C;
+    const int32_t best = hitbest[r];
     uint8_t nw = 0;
-    if (!a.skip[ch]) {
-      const int32_t* cells = a.col + a.cs[ch] + lane;
-      int32_t best = -1;
-      for (int32_t j = 0; j < a.cl[ch]; ++j) {
-        const int32_t c = cells[int64_t(j) * a.C];
-        if (c >= 0 && a.fcur[c]) best = c;
-      }
-      if (best >= 0 && r < a.n && !a.vis[r]) {
+    if (best >= 0) {
+      hitbest[r] = -1;
+      if (r < a.n && !a.vis[r]) {
         nw = 1;
         a.vis[r] = 1;
         a.level[r] = a.k;
@@ -2042,7 +2080,35 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
   g.level.ensure(size_t(std::max<int64_t>(np, 1)));
   g.parent.ensure(size_t(std::max<int64_t>(np, 1)));
   g.gbytes.ensure(size_t(3 * np + g.n_chunks + 16));
-  g.dstats.ensure(kStatW);
+  // iterations are enqueued kGenBatch at a time, each reading a device-side
+  // "converged" flag, so the host waits once per batch instead of once per
+  // iteration (a BFS of the small-C parity configs is a single batch)
+  constexpr int kGenBatch = 16;
+  g.dstats.ensure(size_t(kGenBatch) * kStatW);
+  g.flag.ensure(1);
+  // the unit plan (host, from cl) and the per-row hit slots, cached per graph
+  struct GenPlan {
+    DevBuf<GenUnit> units;
+    int64_t n_units = 0;
+    DevBuf<int32_t> hitbest;
+  };
+  if (!g.gen_plan) {
+    auto gp = std::make_shared<GenPlan>();
+    std::vector<GenUnit> us;
+    for (int64_t i = 0; i < g.n_chunks; ++i)
+      for (int32_t c = 0; c < g.cl_host[size_t(i)]; c += kGenUnitCols)
+        us.push_back({int32_t(i), c, std::min(kGenUnitCols, g.cl_host[size_t(i)] - c)});
+    // longest first: hub pieces start early instead of trailing the launch
+    std::stable_sort(us.begin(), us.end(), [](const GenUnit& x, const GenUnit& y) { return x.col_len > y.col_len; });
+    gp->n_units = int64_t(us.size());
+    gp->units.alloc(std::max<size_t>(us.size(), 1));
+    if (!us.empty())
+      SSB_CUDA(cudaMemcpy(gp->units.p, us.data(), us.size() * sizeof(GenUnit), cudaMemcpyHostToDevice));
+    gp->hitbest.alloc(size_t(std::max<int64_t>(np, 1)));
+    SSB_CUDA(cudaMemset(gp->hitbest.p, 0xff, gp->hitbest.bytes()));  // -1
+    g.gen_plan = gp;
+  }
+  GenPlan& GP = *static_cast<GenPlan*>(g.gen_plan.get());
   uint8_t* vis = g.gbytes.p;
   uint8_t* f0 = vis + np;
   uint8_t* f1 = f0 + np;
@@ -2070,32 +2136,56 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
   a.slimwork = o.slimwork ? 1 : 0;
   a.root_code = root_code;
   a.selmax = o.variant == SSB_SELMAX;
+  a.done = g.flag.p;
+  SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, sizeof(int), s));
   bool conv = false;
-  std::vector<int64_t> rec(kStatW);
-  for (int64_t k = 1; k <= cap && !conv; ++k) {
-    a.k = int32_t(k);
-    a.fcur = (k & 1) ? f0 : f1;
-    a.fnext = (k & 1) ? f1 : f0;
-    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, kStatW * 8, s));
-    SSB_CUDA(cudaEventRecord(g.sc.e0, s));
-    if (g.n_chunks) {
-      gen_chunk_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(a);
-      gen_sweep_kernel<<<grid_for(np), 256, 0, s>>>(a);
+  std::vector<int64_t> rec(size_t(kGenBatch) * kStatW);
+  std::vector<cudaEvent_t> ev(size_t(kGenBatch) + 1);
+  for (auto& e : ev) SSB_CUDA(cudaEventCreate(&e));
+  try {
+    for (int64_t kb = 1; kb <= cap && !conv;) {
+      const int64_t nb = std::min<int64_t>(kGenBatch, cap - kb + 1);
+      SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, size_t(nb) * kStatW * 8, s));
+      for (int64_t i = 0; i < nb; ++i) {
+        const int64_t k = kb + i;
+        a.k = int32_t(k);
+        a.fcur = (k & 1) ? f0 : f1;
+        a.fnext = (k & 1) ? f1 : f0;
+        a.stats = reinterpret_cast<unsigned long long*>(g.dstats.p + i * kStatW);
+        SSB_CUDA(cudaEventRecord(ev[size_t(i)], s));
+        if (g.n_chunks) {
+          gen_chunk_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(a);
+          if (GP.n_units)
+            gen_units_kernel<<<grid_for(GP.n_units * 32), 256, 0, s>>>(a, GP.units.p, GP.n_units, GP.hitbest.p);
+          gen_final_kernel<<<grid_for(np), 256, 0, s>>>(a, GP.hitbest.p);
+        }
+        gen_done_kernel<<<1, 1, 0, s>>>(a.stats, g.flag.p);
+        SSB_CUDA(cudaGetLastError());
+      }
+      SSB_CUDA(cudaEventRecord(ev[size_t(nb)], s));
+      SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, size_t(nb) * kStatW * 8, cudaMemcpyDeviceToHost, s));
+      SSB_CUDA(cudaEventRecord(g.sc.e_end, s));  // bfs_run's device-time end
+      g.sc.sync();
+      int64_t ran = 0;
+      for (int64_t i = 0; i < nb && !conv; ++i) {
+        ++ran;
+        int64_t* r = rec.data() + i * kStatW;
+        float ms = 0;
+        SSB_CUDA(cudaEventElapsedTime(&ms, ev[size_t(i)], ev[size_t(i + 1)]));
+        r[5] = int64_t(double(ms) * 1e6);
+        g.last_swept += r[4];  // the generic engine streams every processed column
+        g.last_kernel_ms += ms;
+        g.last_launches += g.n_chunks ? 4 : 1;
+        conv = r[0] == 0;
+      }
+      collect_stats(rec, kb, ran, stats);
+      kb += ran;
     }
-    SSB_CUDA(cudaGetLastError());
-    SSB_CUDA(cudaEventRecord(g.sc.e1, s));
-    SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, kStatW * 8, cudaMemcpyDeviceToHost, s));
-    SSB_CUDA(cudaEventRecord(g.sc.e_end, s));
-    g.sc.sync();
-    float ms = 0;
-    SSB_CUDA(cudaEventElapsedTime(&ms, g.sc.e0, g.sc.e1));
-    rec[5] = int64_t(double(ms) * 1e6);
-    g.last_swept += rec[4];  // the generic engine streams every processed column
-    g.last_kernel_ms += ms;
-    g.last_launches += g.n_chunks ? 2 : 0;
-    collect_stats(rec, k, 1, stats);
-    conv = rec[0] == 0;
+  } catch (...) {
+    for (auto e : ev) cudaEventDestroy(e);
+    throw;
   }
+  for (auto e : ev) cudaEventDestroy(e);
   // the shared epilogue reads the visited bitmap
   BitRegions R = bit_regions(g, 0);
   bytes_to_bits_kernel<<<grid_for((np + 31) / 32), 256, 0, s>>>(vis, np, R.visited);

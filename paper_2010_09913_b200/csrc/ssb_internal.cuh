@@ -197,6 +197,7 @@ struct ssb_graph {
   std::shared_ptr<void> p2p;      // ... and its peer table (bfs.cu)
   std::shared_ptr<void> geom;   // cached shared-memory image geometry (bfs.cu)
   std::shared_ptr<void> spmv_plan;  // work units of the last spmv_step chunk range (spmv.cu)
+  std::shared_ptr<void> gen_plan;   // work units + per-row hit slots of the C != 32 engine (bfs.cu)
 
   ssb::StreamCtx sc;
 };
