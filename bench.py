@@ -713,8 +713,9 @@ def shard_evidence(a, world, n_padded, iters_first, cells_rank, peak):
     words = (n_padded + 31) // 32
     per_iter_rank_in = 4 * words * (world - 1) // max(world, 1)  # bytes each rank receives per iteration
     return {"frontier_words": words, "exchange_bytes_per_iteration_per_rank": per_iter_rank_in,
-            "nvlink_gbs_assumed": 900.0,
-            "nvlink_floor_us_per_iteration": round(per_iter_rank_in / 900e9 * 1e6, 2),
+            "nvlink_gbs": 770.0, "nvlink_gbs_source": "measured peer copy per direction on this pool "
+                                                      "(B200_PROFILING.md; nominal 900)",
+            "nvlink_floor_us_per_iteration": round(per_iter_rank_in / 770e9 * 1e6, 2),
             "cells_per_rank": cells_rank, "iterations_first_root": iters_first,
             "hbm_peak_gbs": peak}
 
