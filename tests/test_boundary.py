@@ -53,3 +53,28 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "absent.so"))
     with pytest.raises(ImportError):
         _lib.lib()
+
+
+def test_new_entry_points_reject_bad_arguments_without_a_device(libpath):
+    """Round-2 entry points validate their arguments before touching a
+    device: status codes and the thread-local message, as the rest of the ABI."""
+    import numpy as np
+
+    from paper_2010_09913_b200 import _lib as L
+    lib = L.lib()
+    EINVAL = L.SSB_EINVAL
+    out = ctypes.c_void_p()
+    ids = (ctypes.c_int * 9)(*([0] * 9))
+    assert lib.ssb_ctx_create(0, ids, ctypes.byref(out)) == EINVAL
+    assert lib.ssb_ctx_create(9, ids, ctypes.byref(out)) == EINVAL
+    assert b"ranks" in lib.ssb_last_error()
+    bounds = np.zeros(8, np.int64)
+    cl = np.ones(4, np.int32)
+    assert lib.ssb_partition_segments(cl.ctypes.data_as(L.i32p), 4, 32, 0, 1,
+                                      bounds.ctypes.data_as(L.i64p)) == EINVAL
+    assert lib.ssb_partition_segments(cl.ctypes.data_as(L.i32p), 4, 32, 1, 1, None) == EINVAL
+    v = ctypes.c_int64()
+    assert lib.ssb_validate_bfs_exact(None, None, 0, None, None, 0, ctypes.byref(v), None, 0) == EINVAL
+    assert lib.ssb_sharded_bfs(None, 0, None, None, None, None, None, 0, None, None) == EINVAL
+    assert lib.ssb_spmv_segment(None, 0, None, None, 0, 0, 0) == EINVAL
+    assert lib.ssb_bfs_shard_front(None, 1, ctypes.byref(v)) == EINVAL
