@@ -1211,105 +1211,155 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32p_kernel(const __grid_consta
 
 // ---- generic engine (any C) ------------------------------------------------
 
+struct GenUnit {
+  int32_t chunk, col_begin, col_len;
+};
+constexpr int32_t kGenUnitCols = 256;
+
+// The C != 32 engine (the reference's small-C parity configurations, e.g.
+// config 1's C = 8): byte-per-row state, one cooperative launch for the whole
+// BFS, three grid-wide phases per iteration:
+//   A  should_skip_chunk (semiring.cpp:130-150) per chunk + the counters;
+//   B  one warp per work unit (a chunk's column range of <= kGenUnitCols
+//      columns, so hub chunks are split across warps); lane l (and l + 32,
+//      ... for C > 32) owns row l of the chunk and folds its largest
+//      frontier-neighbour position into hitbest[row] with atomicMax — the
+//      sel-max max (bfs.cpp:94-101), any hit for the other semirings;
+//   C  post_process_rows (semiring.cpp:90-124) per row, the next frontier,
+//      |newly|; hitbest is reset for the next iteration.
+// Convergence (semiring.cpp:152-157) and the per-iteration records stay on
+// the device.
 struct ArgsG {
   const int32_t* col;
   const int64_t* cs;
   const int32_t* cl;
   int64_t C, n, n_chunks;
   uint8_t* vis;    // n_padded
-  uint8_t* fcur;   // n_padded
-  uint8_t* fnext;  // n_padded
+  uint8_t* f0;     // n_padded: frontier of even iterations' input
+  uint8_t* f1;     // n_padded
   uint8_t* skip;   // n_chunks
   int32_t* level;
   int32_t* parent;
-  unsigned long long* stats;  // this iteration's record
-  const int* done;            // set once an earlier iteration of the batch found nothing new
-  int32_t L, slimwork, root_code, k, selmax;
+  const GenUnit* units;
+  int64_t n_units;
+  int32_t* hitbest;          // n_padded, -1 between iterations
+  unsigned long long* stats; // [kItersPerLaunch][kStatW]
+  int32_t L, slimwork, root_code, selmax;
+  int32_t k_begin, k_end;
 };
 
-// is_converged (semiring.cpp:152-157) on the device: later iterations of the
-// same batch become no-ops
-__global__ void gen_done_kernel(const unsigned long long* stats, int* done) {
-  if (stats[0] == 0) *done = 1;
-}
-
-__global__ void gen_chunk_kernel(ArgsG a) {
-  if (*a.done) return;
-  unsigned long long proc = 0, skp = 0, sub = 0, cols = 0;
-  GRID_STRIDE(i, a.n_chunks) {
-    bool s = false;
-    if (a.slimwork) {
-      s = true;
-      const int64_t r1 = min((i + 1) * a.C, a.n);
-      for (int64_t r = i * a.C; r < r1 && s; ++r) s = a.vis[r] != 0;
-    }
-    a.skip[i] = s;
-    if (s) ++skp;
-    else {
-      ++proc;
-      cols += uint32_t(a.cl[i]);
-      if (a.L > 0 && a.cl[i] > 0) sub += uint32_t((a.cl[i] + a.L - 1) / a.L);
-    }
-  }
-  if (proc) atomicAdd(&a.stats[1], proc);
-  if (skp) atomicAdd(&a.stats[2], skp);
-  if (sub) atomicAdd(&a.stats[3], sub);
-  if (cols) atomicAdd(&a.stats[4], cols);
-}
-
-// Work units of the generic engine: a chunk's column range of at most
-// kGenUnitCols columns (hub chunks split across warps instead of one thread
-// per row walking a 5000-column row).
-struct GenUnit {
-  int32_t chunk, col_begin, col_len;
-};
-constexpr int32_t kGenUnitCols = 128;
-
-// One warp per unit; lane l (and l + 32, ... for C > 32) owns row l of the
-// chunk. The row's hit among the unit's columns is folded into hitbest[row]
-// with atomicMax: the largest frontier-neighbour position (sel-max's max,
-// bfs.cpp:94-101; any hit for the other semirings).
-__global__ void gen_units_kernel(ArgsG a, const GenUnit* __restrict__ units, int64_t n_units,
-                                 int32_t* __restrict__ hitbest) {
-  if (*a.done) return;
+__global__ void __launch_bounds__(1024, 1) genc_kernel(const ArgsG a) {
+  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_units; w += warps) {
-    const GenUnit u = units[w];
-    if (a.skip[u.chunk]) continue;
-    const int32_t* base = a.col + a.cs[u.chunk] + int64_t(u.col_begin) * a.C;
-    for (int64_t l = lane; l < a.C; l += 32) {
-      int32_t best = -1;
-      for (int32_t j = 0; j < u.col_len; ++j) {
-        const int32_t c = base[int64_t(j) * a.C + l];
-        if (c >= 0 && a.fcur[c]) best = c;  // columns ascend: the last hit is the largest
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  const int64_t np = a.n_chunks * a.C;
+  uint64_t t_prev = 0;
+  if (tid == 0) t_prev = globaltimer();
+  for (int32_t k = a.k_begin; k < a.k_end; ++k) {
+    unsigned long long* st = a.stats + int64_t(k - a.k_begin) * kStatW;
+    const uint8_t* fcur = (k & 1) ? a.f0 : a.f1;  // F_{k-1}: k = 1 reads f0 (the root)
+    uint8_t* fnext = (k & 1) ? a.f1 : a.f0;
+    // A: SlimWork skip flags + processed / skipped / subchunk / column counters
+    {
+      unsigned long long proc = 0, skp = 0, sub = 0, cols = 0;
+      for (int64_t i = tid; i < a.n_chunks; i += nth) {
+        bool sk = false;
+        if (a.slimwork) {
+          sk = true;
+          const int64_t r1 = min((i + 1) * a.C, a.n);
+          for (int64_t r = i * a.C; r < r1 && sk; ++r) sk = a.vis[r] != 0;
+        }
+        a.skip[i] = sk;
+        if (sk) {
+          ++skp;
+        } else {
+          ++proc;
+          cols += uint32_t(a.cl[i]);
+          if (a.L > 0 && a.cl[i] > 0) sub += uint32_t((a.cl[i] + a.L - 1) / a.L);
+        }
       }
-      if (best >= 0) atomicMax(&hitbest[int64_t(u.chunk) * a.C + l], best);
-    }
-  }
-}
-
-// post_process_rows (semiring.cpp:90-124) per row, and the next frontier
-// for every row; hitbest is reset for the next iteration.
-__global__ void gen_final_kernel(ArgsG a, int32_t* __restrict__ hitbest) {
-  if (*a.done) return;
-  unsigned long long front = 0;
-  GRID_STRIDE(r, a.n_chunks * a.C) {
-    const int32_t best = hitbest[r];
-    uint8_t nw = 0;
-    if (best >= 0) {
-      hitbest[r] = -1;
-      if (r < a.n && !a.vis[r]) {
-        nw = 1;
-        a.vis[r] = 1;
-        a.level[r] = a.k;
-        if (a.selmax) a.parent[r] = a.k == 1 ? a.root_code : best;
-        ++front;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        proc += __shfl_xor_sync(0xffffffffu, proc, o);
+        skp += __shfl_xor_sync(0xffffffffu, skp, o);
+        sub += __shfl_xor_sync(0xffffffffu, sub, o);
+        cols += __shfl_xor_sync(0xffffffffu, cols, o);
+      }
+      if (lane == 0) {
+        if (proc) atomicAdd(&st[1], proc);
+        if (skp) atomicAdd(&st[2], skp);
+        if (sub) atomicAdd(&st[3], sub);
+        if (cols) atomicAdd(&st[4], cols);
       }
     }
-    a.fnext[r] = nw;
+    grid.sync();
+    // B: the sweep, one warp per unit. For C <= 32 the warp holds G = 32 / C
+    // column groups: lane l takes row l % C and columns l / C, l / C + G, ...
+    // (four in flight), so a C = 8 unit keeps every lane busy; each lane
+    // folds its own largest hit (the row's max over groups by atomicMax).
+    {
+      const int64_t C = a.C;
+      const int32_t G = C <= 32 ? int32_t(32 / C) : 1;
+      const int32_t grp = C <= 32 ? int32_t(lane / C) : 0;
+      for (int64_t w = tid >> 5; w < a.n_units; w += nth >> 5) {
+        const GenUnit u = a.units[w];
+        if (a.skip[u.chunk]) continue;
+        const int32_t* base = a.col + a.cs[u.chunk] + int64_t(u.col_begin) * C;
+        if (grp >= G) continue;  // lanes beyond G·C (C not a divisor of 32)
+        for (int64_t l = C <= 32 ? lane % C : lane; l < C; l += 32) {
+          int32_t best = -1;
+          int32_t j = grp;
+          for (; j + 3 * G < u.col_len; j += 4 * G) {
+            int32_t c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = base[int64_t(j + q * G) * C + l];
+            uint8_t f[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) f[q] = c[q] >= 0 ? fcur[c[q]] : uint8_t(0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (f[q]) best = max(best, c[q]);
+          }
+          for (; j < u.col_len; j += G) {
+            const int32_t c = base[int64_t(j) * C + l];
+            if (c >= 0 && fcur[c]) best = max(best, c);  // columns ascend within a row
+          }
+          if (best >= 0) atomicMax(&a.hitbest[int64_t(u.chunk) * C + l], best);
+        }
+      }
+    }
+    grid.sync();
+    // C: post-process, next frontier, |newly|
+    {
+      unsigned long long front = 0;
+      for (int64_t r = tid; r < np; r += nth) {
+        const int32_t best = a.hitbest[r];
+        uint8_t nw = 0;
+        if (best >= 0) {
+          a.hitbest[r] = -1;
+          if (r < a.n && !a.vis[r]) {
+            nw = 1;
+            a.vis[r] = 1;
+            a.level[r] = k;
+            if (a.selmax) a.parent[r] = k == 1 ? a.root_code : best;
+            ++front;
+          }
+        }
+        fnext[r] = nw;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) front += __shfl_xor_sync(0xffffffffu, front, o);
+      if (lane == 0 && front) atomicAdd(&st[0], front);
+    }
+    grid.sync();
+    if (tid == 0) {
+      const uint64_t t = globaltimer();
+      st[5] = t - t_prev;
+      t_prev = t;
+    }
+    if (*reinterpret_cast<volatile unsigned long long*>(&st[0]) == 0) break;  // is_converged
   }
-  if (front) atomicAdd(&a.stats[0], front);
 }
 
 // ---- shared init / epilogue kernels ---------------------------------------
@@ -2080,12 +2130,7 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
   g.level.ensure(size_t(std::max<int64_t>(np, 1)));
   g.parent.ensure(size_t(std::max<int64_t>(np, 1)));
   g.gbytes.ensure(size_t(3 * np + g.n_chunks + 16));
-  // iterations are enqueued kGenBatch at a time, each reading a device-side
-  // "converged" flag, so the host waits once per batch instead of once per
-  // iteration (a BFS of the small-C parity configs is a single batch)
-  constexpr int kGenBatch = 16;
-  g.dstats.ensure(size_t(kGenBatch) * kStatW);
-  g.flag.ensure(1);
+  g.dstats.ensure(size_t(kItersPerLaunch) * kStatW);
   // the unit plan (host, from cl) and the per-row hit slots, cached per graph
   struct GenPlan {
     DevBuf<GenUnit> units;
@@ -2098,7 +2143,7 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
     for (int64_t i = 0; i < g.n_chunks; ++i)
       for (int32_t c = 0; c < g.cl_host[size_t(i)]; c += kGenUnitCols)
         us.push_back({int32_t(i), c, std::min(kGenUnitCols, g.cl_host[size_t(i)] - c)});
-    // longest first: hub pieces start early instead of trailing the launch
+    // longest first: hub pieces start early instead of trailing the sweep
     std::stable_sort(us.begin(), us.end(), [](const GenUnit& x, const GenUnit& y) { return x.col_len > y.col_len; });
     gp->n_units = int64_t(us.size());
     gp->units.alloc(std::max<size_t>(us.size(), 1));
@@ -2113,7 +2158,7 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
   uint8_t* f0 = vis + np;
   uint8_t* f1 = f0 + np;
   uint8_t* skip = f1 + np;
-  SSB_CUDA(cudaMemsetAsync(vis, 0, size_t(2 * np), s));
+  SSB_CUDA(cudaMemsetAsync(vis, 0, size_t(2 * np), s));  // visited + F_0
   const uint8_t one = 1;
   SSB_CUDA(cudaMemcpyAsync(vis + root_pos, &one, 1, cudaMemcpyHostToDevice, s));
   SSB_CUDA(cudaMemcpyAsync(f0 + root_pos, &one, 1, cudaMemcpyHostToDevice, s));
@@ -2128,64 +2173,54 @@ bool run_generic(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bf
   a.n = g.n;
   a.n_chunks = g.n_chunks;
   a.vis = vis;
+  a.f0 = f0;
+  a.f1 = f1;
   a.skip = skip;
   a.level = g.level.p;
   a.parent = g.parent.p;
+  a.units = GP.units.p;
+  a.n_units = GP.n_units;
+  a.hitbest = GP.hitbest.p;
   a.stats = reinterpret_cast<unsigned long long*>(g.dstats.p);
   a.L = int32_t(std::max<int64_t>(0, std::min<int64_t>(o.slimchunk_len, INT32_MAX)));
   a.slimwork = o.slimwork ? 1 : 0;
   a.root_code = root_code;
   a.selmax = o.variant == SSB_SELMAX;
-  a.done = g.flag.p;
-  SSB_CUDA(cudaMemsetAsync(g.flag.p, 0, sizeof(int), s));
-  bool conv = false;
-  std::vector<int64_t> rec(size_t(kGenBatch) * kStatW);
-  std::vector<cudaEvent_t> ev(size_t(kGenBatch) + 1);
-  for (auto& e : ev) SSB_CUDA(cudaEventCreate(&e));
-  try {
-    for (int64_t kb = 1; kb <= cap && !conv;) {
-      const int64_t nb = std::min<int64_t>(kGenBatch, cap - kb + 1);
-      SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, size_t(nb) * kStatW * 8, s));
-      for (int64_t i = 0; i < nb; ++i) {
-        const int64_t k = kb + i;
-        a.k = int32_t(k);
-        a.fcur = (k & 1) ? f0 : f1;
-        a.fnext = (k & 1) ? f1 : f0;
-        a.stats = reinterpret_cast<unsigned long long*>(g.dstats.p + i * kStatW);
-        SSB_CUDA(cudaEventRecord(ev[size_t(i)], s));
-        if (g.n_chunks) {
-          gen_chunk_kernel<<<grid_for(g.n_chunks), 256, 0, s>>>(a);
-          if (GP.n_units)
-            gen_units_kernel<<<grid_for(GP.n_units * 32), 256, 0, s>>>(a, GP.units.p, GP.n_units, GP.hitbest.p);
-          gen_final_kernel<<<grid_for(np), 256, 0, s>>>(a, GP.hitbest.p);
-        }
-        gen_done_kernel<<<1, 1, 0, s>>>(a.stats, g.flag.p);
-        SSB_CUDA(cudaGetLastError());
-      }
-      SSB_CUDA(cudaEventRecord(ev[size_t(nb)], s));
-      SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, size_t(nb) * kStatW * 8, cudaMemcpyDeviceToHost, s));
-      SSB_CUDA(cudaEventRecord(g.sc.e_end, s));  // bfs_run's device-time end
-      g.sc.sync();
-      int64_t ran = 0;
-      for (int64_t i = 0; i < nb && !conv; ++i) {
-        ++ran;
-        int64_t* r = rec.data() + i * kStatW;
-        float ms = 0;
-        SSB_CUDA(cudaEventElapsedTime(&ms, ev[size_t(i)], ev[size_t(i + 1)]));
-        r[5] = int64_t(double(ms) * 1e6);
-        g.last_swept += r[4];  // the generic engine streams every processed column
-        g.last_kernel_ms += ms;
-        g.last_launches += g.n_chunks ? 4 : 1;
-        conv = r[0] == 0;
-      }
-      collect_stats(rec, kb, ran, stats);
-      kb += ran;
-    }
-  } catch (...) {
-    for (auto e : ev) cudaEventDestroy(e);
-    throw;
+  static int grid = 0;  // co-resident CTAs of 1024 threads, once per process
+  if (!grid) {
+    int per_sm = 0;
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)genc_kernel, 1024, 0));
+    if (per_sm < 1) fail(SSB_ECUDA, "genc kernel does not fit on an SM");
+    grid = num_sms() * std::min(per_sm, 2);
   }
-  for (auto e : ev) cudaEventDestroy(e);
+  bool conv = false;
+  std::vector<int64_t> rec(size_t(kItersPerLaunch) * kStatW);
+  for (int64_t kb = 1; kb <= cap && !conv;) {
+    const int64_t ke = std::min<int64_t>(cap + 1, kb + kItersPerLaunch);
+    a.k_begin = int32_t(kb);
+    a.k_end = int32_t(ke);
+    SSB_CUDA(cudaMemsetAsync(g.dstats.p, 0, size_t(ke - kb) * kStatW * 8, s));
+    void* params[] = {&a};
+    SSB_CUDA(cudaEventRecord(g.sc.e0, s));
+    SSB_CUDA(cudaLaunchCooperativeKernel((const void*)genc_kernel, dim3(grid), dim3(1024), params, 0, s));
+    SSB_CUDA(cudaGetLastError());
+    SSB_CUDA(cudaEventRecord(g.sc.e1, s));
+    SSB_CUDA(cudaMemcpyAsync(rec.data(), g.dstats.p, size_t(ke - kb) * kStatW * 8, cudaMemcpyDeviceToHost, s));
+    SSB_CUDA(cudaEventRecord(g.sc.e_end, s));  // bfs_run's device-time end
+    g.sc.sync();
+    float ms = 0;
+    SSB_CUDA(cudaEventElapsedTime(&ms, g.sc.e0, g.sc.e1));
+    g.last_kernel_ms += ms;
+    g.last_launches += 1;
+    int64_t ran = 0;
+    for (int64_t i = 0; i < ke - kb && !conv; ++i) {
+      ++ran;
+      g.last_swept += rec[size_t(i) * kStatW + 4];  // the generic engine streams every processed column
+      conv = rec[size_t(i) * kStatW] == 0;
+    }
+    collect_stats(rec, kb, ran, stats);
+    kb += ran;
+  }
   // the shared epilogue reads the visited bitmap
   BitRegions R = bit_regions(g, 0);
   bytes_to_bits_kernel<<<grid_for((np + 31) / 32), 256, 0, s>>>(vis, np, R.visited);
