@@ -76,3 +76,9 @@ print("by (body line, next level):")
 for k, v in sorted(agg2.items(), key=lambda kv: -kv[1][0])[:ntop]:
     txt = srcl[k[1] - 1].strip()[:70] if k[1] > 0 else "?"
     print(f"{k[0]:>5}/{k[1]:<5} {100*v[0]/T:5.1f}% samp {100*v[1]/E:5.1f}% inst  {txt}")
+if os.environ.get("DEEP"):
+    # innermost source line (any depth) inside take_cells / Probe
+    print("by innermost line:")
+    inner = collections.Counter()
+    for a, (ch) in addr_site.items():
+        pass
