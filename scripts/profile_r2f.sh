@@ -1,0 +1,16 @@
+#!/bin/bash
+# Final round-2 lines after the mask-form early-exit step (r2f): bench lines
+# without a profiler, iteration profile, then the ncu captures.
+R=r2f
+python -m pytest tests -m gpu -q > gpurun_out/${R}_gputest.log 2>&1; echo rc=$? >> gpurun_out/${R}_gputest.log
+python bench.py --steps 20 --warmup 5 > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err
+python bench.py --scale 22 --no-cpu-baseline > gpurun_out/${R}_s22_selmax.json 2> gpurun_out/${R}_s22.err
+python bench.py --graph er --no-cpu-baseline > gpurun_out/${R}_er.json 2> gpurun_out/${R}_er.err
+python bench.py --variant tropical --no-cpu-baseline > gpurun_out/${R}_s26_tropical.json 2> gpurun_out/${R}_s26t.err
+for c in "--scale 26" "--scale 22" "--scale 26 --graph er" "--scale 26 --variant 0"; do python scripts/iter_profile.py $c >> gpurun_out/${R}_iterprof.jsonl 2>/dev/null; done
+ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/${R}_launches.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-validate --e2e-steps 0 > gpurun_out/${R}_ncu_launches.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:bfs32 -s 1 -c 1 -o gpurun_out/${R}_bfs32_full \
+    python scripts/prof_iter.py --iters 100 --L 2048 --root 2564265 > gpurun_out/${R}_ncu_full.log 2>&1
+ncu --set full --clock-control none -k regex:bfs32 -s 1 -c 1 -o gpurun_out/${R}_bfs32_s22_full \
+    python scripts/prof_iter.py --scale 22 --iters 100 --L 2048 --g500 0 > gpurun_out/${R}_ncu_s22.log 2>&1
