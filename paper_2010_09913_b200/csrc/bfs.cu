@@ -371,7 +371,7 @@ __device__ __forceinline__ void take_cells_direct(const int4 v, const Probe& pr,
 __device__ unsigned long long g_cnt[8];
 #endif
 #ifndef SSB_LEAN_DENSE
-#define SSB_LEAN_DENSE 1  // A/B: S26 4.548 -> 4.470 ms per BFS, S22 0.443 -> 0.434, ER flat
+#define SSB_LEAN_DENSE 2  // A/B: S26 4.548 -> 4.470 (1) -> 4.439 (2) ms per BFS, S22 0.443 -> 0.434, ER flat
 #endif
 // The summary-probe early-exit step with mask arithmetic instead of per-cell
 // selects: one rotate-and-mask per probe puts its bit at position q, the
@@ -399,13 +399,21 @@ __device__ __forceinline__ void take_cells_lean(const int4 v, const Probe& pr, u
   uint32_t e = vb & pm;            // prefix bits are exact
   if (__any_sync(0xffffffffu, need)) {
     uint32_t x[4];
+#if SSB_LEAN_DENSE >= 2
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      x[q] = 0u;
+      if ((need >> q) & 1u) x[q] = pr.Fc[uint32_t(c[q]) >> 5];
+    }
+#else
 #pragma unroll
     for (int q = 0; q < 4; ++q) x[q] = pr.Fc[((need >> q) & 1u) ? (uint32_t(c[q]) >> 5) : 0u];
+#endif
 #pragma unroll
     for (int q = 0; q < 4; ++q) e |= __funnelshift_r(x[q], x[q], c[q] - q) & (need & (1u << q));
   }
   hit |= e;
-  if (kSelMax) {
+  if (kSelMax && (SSB_LEAN_DENSE < 2 || __any_sync(0xffffffffu, e))) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) best[q] = ((e >> q) & 1u) ? c[q] : best[q];
   }
