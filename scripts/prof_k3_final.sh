@@ -1,0 +1,4 @@
+export SSB_LIB=$PWD/build_variants/iters1.so
+python scripts/prof_iter.py --scale 26 --iters 3 --L 2048 --root 24490569 > gpurun_out/k3f_iters.txt 2>&1
+ncu --set full --import-source on --clock-control none -k regex:bfs32 -s 5 -c 1 -o gpurun_out/final_k3_mid python scripts/prof_iter.py --scale 26 --iters 3 --L 2048 --root 24490569 > gpurun_out/ncu_k3f.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:bfs32 -s 3 -c 1 -o gpurun_out/final_k4 python scripts/prof_iter.py --scale 26 --iters 4 --L 2048 --root 24490569 > gpurun_out/ncu_k4f.log 2>&1
