@@ -2014,7 +2014,10 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     // batched exact lookups of the early-exit sweep win once the summary is
     // mostly set, even when few rows exit early).
     const bool hubby = G.S == 8;
-    const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 4096 : 128));
+    // (hub-heavy: n/8192 since the mask-form early-exit step; A/B at S26 /
+    // S22 over 64 roots: 4096 4.455 / 0.434, 8192 4.420 / 0.434, 16384
+    // 4.411 / 0.437 ms per BFS)
+    const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 8192 : 128));
     a.dense_thr = std::max<int64_t>(1, g.n / div);
     // once |F| exceeds the summary's bits most of them are set: probe exactly
     const int64_t dt = env_int("SSB_DIRECT_THR", -1);

@@ -8,7 +8,7 @@ g = ssb.gen_kronecker(26, 16, 1); r = ssb.build_slimsell(g, 32, g.num_vertices()
 roots = graph500_roots(r.degrees(), 64, 1)
 db = ssb.DeviceBfs(r)
 o = ssb.BfsOptions(variant=ssb.Variant.selmax, slimwork=True, slimchunk_len=2048)
-dense_thr, direct_thr = r.n // 4096, 262144
+dense_thr, direct_thr = r.n // 8192, 262144
 rows = []
 for x in roots:
     k, ms, st, rc = db.run(x, o)
