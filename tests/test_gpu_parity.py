@@ -1006,3 +1006,47 @@ def test_context_rejects_bad_device_lists(ssb):
     if nd >= 2:
         with pytest.raises(ssb.InvalidArgument):
             Context([0, 0, 1])  # mixed
+
+
+def test_spmv_step_on_range_built_handles(ssb, port):
+    """spmv_step / spmv_step_device on a handle that holds only a chunk range
+    (a multi-GPU rank's cells): the rows of that range equal the whole
+    layout's product; ranges outside the held cells are refused."""
+    import torch
+    n, uv = port.gen_kronecker(13, 16, 4)
+    g = ssb.Graph.from_pairs(uv, n)
+    full = ssb.build_slimsell(g, 32, n)
+    nc = full.n_chunks
+    rng = np.random.default_rng(11)
+    for b, e in ((0, nc // 3), (nc // 3, nc), (5, 6)):
+        part = ssb.build_slimsell(g, 32, n, chunk_range=(b, e))
+        for v in range(4):
+            x = rng.integers(0, 1 << 30, full.n_padded)
+            want = ssb.spmv_step(full, ssb.Variant(v), x, np.zeros(full.n_padded, np.int64), b, e)
+            got = ssb.spmv_step(part, ssb.Variant(v), x, np.zeros(full.n_padded, np.int64), b, e)
+            assert np.array_equal(got, want), (b, e, v)
+            dx = torch.from_numpy(x).cuda()
+            dout = torch.zeros(full.n_padded, dtype=torch.int64, device="cuda")
+            ssb.spmv_step_device(part, ssb.Variant(v), dx, dout, b, e)
+            assert np.array_equal(dout.cpu().numpy(), want), (b, e, v)
+        if e < nc:
+            with pytest.raises(ssb.InvalidArgument):
+                ssb.spmv_step(part, ssb.Variant.real, x, None, b, e + 1)
+
+
+@pytest.mark.parametrize("segments", [1, 8])
+def test_context_segment_counts(ssb, port, segments):
+    """ssb_ctx_build with 1 and 8 round-robin segments per rank (the two
+    ends of the partition's range) equals the oracle."""
+    from paper_2010_09913_b200.sharding import Context
+    n, uv = port.gen_kronecker(14, 16, 6)
+    g = ssb.Graph.from_pairs(uv, n)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    sh = Context([0, 0, 0]).build(g, 32, n, segments=segments)
+    assert all(s <= segments for s in sh.segments_per_rank)
+    for root in (1, 777):
+        res = sh.bfs_spmv(root, opts(ssb, 3, True, 128))
+        b = port.bfs_spmv(L, root, 3, True, 128)
+        assert np.array_equal(res.dist, b.dist) and np.array_equal(res.parent, b.parent)
+        assert dev_rows(res) == port_rows(b.stats)
