@@ -604,7 +604,7 @@ def main():
             dd, pp = db.fetch(True)
             same = bool(np.array_equal(dd, out.dist) and np.array_equal(pp, out.parent))
             cpu = {"value": round(mcc[root0] / t / 1e9, 5), "unit": "GTEPS", "cores": cores,
-                   "kind": "reference",
+                   "kind": "reference", "cpu_model": lscpu_model(),
                    "sample": f"1 of {len(roots)} roots (root {root0}), full S{a.scale} graph; "
                              f"reference bfs_spmv, workers={cores}, dynamic_queue; t = Σ elapsed_ns "
                              f"{t:.2f}s (wall {wall:.2f}s)",
