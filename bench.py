@@ -87,6 +87,8 @@ def args_():
                          "other's memory, else chunks; single GPU at N = 1): independent roots per "
                          "rank, chunk-range shards with a per-iteration NCCL frontier all-gather, or "
                          "chunk-range shards with the exchange fused into the BFS kernel (p2p)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="N > 1: skip the secondary root-parallel figure")
     ap.add_argument("--segments", type=int, default=4,
                     help="--shard p2p: chunk segments per rank, dealt round-robin (snake order)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
@@ -708,6 +710,35 @@ def sharded_e2e(torch, dist_mod, world, roots, run_fetch, mcc, variant_id, n):
                     "(ssb_bfs_shard_fetch); host wall clock, max over ranks"}
 
 
+def root_parallel_secondary(torch, dist_mod, ssb, a, world, rank, roots, opts, mcc):
+    """The secondary figure at N > 1: every rank holds the WHOLE layout and
+    runs roots[rank::N] with no collective (what root-parallel batches give on
+    this box), timed like the primary line (device time, max over ranks)."""
+    g = (ssb.gen_erdos_renyi(1 << a.scale, a.avg_degree / ((1 << a.scale) - 1), a.seed) if a.graph == "er"
+         else ssb.gen_kronecker(a.scale, a.edgefactor, a.seed))
+    r = ssb.build_slimsell(g, 32, g.num_vertices())
+    del g
+    db = ssb.DeviceBfs(r)
+    mine = roots[rank::world]
+    for root in mine:
+        db.run(root, opts)
+    if world > 1:
+        dist_mod.barrier()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(a.steps):
+        for root in mine:
+            tot += db.run(root, opts)[1]
+    t = torch.tensor([tot / a.steps], dtype=torch.float64, device=RED_DEV)
+    if world > 1:
+        dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+    ms = float(t.item())
+    del db, r
+    return {"value": round(sum(mcc[x] for x in roots) / (ms * 1e-3) / 1e9, 3), "unit": "GTEPS",
+            "ms_per_step": round(ms, 3),
+            "what": "secondary: every rank holds the whole layout and runs roots[rank::N], no data-path collective"}
+
+
 def shard_evidence(a, world, n_padded, iters_first, cells_rank, peak):
     """Exchange volume and its NVLink floor next to the HBM figures."""
     words = (n_padded + 31) // 32
@@ -815,6 +846,9 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork):
 
     mcc, golden = sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n)
     e2e = sharded_e2e(torch, dist_mod, world, roots, run_fetch, mcc, variant_id, n)
+    secondary = None
+    if world > 1 and not a.no_secondary:
+        secondary = root_parallel_secondary(torch, dist_mod, ssb, a, world, rank, roots, opts, mcc)
     my_ms = float(np.mean(step_ms))
     t = torch.tensor([my_ms, swept], dtype=torch.float64, device=RED_DEV)
     per_rank_ms = [my_ms]
@@ -853,7 +887,7 @@ def main_chunks(a, world, rank, local, log, variant_id, slimwork):
         "roofline": None, "cpu_baseline": None,
         "e2e": e2e,
         "clocks": clocks, "gpu_launches": int(launches[0]),
-        "sharding": ev, "validation": {"reference_golden": golden},
+        "sharding": ev, "validation": {"reference_golden": golden}, "root_parallel": secondary,
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
                    "build_s": round(t_build, 3),
                    "clock": "CUDA events on the shard stream" if mode == "async" else
@@ -956,6 +990,9 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork):
 
     mcc, golden = sharded_parity(torch, dist_mod, world, a, roots, variant_id, slimwork, run_fetch, deg, n)
     e2e = sharded_e2e(torch, dist_mod, world, roots, run_fetch, mcc, variant_id, n)
+    secondary = None
+    if world > 1 and emu == 1 and not a.no_secondary:
+        secondary = root_parallel_secondary(torch, dist_mod, ssb, a, world, rank, roots, opts, mcc)
     my_ms = float(np.mean(step_ms))
     per_rank_ms = [my_ms]
     cells = [x.range_cells for x in (reprs if emu > 1 else [r])]
@@ -989,7 +1026,7 @@ def main_p2p(a, world, rank, local, log, variant_id, slimwork):
         "roofline": None, "cpu_baseline": None,
         "e2e": e2e,
         "clocks": clocks, "gpu_launches": 2 * len(roots) * a.steps,
-        "sharding": ev, "validation": {"reference_golden": golden},
+        "sharding": ev, "validation": {"reference_golden": golden}, "root_parallel": secondary,
         "timing": {"device_ms_steps": [round(x, 3) for x in step_ms], "gen_s": round(t_gen, 3),
                    "build_s": round(t_build, 3)},
     }
