@@ -278,3 +278,84 @@ def test_fingerprints_numpy_torch_partial_and_roots(port):
     deg = np.random.default_rng(4).integers(0, 3, n)
     want = [int(x) for x in port.pick_roots(n, n, 1) if deg[x] > 0][:40]
     assert graph500_roots(deg, 40, 1) == want
+
+
+class _FakeShard:
+    """A numpy stand-in for sharding.DeviceShard (the 1-bit sweep of
+    sweep_range over chunks [b, e)) so run_sharded_bfs's host logic runs on
+    CPU: lockstep iterations, the all-gather, the counter sums, the
+    iteration cap."""
+
+    def __init__(self, L, b, e):
+        import types
+        self.L, self.b, self.e = L, b, e
+        self.r = types.SimpleNamespace(n=L.n)
+
+    def begin(self, root, opts):
+        L = self.L
+        self.k = 0
+        self.sw, self.Lseg = bool(opts.slimwork), int(opts.slimchunk_len)
+        self.root_code = root
+        rp = int(L.inv_perm[root])
+        self.visited = np.zeros(L.n_chunks, dtype=np.uint32)
+        self.F = np.zeros(L.n_chunks, dtype=np.uint32)
+        self.visited[rp >> 5] |= np.uint32(1 << (rp & 31))
+        self.F[rp >> 5] |= np.uint32(1 << (rp & 31))
+        self.level = np.full(L.n_padded, -1, dtype=np.int64)
+        self.parent = np.full(L.n_padded, -1, dtype=np.int64)
+        self.level[rp], self.parent[rp] = 0, root
+        self.rp = rp
+
+    def step(self):
+        import torch
+
+        from paper_2010_09913_b200.api import IterStats
+        self.k += 1
+        newF, st = sweep_range(self.L, self.b, self.e, self.F, self.visited, self.k, self.root_code,
+                               self.level, self.parent, self.sw, self.Lseg)
+        s = IterStats(self.k, 0, *[int(x) for x in st])
+        return s, torch.from_numpy(newF.view(np.int32).copy())
+
+    def exchange(self, full, newly_total):
+        words = full.numpy().view(np.uint32)
+        self.visited |= words
+        self.F = words.copy()
+
+    def fetch(self, want_parents, dist, parent):
+        L = self.L
+        for pos in range(32 * self.b, min(32 * self.e, L.n)):
+            o = int(L.perm[pos])
+            if self.level[pos] >= 0:
+                dist[o] = self.level[pos]
+                if want_parents:
+                    parent[o] = int(L.perm[self.parent[pos]])
+        if want_parents and self.b <= self.rp >> 5 < self.e:
+            parent[int(L.perm[self.rp])] = int(L.perm[self.root_code])
+
+
+def test_run_sharded_bfs_host_logic_and_cap(port):
+    """sharding.run_sharded_bfs over two shards in one process (LocalComm):
+    dist, sel-max parents (the reference's root encoding) and every counter
+    equal the oracle; opts.max_iterations caps the BFS with BfsCapError
+    carrying the partial distances and no parents (bfs.cpp:86-90)."""
+    from paper_2010_09913_b200.api import BfsCapError, BfsOptions, Variant
+    from paper_2010_09913_b200.sharding import LocalComm, run_sharded_bfs
+    n, uv = port.gen_kronecker(10, 16, 9)
+    row, col = port.to_csr(n, uv)
+    L = port.build_slimsell(n, row, col, 32, n)
+    ranges = partition_chunks(L.cl, 32, 2)
+    shards = [_FakeShard(L, b, e) for b, e in ranges]
+    for root in (3, 500):
+        o = BfsOptions(variant=Variant.selmax, slimwork=True, slimchunk_len=8)
+        dist_, parent, per_iter = run_sharded_bfs(shards, LocalComm(), root, o)
+        ref = port.bfs_spmv(L, root, 3, True, 8)
+        assert np.array_equal(dist_, ref.dist)
+        assert np.array_equal(parent, ref.parent)
+        assert [[s.chunks_processed, s.chunks_skipped, s.subchunks_processed, s.columns_processed,
+                 s.frontier_size] for s in per_iter] == [[int(r[c]) for c in (2, 3, 4, 5, 6)] for r in ref.stats]
+    o = BfsOptions(variant=Variant.selmax, slimwork=True, slimchunk_len=8, max_iterations=2)
+    with pytest.raises(BfsCapError) as ei:
+        run_sharded_bfs(shards, LocalComm(), 3, o)
+    capped = port.bfs_spmv(L, 3, 3, True, 8, max_iterations=2)
+    assert ei.value.partial.iterations == 2 and len(ei.value.partial.parent) == 0
+    assert np.array_equal(ei.value.partial.dist, capped.dist)
