@@ -8,6 +8,9 @@
 // Everything lives in the inline namespace slimsell::b200, so user code keeps
 // writing slimsell::bfs_spmv(...) while the mangled names differ from the
 // reference's — both libraries can be linked into one test binary.
+// A translation unit that ALSO includes the reference's headers defines
+// SLIMSELL_B200_ALONGSIDE_REFERENCE first: b200 is then an ordinary nested
+// namespace, slimsell::X names the reference's X and slimsell::b200::X ours.
 //
 // Differences a maintainer should know:
 //  * Graph and SlimSellRepr own DEVICE handles; their host arrays
@@ -44,7 +47,11 @@
 #include "slimsell_b200.h"
 
 namespace slimsell {
+#ifdef SLIMSELL_B200_ALONGSIDE_REFERENCE
+namespace b200 {
+#else
 inline namespace b200 {
+#endif
 
 // ---- graph.hpp ----------------------------------------------------------
 using vid_t = std::int64_t;
@@ -456,17 +463,26 @@ inline SlimSellRepr upload(const HostRepr& r, bool force = false) {
   return *c.dev;
 }
 
-template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
-inline void spmv_step(const HostRepr& r, const SemiringSpec& s, std::span<const val_t> x_prev,
+// The semiring may be the reference's own SemiringSpec (its variant selects
+// the device algebra).
+template <class HostRepr, class Semi, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline void spmv_step(const HostRepr& r, const Semi& s, std::span<const val_t> x_prev,
                       std::span<val_t> out, std::int64_t chunk_begin, std::int64_t chunk_end) {
-  spmv_step(upload(r), s, x_prev, out, chunk_begin, chunk_end);
+  spmv_step(upload(r), semiring(static_cast<Variant>(static_cast<int>(s.variant))), x_prev, out,
+            chunk_begin, chunk_end);
 }
 
-template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
-inline void spmv_segment(const HostRepr& r, const SemiringSpec& s, std::span<const val_t> x_prev,
+template <class HostRepr, class Semi, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline std::vector<val_t> spmv_step(const HostRepr& r, const Semi& s, std::span<const val_t> x_prev) {
+  return spmv_step(upload(r), semiring(static_cast<Variant>(static_cast<int>(s.variant))), x_prev);
+}
+
+template <class HostRepr, class Semi, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline void spmv_segment(const HostRepr& r, const Semi& s, std::span<const val_t> x_prev,
                          std::span<val_t> acc, std::int64_t chunk, std::int64_t col_begin,
                          std::int64_t col_len) {
-  spmv_segment(upload(r), s, x_prev, acc, chunk, col_begin, col_len);
+  spmv_segment(upload(r), semiring(static_cast<Variant>(static_cast<int>(s.variant))), x_prev, acc,
+               chunk, col_begin, col_len);
 }
 
 /// repr.hpp:104-107 (repr.cpp:239-253) — pure relabelling through perm.
@@ -567,8 +583,9 @@ inline std::vector<val_t> combine_partials(const SemiringSpec& s,
 /// bfs.hpp:80-81 — algebraic BFS on the device. As the reference: sel-max
 /// parents always (when want_parents), the other variants only with a CSR
 /// (dp_transform semantics, evaluated on the device over the layout).
-inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& opts,
-                          const CsrView* csr_for_parents = nullptr) {
+namespace detail {
+inline BfsResult bfs_spmv_device(const SlimSellRepr& r, vid_t root, const BfsOptions& opts,
+                                 bool csr_given) {
   ssb_bfs_options o{};
   o.variant = static_cast<std::int32_t>(opts.variant);
   o.slimwork = opts.slimwork;
@@ -576,8 +593,7 @@ inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& o
   o.schedule = static_cast<std::int32_t>(opts.schedule);
   o.workers = opts.workers;
   o.max_iterations = opts.max_iterations;
-  o.want_parents = opts.want_parents &&
-                   (opts.variant == Variant::selmax || csr_for_parents != nullptr);
+  o.want_parents = opts.want_parents && (opts.variant == Variant::selmax || csr_given);
   o.selmax_compat = opts.selmax_compat;
   BfsResult res;
   res.dist.resize(r.n);
@@ -604,12 +620,21 @@ inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& o
   if (rc == SSB_ECAP) throw BfsCapError(ssb_last_error(), std::move(res));
   return res;
 }
+}  // namespace detail
 
-/// bfs.hpp:80-81 on a layout the reference built on the host (upload()).
-template <class HostRepr, std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
-inline BfsResult bfs_spmv(const HostRepr& r, vid_t root, const BfsOptions& opts,
+inline BfsResult bfs_spmv(const SlimSellRepr& r, vid_t root, const BfsOptions& opts,
                           const CsrView* csr_for_parents = nullptr) {
-  return bfs_spmv(upload(r), root, opts, csr_for_parents);
+  return detail::bfs_spmv_device(r, root, opts, csr_for_parents != nullptr);
+}
+
+/// bfs.hpp:80-81 on a layout the reference built on the host (upload()). The
+/// CSR may be the reference's own CsrView: only its presence matters (the
+/// parents are dp_transform's, evaluated on the device over the layout).
+template <class HostRepr, class Csr = CsrView,
+          std::enable_if_t<detail::is_host_repr<HostRepr>::value, int> = 0>
+inline BfsResult bfs_spmv(const HostRepr& r, vid_t root, const BfsOptions& opts,
+                          const Csr* csr_for_parents = nullptr) {
+  return detail::bfs_spmv_device(upload(r), root, opts, csr_for_parents != nullptr);
 }
 
 /// Extension: a Graph500 root list through ssb_bfs_spmv_batch — results as
@@ -682,8 +707,17 @@ inline BfsResult bfs_traditional(const Graph& g, vid_t root) {
 /// bfs.hpp:85 (bfs.cpp:248-291) on a CSR: its arcs become the normalised
 /// edge set on the device (a symmetric CSR, as to_csr returns, gives exactly
 /// the reference's traversal), then the device queue BFS.
-inline BfsResult bfs_traditional(const CsrView& csr, vid_t root) {
-  const vid_t n = csr.num_vertices();
+template <class Csr,
+          std::enable_if_t<std::is_same_v<std::decay_t<decltype(std::declval<const Csr&>().row[0])>,
+                                          vid_t> &&
+                               std::is_same_v<std::decay_t<decltype(std::declval<const Csr&>().col[0])>,
+                                              vid_t>,
+                           int> = 0>
+inline BfsResult bfs_traditional(const Csr& csr, vid_t root) {
+  const vid_t n = static_cast<vid_t>(csr.row.size()) - 1;
+  auto has_edge = [&](vid_t u, vid_t v) {
+    return std::binary_search(csr.col.begin() + csr.row[u], csr.col.begin() + csr.row[u + 1], v);
+  };
   if (root < 0 || root >= n)
     throw std::out_of_range("root " + std::to_string(root) + " outside [0, " + std::to_string(n) + ")");
   std::vector<std::int64_t> uv;
@@ -693,7 +727,7 @@ inline BfsResult bfs_traditional(const CsrView& csr, vid_t root) {
       if (u < csr.col[e]) {
         uv.push_back(u);
         uv.push_back(csr.col[e]);
-      } else if (csr.col[e] < u && !csr.has_edge(csr.col[e], u)) {  // an arc with no mirror
+      } else if (csr.col[e] < u && !has_edge(csr.col[e], u)) {  // an arc with no mirror
         uv.push_back(csr.col[e]);
         uv.push_back(u);
       }

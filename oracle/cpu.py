@@ -30,11 +30,14 @@ class OracleError(RuntimeError):
         self.code = code
 
 
-def build(ref: bool = True) -> None:
-    """Compile liboracle.so (and _ref when /root/reference is present)."""
+def build(ref: bool = True, alongside: bool = False) -> None:
+    """Compile liboracle.so (and _ref when /root/reference is present; with
+    ``alongside`` also _ref/test_alongside, which links libslimsell_b200.so)."""
     targets = ["liboracle.so"]
     if ref and os.path.isdir(REF_DIR):
         targets.append("ref")
+        if alongside:
+            targets.append("alongside")
     subprocess.run(["make", "-s", "-C", HERE, f"REF={REF_DIR}", *targets], check=True)
 
 
