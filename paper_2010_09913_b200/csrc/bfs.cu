@@ -1988,7 +1988,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
       else current.push_back({dev, fn, G.smem});
     }
   }
-  r.grid = num_sms();
+  r.grid = std::max(1, std::min(num_sms(), env_int("SSB_GRID", num_sms())));  // A/B: fewer CTAs
 
   Args32& a = r.a;
   a.col = g.col.p;
