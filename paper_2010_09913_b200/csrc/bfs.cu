@@ -66,6 +66,7 @@ constexpr int kStatW = 8;  // int64 per iteration record
 #define SSB_ITERS_PER_LAUNCH 1024  // (1: one launch per iteration, for per-iteration profiles)
 #endif
 constexpr int kItersPerLaunch = SSB_ITERS_PER_LAUNCH;
+constexpr int64_t kRecFirst = 64;  // records returned with every launch (a BFS rarely needs more)
 
 int env_int(const char* name, int def) {
   const char* v = std::getenv(name);
@@ -207,6 +208,10 @@ struct Args32 {
   // start instead of n_tasks / front_in / gone_base, written back at the end;
   // a launch entering with |F| = 0 (the BFS already converged) does nothing.
   int64_t* carry;
+  // Mapped pinned host memory receiving the first min(k_end - k_begin,
+  // kRecFirst) records when the launch ends (CTA 0), or null: the host reads
+  // them after the launch without a copy on the stream.
+  int64_t* rec_host;
 };
 
 // Fused multi-GPU exchange (chunk-range shards): every rank's
@@ -1237,6 +1242,11 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     gone += *reinterpret_cast<volatile unsigned long long*>(&a.gone_chunks[rec]);
     if (front == 0) break;  // is_converged: no row newly reached
   }
+  if (a.rec_host && vb == 0) {  // every CTA's counters landed before the last grid.sync
+    __syncthreads();
+    const int32_t nw = min(a.k_end - a.k_begin, int32_t(kRecFirst)) * kStatW;
+    for (int32_t i = threadIdx.x; i < nw; i += blockDim.x) a.rec_host[i] = __ldcg(a.stats + i);
+  }
   // every CTA read the carry at launch start, before the first grid.sync
   if (a.carry && vb == 0 && threadIdx.x == 0) {
     a.carry[0] = front_in;
@@ -1904,7 +1914,8 @@ uint32_t* p2p_window_alloc(ssb_graph& g, WinGeom& wg) {
 // chunk range [cb, ce) (all chunks for a single-GPU BFS). With a window (a
 // fused multi-GPU shard) the frontier and summaries live in the window.
 Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
-                const std::vector<int64_t>& segs, const P2PHost* p2p = nullptr) {
+                const std::vector<int64_t>& segs, const P2PHost* p2p = nullptr,
+                cudaEvent_t start = nullptr) {
   cudaStream_t s = g.sc.s;
   Run32 r;
   r.sel = o.variant == SSB_SELMAX;
@@ -1954,6 +1965,9 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     ra.gshift = G.gshift;
     ra.level = g.level.p;
     ra.parent = g.parent.p;
+    // the BFS's device interval opens with its first device operation (the
+    // host-side preparation above is not device work)
+    if (start) SSB_CUDA(cudaEventRecord(start, s));
     reset32_kernel<<<num_sms() * 4, 256, 0, s>>>(ra);
     SSB_CUDA(cudaGetLastError());
     g.last_launches += 1;  // reset32_kernel
@@ -2043,6 +2057,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.root_code = root_code;
   a.trace = nullptr;
   a.carry = nullptr;
+  a.rec_host = nullptr;
   static int* trace_buf = nullptr;
   if (std::getenv("SSB_TRACE")) {
     if (!trace_buf) SSB_CUDA(cudaHostAlloc(&trace_buf, 64, cudaHostAllocMapped));
@@ -2060,7 +2075,6 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   for (size_t q = 0; q + 1 < segs.size(); q += 2) owns_rc = owns_rc || (rc >= segs[q] && rc < segs[q + 1]);
   r.z_skip = o.slimwork && owns_rc && g.cl_host[rc] == 0 &&
              std::min<int64_t>(32, g.n - rc * 32) == 1;
-  r.rec.resize(size_t(kItersPerLaunch) * kStatW);
   r.k = 1;
   return r;
 }
@@ -2078,6 +2092,22 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
     SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
   }
   r.zeroed = false;
+  // the launch's first records land in mapped PINNED host memory, written by
+  // the kernel itself as it ends: no copy on the stream after it (a pageable
+  // cudaMemcpyAsync cost ~12 us, a pinned one ~6 us, of a 0.41 ms S22 BFS)
+  struct RecHost {
+    int64_t* p = nullptr;
+    ~RecHost() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  if (!g.rec_host) {
+    auto h = std::make_shared<RecHost>();
+    SSB_CUDA(cudaHostAlloc(&h->p, size_t(kRecFirst) * kStatW * 8, cudaHostAllocMapped | cudaHostAllocPortable));
+    g.rec_host = h;
+  }
+  int64_t* pin = static_cast<RecHost*>(g.rec_host.get())->p;
+  SSB_CUDA(cudaHostGetDevicePointer(&a.rec_host, pin, 0));
   void* params[] = {&a};
   SSB_CUDA(cudaEventRecord(g.sc.e0, s));
   SSB_CUDA(cudaLaunchCooperativeKernel(
@@ -2120,17 +2150,17 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
     SSB_CUDA(cudaMemcpyToSymbol(g_phase, z, sizeof z));
   }
 #endif
-  // the records of the first 64 iterations come back with the launch (a BFS
-  // rarely needs more); the rest only when the launch got that far
+  // the records of the first kRecFirst iterations come back with the launch;
+  // the rest only when the launch got that far
   const int64_t nrec = kend - r.k;
-  const int64_t first = std::min<int64_t>(nrec, 64);
-  SSB_CUDA(cudaMemcpyAsync(r.rec.data(), g.dstats.p, size_t(first) * kStatW * 8,
-                           cudaMemcpyDeviceToHost, s));
+  const int64_t first = std::min<int64_t>(nrec, kRecFirst);
   SSB_CUDA(cudaEventRecord(g.sc.e_end, s));
   // blocking wait (e_end is a blocking-sync event): the host threads widening
   // the previous root's result during a batch keep every core
   SSB_CUDA(cudaEventSynchronize(g.sc.e_end));
+  r.rec.assign(pin, pin + first * kStatW);
   if (nrec > first && r.rec[size_t(first - 1) * kStatW] != 0) {
+    r.rec.resize(size_t(nrec) * kStatW);
     SSB_CUDA(cudaMemcpy(r.rec.data() + first * kStatW, g.dstats.p + first * kStatW,
                         size_t(nrec - first) * kStatW * 8, cudaMemcpyDeviceToHost));
   }
@@ -2175,9 +2205,9 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
 
 // Returns true when converged; appends per-iteration stats.
 bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
-           int64_t cap, std::vector<ssb_iter_stats>& stats) {
+           int64_t cap, std::vector<ssb_iter_stats>& stats, cudaEvent_t start = nullptr) {
   const auto h0 = std::chrono::steady_clock::now();
-  Run32 r = prepare32(g, root_pos, root_code, o, {0, g.n_chunks});
+  Run32 r = prepare32(g, root_pos, root_code, o, {0, g.n_chunks}, nullptr, start);
   if (std::getenv("SSB_GAPS"))
     fprintf(stderr, "[ssb gaps] host prepare32 %.1f us\n",
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
@@ -2334,10 +2364,10 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
   cudaEvent_t t0, t1;
   SSB_CUDA(cudaEventCreate(&t0));
   SSB_CUDA(cudaEventCreate(&t1));
-  SSB_CUDA(cudaEventRecord(t0, g.sc.s));
+  if (g.C != 32) SSB_CUDA(cudaEventRecord(t0, g.sc.s));  // (C = 32: before its first launch)
   bool conv;
   try {
-    conv = g.C == 32 ? run32(g, root_pos, root_code, o, cap, st)
+    conv = g.C == 32 ? run32(g, root_pos, root_code, o, cap, st, t0)
                      : run_generic(g, root_pos, root_code, o, cap, st);
   } catch (...) {
     cudaEventDestroy(t0);
@@ -2347,8 +2377,9 @@ int bfs_run(ssb_graph& g, int64_t root, const ssb_bfs_options& o, ssb_iter_stats
   SSB_CUDA(cudaEventRecord(t1, g.sc.s));
   SSB_CUDA(cudaEventSynchronize(t1));
   // device time: from the first enqueued operation to the end of the last
-  // launch's stats copy — the host's wake-up after that copy is not device work
-  // (t1 bounds it when the engine enqueued nothing that records e_end)
+  // launch (its records land in mapped host memory as it ends) — the host's
+  // wake-up after that is not device work (t1 bounds it when the engine
+  // enqueued nothing that records e_end)
   float ms = 0;
   SSB_CUDA(cudaEventElapsedTime(&ms, t0, g.sc.e_end));
   {

@@ -198,6 +198,7 @@ struct ssb_graph {
   std::shared_ptr<void> geom;   // cached shared-memory image geometry (bfs.cu)
   std::shared_ptr<void> spmv_plan;  // work units of the last spmv_step chunk range (spmv.cu)
   std::shared_ptr<void> gen_plan;   // work units + per-row hit slots of the C != 32 engine (bfs.cu)
+  std::shared_ptr<void> rec_host;   // pinned landing buffer of the launch records (bfs.cu)
 
   ssb::StreamCtx sc;
 };
