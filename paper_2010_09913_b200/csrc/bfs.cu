@@ -1255,8 +1255,58 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
   }
 }
 
+struct ResetArgs {
+  uint4* reg[5];      // visited, F0, S0..S2, stats, control words
+  int64_t n16[5];
+  uint8_t* tskip;
+  int64_t n_tasks;
+  uint32_t* visited;
+  uint32_t* F0;
+  uint32_t* S0;       // null without a summary
+  int32_t root_pos, root_code, PW, gshift;
+  int32_t* level;
+  int32_t* parent;
+  int32_t active;     // bfs32_kernel: reset before the first iteration
+};
+
+// init_state (semiring.cpp:56-88) in 1-bit form over the whole grid: the
+// state regions zeroed, the root's visited / frontier / summary bits set, its
+// level and parent seeded.
+__device__ __forceinline__ void reset_body(const ResetArgs& r) {
+  const int32_t rw = r.root_pos >> 5;
+  const uint32_t rbit = 1u << (r.root_pos & 31);
+  const int32_t sgi = r.S0 && rw >= r.PW ? (rw - r.PW) >> r.gshift : -1;
+  for (int q = 0; q < 5; ++q) {
+    uint4* p = r.reg[q];
+    GRID_STRIDE(i, r.n16[q]) {
+      uint4 z = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t* zw = reinterpret_cast<uint32_t*>(&z);
+      uint32_t* base = reinterpret_cast<uint32_t*>(p + i);
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t* w = base + t;
+        if (w == r.visited + rw || w == r.F0 + rw) zw[t] = rbit;
+        if (sgi >= 0 && w == r.S0 + (sgi >> 5)) zw[t] = 1u << (sgi & 31);
+      }
+      p[i] = z;
+    }
+  }
+  GRID_STRIDE(i, r.n_tasks) r.tskip[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    r.level[r.root_pos] = 0;
+    r.parent[r.root_pos] = r.root_code;
+  }
+}
+
+__global__ void reset32_kernel(const ResetArgs r) { reset_body(r); }
+
+// One single-GPU BFS launch; the first launch of a BFS also does init_state
+// (one launch less per BFS than a separate reset kernel).
 template <bool kSelMax, int kS>
-__global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a) {
+__global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a, const ResetArgs r) {
+  if (r.active) {
+    reset_body(r);
+    cg::this_grid().sync();
+  }
   bfs32_body<kSelMax, kS, false>(a, P2PArgs{}, int(blockIdx.x), int(gridDim.x));
 }
 
@@ -1432,44 +1482,6 @@ __global__ void __launch_bounds__(1024, 1) genc_kernel(const ArgsG a) {
 // zero the 16-byte-aligned regions (visited+F0, the summaries, the stats and
 // control words), the per-task skip flags, and set the root's bits; the
 // thread that zeroes the root's words writes them with the root bit instead.
-struct ResetArgs {
-  uint4* reg[5];      // visited, F0, S0..S2, stats, control words
-  int64_t n16[5];
-  uint8_t* tskip;
-  int64_t n_tasks;
-  uint32_t* visited;
-  uint32_t* F0;
-  uint32_t* S0;       // null without a summary
-  int32_t root_pos, root_code, PW, gshift;
-  int32_t* level;
-  int32_t* parent;
-};
-
-__global__ void reset32_kernel(const ResetArgs r) {
-  const int32_t rw = r.root_pos >> 5;
-  const uint32_t rbit = 1u << (r.root_pos & 31);
-  const int32_t sgi = r.S0 && rw >= r.PW ? (rw - r.PW) >> r.gshift : -1;
-  for (int q = 0; q < 5; ++q) {
-    uint4* p = r.reg[q];
-    GRID_STRIDE(i, r.n16[q]) {
-      uint4 z = make_uint4(0u, 0u, 0u, 0u);
-      uint32_t* zw = reinterpret_cast<uint32_t*>(&z);
-      uint32_t* base = reinterpret_cast<uint32_t*>(p + i);
-      for (int t = 0; t < 4; ++t) {
-        const uint32_t* w = base + t;
-        if (w == r.visited + rw || w == r.F0 + rw) zw[t] = rbit;
-        if (sgi >= 0 && w == r.S0 + (sgi >> 5)) zw[t] = 1u << (sgi & 31);
-      }
-      p[i] = z;
-    }
-  }
-  GRID_STRIDE(i, r.n_tasks) r.tskip[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    r.level[r.root_pos] = 0;
-    r.parent[r.root_pos] = r.root_code;
-  }
-}
-
 __global__ void bytes_to_bits_kernel(const uint8_t* __restrict__ vis, int64_t n_padded,
                                      uint32_t* __restrict__ bits) {
   GRID_STRIDE(w, (n_padded + 31) / 32) {
@@ -1614,7 +1626,7 @@ struct Geometry {
 };
 
 // Summary granularities the kernel is instantiated for.
-using Bfs32Fn = void (*)(const Args32);
+using Bfs32Fn = void (*)(const Args32, const ResetArgs);
 Bfs32Fn bfs32_fn(bool sel, int S) {
   if (S == 6) return sel ? bfs32_kernel<true, 6> : bfs32_kernel<false, 6>;
   return sel ? bfs32_kernel<true, 8> : bfs32_kernel<false, 8>;
@@ -1845,6 +1857,8 @@ struct Run32 {
   uint32_t* task_out = nullptr;
   unsigned long long* gone = nullptr;
   std::vector<int64_t> rec;
+  ResetArgs reset{};             // init_state, done by the first bfs32_kernel launch (reset.active)
+  cudaEvent_t start = nullptr;   // recorded just before that launch (the BFS's device interval)
   bool stepping = false;         // shard mode: always carry state to the next launch
   bool zeroed = false;           // stats/control words already clear for the next launch
   std::vector<int64_t> segs;     // owned chunk segments
@@ -1915,7 +1929,7 @@ uint32_t* p2p_window_alloc(ssb_graph& g, WinGeom& wg) {
 // fused multi-GPU shard) the frontier and summaries live in the window.
 Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
                 const std::vector<int64_t>& segs, const P2PHost* p2p = nullptr,
-                cudaEvent_t start = nullptr) {
+                cudaEvent_t start = nullptr, bool reset_in_kernel = false) {
   cudaStream_t s = g.sc.s;
   Run32 r;
   r.sel = o.variant == SSB_SELMAX;
@@ -1965,12 +1979,18 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     ra.gshift = G.gshift;
     ra.level = g.level.p;
     ra.parent = g.parent.p;
-    // the BFS's device interval opens with its first device operation (the
-    // host-side preparation above is not device work)
-    if (start) SSB_CUDA(cudaEventRecord(start, s));
-    reset32_kernel<<<num_sms() * 4, 256, 0, s>>>(ra);
-    SSB_CUDA(cudaGetLastError());
-    g.last_launches += 1;  // reset32_kernel
+    if (reset_in_kernel) {  // the first bfs32_kernel launch does it (launch32)
+      ra.active = 1;
+      r.reset = ra;
+      r.start = start;
+    } else {
+      // the BFS's device interval opens with its first device operation (the
+      // host-side preparation above is not device work)
+      if (start) SSB_CUDA(cudaEventRecord(start, s));
+      reset32_kernel<<<num_sms() * 4, 256, 0, s>>>(ra);
+      SSB_CUDA(cudaGetLastError());
+      g.last_launches += 1;  // reset32_kernel
+    }
     r.zeroed = true;       // the first launch's stats/control words are clear
   }
 
@@ -2108,13 +2128,16 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
   }
   int64_t* pin = static_cast<RecHost*>(g.rec_host.get())->p;
   SSB_CUDA(cudaHostGetDevicePointer(&a.rec_host, pin, 0));
-  void* params[] = {&a};
+  void* params[] = {&a, &r.reset};
+  if (r.start) SSB_CUDA(cudaEventRecord(r.start, s));
+  r.start = nullptr;
   SSB_CUDA(cudaEventRecord(g.sc.e0, s));
   SSB_CUDA(cudaLaunchCooperativeKernel(
       (const void*)bfs32_fn(r.sel, r.G.S), dim3(r.grid),
       dim3(kThreads), params, r.G.smem, s));
   SSB_CUDA(cudaGetLastError());
   SSB_CUDA(cudaEventRecord(g.sc.e1, s));
+  r.reset.active = 0;  // later launches of this BFS carry the state on
   if (a.trace) {  // debug: poll progress instead of blocking forever
     cudaEvent_t done;
     SSB_CUDA(cudaEventCreate(&done));
@@ -2207,7 +2230,7 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
 bool run32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
            int64_t cap, std::vector<ssb_iter_stats>& stats, cudaEvent_t start = nullptr) {
   const auto h0 = std::chrono::steady_clock::now();
-  Run32 r = prepare32(g, root_pos, root_code, o, {0, g.n_chunks}, nullptr, start);
+  Run32 r = prepare32(g, root_pos, root_code, o, {0, g.n_chunks}, nullptr, start, true);
   if (std::getenv("SSB_GAPS"))
     fprintf(stderr, "[ssb gaps] host prepare32 %.1f us\n",
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
@@ -2797,7 +2820,7 @@ void shard_step_async(ssb_graph& g, uint32_t* owned_words) {
     SSB_CUDA(cudaMemsetAsync(g.dctrl.p, 0, g.dctrl.bytes(), s));
   }
   r.zeroed = false;
-  void* params[] = {&a};
+  void* params[] = {&a, &r.reset};  // (reset.active = 0: begin_async ran the reset kernel)
   SSB_CUDA(cudaLaunchCooperativeKernel((const void*)bfs32_fn(r.sel, r.G.S), dim3(r.grid), dim3(kThreads),
                                        params, r.G.smem, s));
   SSB_CUDA(cudaGetLastError());
