@@ -57,7 +57,7 @@ namespace {
 #ifndef SSB_BFS_THREADS
 #define SSB_BFS_THREADS 1024
 #endif
-constexpr int kThreads = SSB_BFS_THREADS;  // 32 warps: 64 registers, no spills
+constexpr int kThreads = SSB_BFS_THREADS;  // 32 warps, 64 registers (spills: a few words of per-task bookkeeping, none in the column loops)
 constexpr int kUnitsPerTask = 32;
 constexpr int kStatW = 8;  // int64 per iteration record
 // record: 0 frontier_size, 1 chunks_processed, 2 chunks_skipped,
