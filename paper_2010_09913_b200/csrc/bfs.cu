@@ -128,6 +128,25 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
       "r"(phase)
       : "memory");
 }
+#ifndef SSB_BCAST
+#define SSB_BCAST 1  // per-iteration totals read by one thread per CTA and broadcast in shared memory
+#endif
+#ifndef SSB_LAZY_STAGE
+#define SSB_LAZY_STAGE 1  // warps wait for the staged image at their first probe, not before their first task
+#endif
+// The wait for an iteration's staged frontier image, taken once per warp
+// (warp-uniform: every lane of the warp calls it together).
+struct ImgWait {
+  unsigned long long* bar;
+  uint32_t phase;
+  bool ok;
+  __device__ __forceinline__ void operator()() {
+    if (!ok) {
+      mbar_wait(bar, phase);
+      ok = true;
+    }
+  }
+};
 // TMA bulk copy global -> this CTA's shared memory in <= 32 KB pieces
 // (bytes and both addresses 16-byte aligned), completing on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -187,6 +206,7 @@ struct Args32 {
   ssb_tentry* tlist1;
   uint8_t* tskip;      // per task (SSB_TLIST64: per first unit): every unit skipped in its last sweep
   unsigned long long* gone_chunks;  // chunks of retired tasks (skipped forever)
+  int32_t retire_once; // retire a task the first time all its units are skipped (see run_tasks)
   int32_t n_tasks;     // active tasks entering iteration k_begin
   unsigned long long gone_base;  // chunks of tasks retired before k_begin
   int64_t front_in;    // frontier size entering iteration k_begin
@@ -603,7 +623,7 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
 template <bool kSelMax, bool kEarly, bool kDirect, class Probe>
 __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int lane, int lg,
                                            const Probe& pr, uint64_t pol, uint32_t& hit,
-                                           int32_t (&best)[4]) {
+                                           int32_t (&best)[4], ImgWait& iw) {
   const int32_t nv = len * 8, imax = nv - 8 + lg;
   const int32_t nsteps = (nv + 31) >> 5;
   // lanes sharing rows exchange decided-row bits after every 4 steps
@@ -623,6 +643,7 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     int4 v1 = ld_stream(base + min(32 + lane, imax), pol);
     int4 v2 = ld_stream(base + min(64 + lane, imax), pol);
     int4 v3 = ld_stream(base + min(96 + lane, imax), pol);
+    iw();  // the image is needed from the first probe on
     // Steps s+4..s+7 are all full (no clamping) while s + 9 <= nsteps; the
     // prefetch pointer then advances by 2 KB per 4 steps, offsets immediate.
     const int4* pf = base + 128 + lane;
@@ -669,6 +690,7 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
     int4 v1 = ld_stream(at(top - 1), pol);
     int4 v2 = ld_stream(at(top - 2), pol);
     int4 v3 = ld_stream(at(top - 3), pol);
+    iw();
     // steps top-r-4 .. top-r-7 are all full and >= 0 while r + 8 <= nsteps
     const int4* pf = base + 32 * (top - 4) + lane;
     int32_t r = 0;
@@ -732,13 +754,14 @@ __device__ __forceinline__ int32_t sweep_long(const int4* base, int32_t len, int
 template <bool kSelMax, bool kEarly, bool kDirect, class Probe>
 __device__ __forceinline__ int32_t sweep_group(const int4* p, int32_t jlast, int64_t stride,
                                             int32_t maxlen, const Probe& pr, uint64_t pol,
-                                            uint32_t& hit, int32_t (&best)[4]) {
+                                            uint32_t& hit, int32_t (&best)[4], ImgWait& iw) {
   constexpr bool kBack = kSelMax && kEarly;
   auto at = [&](int32_t j) { return p + (kBack ? max(jlast - j, 0) : min(j, jlast)) * stride; };
   int4 v0 = ld_stream(at(0), pol);
   int4 v1 = ld_stream(at(1), pol);
   int4 v2 = ld_stream(at(2), pol);
   int4 v3 = ld_stream(at(3), pol);
+  iw();
   int32_t j = 0;
   while (j < maxlen) {
     const bool more = j + 4 < maxlen;  // warp-uniform
@@ -835,12 +858,15 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
   __shared__ __align__(8) unsigned long long stage_bar_storage;
   unsigned long long* stage_bar = &stage_bar_storage;
   uint32_t stage_phase = 0;
+  __shared__ unsigned long long blk[6];  // stats slots 0-4 and 6
+  __shared__ int64_t bcast[3];           // the iteration's |newly|, kept tasks, retired chunks
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(stage_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    smem_v4[0] = make_uint4(0u, 0u, 0u, 0u);  // the zero words in front of the image (never staged over)
   }
+  if (threadIdx.x < 6) blk[threadIdx.x] = 0ull;
   __syncthreads();
-  __shared__ unsigned long long blk[6];  // stats slots 0-4 and 6
 
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
@@ -887,7 +913,6 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     // waits on the barrier's phase.
     {
       if (threadIdx.x == 0) {
-        smem_v4[0] = make_uint4(0u, 0u, 0u, 0u);
         // prior generic accesses (reads of the previous image, other CTAs'
         // frontier stores ordered by grid.sync) before the async-proxy copies
         asm volatile("fence.proxy.async;" ::: "memory");
@@ -899,11 +924,18 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       // clear the summary buffer of iteration k+1 (last read at k-1)
       for (int i = vb * kThreads + threadIdx.x; i < a.SW; i += nvb * kThreads)
         Sx[i] = 0u;
-      if (threadIdx.x < 6) blk[threadIdx.x] = 0ull;
     }
+#if SSB_LAZY_STAGE
+    // The copies land while the warps take their first tasks (task entry,
+    // unit, cs and visited loads, the first col loads): each warp waits at
+    // its first probe. blk was cleared at the end of the previous iteration.
+    ImgWait iw{stage_bar, stage_phase, false};
+#else
     mbar_wait(stage_bar, stage_phase);
-    stage_phase ^= 1u;
     __syncthreads();
+    ImgWait iw{stage_bar, stage_phase, true};
+#endif
+    stage_phase ^= 1u;
 #ifdef SSB_PHASES
     if (vb == 0 && threadIdx.x == 0) ph1 = globaltimer();
 #endif
@@ -914,10 +946,10 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     const Probe<kS> pr{sm + 4, Fc, img_words * 32, a.PW * 32 - ((a.PW * 32) >> kS)};
 
     // Active task list: iteration 1 walks every task; later iterations only the
-    // tasks kept by the previous one. A task whose units were all skipped in
-    // two consecutive iterations (so both frontier buffers hold zeros for its
-    // chunks) is retired: SlimWork would skip it forever, and its chunks are
-    // counted as skipped through gone_chunks.
+    // tasks kept by the previous one. A task whose units were all skipped
+    // (a.retire_once; else: in two consecutive iterations, so both frontier
+    // buffers hold zeros for its chunks) is retired: SlimWork would skip it
+    // forever, and its chunks are counted as skipped through gone_chunks.
     const ssb_tentry* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
     ssb_tentry* list_out = (k & 1) ? a.tlist1 : a.tlist0;
     auto run_tasks = [&](auto early_tag, auto direct_tag) {
@@ -1053,7 +1085,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         const uint32_t firsts = __ballot_sync(0xffffffffu, has && U.col_begin == 0);
         if (!kBuf) {
           if (lane == 0 && sub == 0) {
-            if (a.slimwork && all_skipped && a.tskip[t_skip]) {
+            if (a.slimwork && all_skipped && (a.retire_once || a.tskip[t_skip])) {
               atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
             } else {
               list_out[atomicAdd(&a.task_out[rec], 1u)] = t_entry;
@@ -1062,7 +1094,8 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
           }
         } else if (sub == 0) {
           const bool retire = a.slimwork && all_skipped &&
-                              __shfl_sync(0xffffffffu, lane == 0 ? a.tskip[t_skip] : 0, 0);
+                              (a.retire_once ||
+                               __shfl_sync(0xffffffffu, lane == 0 ? a.tskip[t_skip] : 0, 0));
           if (retire) {
             if (lane == 0) atomicAdd(&a.gone_chunks[rec], (unsigned long long)__popc(firsts));
           } else {
@@ -1102,7 +1135,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         // padding) marked decided: their probes are skipped
         uint32_t hit = kEarly ? ((uvis | ~ureal) >> (4 * lg)) & 0xfu : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
-        const int32_t sw = sweep_long<kSelMax, kEarly, kDirect>(base, len, lane, lg, pr, pol, hit, best);
+        const int32_t sw = sweep_long<kSelMax, kEarly, kDirect>(base, len, lane, lg, pr, pol, hit, best, iw);
         if (lane == 0) c_swept += uint32_t(sw);
         uint32_t m = hit << (4 * lg);
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
@@ -1169,7 +1202,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         // (a group without a unit counts as decided)
         uint32_t hit = kEarly ? (src < 0 ? 0xfu : ((uvis | ~ureal) >> (4 * lg)) & 0xfu) : 0u;
         int32_t best[4] = {-1, -1, -1, -1};
-        const int32_t ran = sweep_group<kSelMax, kEarly, kDirect>(p, jlast, stride, maxlen, pr, pol, hit, best);
+        const int32_t ran = sweep_group<kSelMax, kEarly, kDirect>(p, jlast, stride, maxlen, pr, pol, hit, best, iw);
         if (lg == 0) c_swept += uint32_t(min(len, ran));
         // 32-bit row mask of the unit (rows 4*lg+q)
         uint32_t m = hit << (4 * lg);
@@ -1185,6 +1218,9 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     if (direct) run_tasks(std::true_type{}, std::true_type{});
     else if (dense) run_tasks(std::true_type{}, std::false_type{});
     else run_tasks(std::false_type{}, std::false_type{});
+    // every warp has seen this phase complete before thread 0 re-arms the
+    // barrier for the next iteration (warps without a sweep wait here)
+    iw();
 
     // -- iteration counters: warp -> block -> grid --------------------------
 #pragma unroll
@@ -1205,10 +1241,12 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       atomicAdd(&blk[5], (unsigned long long)c_swept);
     }
     __syncthreads();
-    if (threadIdx.x < 6)
+    if (threadIdx.x < 6) {
       atomicAdd(reinterpret_cast<unsigned long long*>(
                     &a.stats[rec * kStatW + (threadIdx.x < 5 ? threadIdx.x : 6)]),
                 blk[threadIdx.x]);
+      blk[threadIdx.x] = 0ull;  // the next adds come after grid.sync
+    }
     if (threadIdx.x == 0 && a.trace) atomicAdd(&a.trace[2], 1);
 #ifdef SSB_PHASES
     if (vb == 0 && threadIdx.x == 0) ph2 = globaltimer();
@@ -1224,7 +1262,20 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     }
 #endif
     if (vb == 0 && threadIdx.x == 0) TRACE(1, 4);
+#if SSB_BCAST
+    // the iteration's totals are read once per CTA and broadcast: uniform
+    // volatile loads from every warp of the grid would queue 4736 requests
+    // per word at one L2 slice
+    if (threadIdx.x == 0) {
+      bcast[0] = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+      bcast[1] = int64_t(*reinterpret_cast<volatile uint32_t*>(&a.task_out[rec]));
+      bcast[2] = int64_t(*reinterpret_cast<volatile unsigned long long*>(&a.gone_chunks[rec]));
+    }
+    __syncthreads();
+    int64_t front = bcast[0];
+#else
     int64_t front = *reinterpret_cast<volatile int64_t*>(&a.stats[rec * kStatW]);
+#endif
     if (kP2P) {
       if (vb == 0 && threadIdx.x == 0) TRACE(1, 5);
       front = p2p_exchange(x, k, Fn, Sn, front, x.gen_base + 2 + uint32_t(rec), vb, nvb);
@@ -1232,14 +1283,22 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       if (vb == 0 && threadIdx.x == 0) a.stats[rec * kStatW + 7] = front;  // global |newly|
     }
     front_in = front;
+#if SSB_BCAST
+    n_in = int32_t(bcast[1]);
+#else
     n_in = int32_t(*reinterpret_cast<volatile uint32_t*>(&a.task_out[rec]));
+#endif
     if (vb == 0 && threadIdx.x == 0) {
       const uint64_t t = globaltimer();
       a.stats[rec * kStatW + 5] = int64_t(t - t_prev);
       a.stats[rec * kStatW + 2] += int64_t(gone);  // retired tasks' chunks: skipped
       t_prev = t;
     }
+#if SSB_BCAST
+    gone += static_cast<unsigned long long>(bcast[2]);
+#else
     gone += *reinterpret_cast<volatile unsigned long long*>(&a.gone_chunks[rec]);
+#endif
     if (front == 0) break;  // is_converged: no row newly reached
   }
   if (a.rec_host && vb == 0) {  // every CTA's counters landed before the last grid.sync
@@ -2049,6 +2108,15 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.tlist0 = reinterpret_cast<ssb_tentry*>(g.plan.tlist.p);
   a.tlist1 = a.tlist0 + g.plan.n_tasks;
   a.tskip = g.plan.tskip.p;
+  // A task may retire the first time all its units are skipped: its chunks'
+  // words in the other frontier buffer then keep the bits of the iteration
+  // before (the rows reached last), never cleared. Those bits are harmless to
+  // the sweeps — every row with one of those vertices among its cells was
+  // reached in the iteration that read them, so later probes that see them
+  // belong to visited (decided, masked) rows — but not to anything that
+  // counts or gathers frontier WORDS: the NCCL shard exchange (front_count /
+  // summary_from_words kernels) keeps the two-iteration rule.
+  a.retire_once = env_int("SSB_RETIRE_ONCE", 1) ? 1 : 0;
   a.n_tasks = int32_t(g.plan.n_tasks);
   a.gone_base = 0;
   a.front_in = 1;  // F_0 = {root}
@@ -2733,6 +2801,7 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
   g.last_launches = 0;
   g.last_swept = 0;
   st->r = prepare32(g, root_pos, root_code, o, {cb, ce});
+  st->r.a.retire_once = 0;  // the exchange counts and summarises frontier words
   st->r.stepping = true;
   owned_mask(g, st->r.segs, st->owned);
   st->o = o;
