@@ -207,6 +207,12 @@ struct Args32 {
   uint8_t* tskip;      // per task (SSB_TLIST64: per first unit): every unit skipped in its last sweep
   unsigned long long* gone_chunks;  // chunks of retired tasks (skipped forever)
   int32_t retire_once; // retire a task the first time all its units are skipped (see run_tasks)
+  int32_t hash_on;     // sparse iterations also build the hashed summary (Probe kHash), used next
+  uint32_t HB;         // hashed summary bits (SW * 32)
+  int64_t hash_thr;    // early-exit iterations probe the hashed summary while |F_{k-1}| <= this
+  uint32_t* H0;        // hashed summaries, rotating like S0..S2
+  uint32_t* H1;
+  uint32_t* H2;
   int32_t n_tasks;     // active tasks entering iteration k_begin
   unsigned long long gone_base;  // chunks of tasks retired before k_begin
   int64_t front_in;    // frontier size entering iteration k_begin
@@ -285,17 +291,34 @@ struct GroupArgs {
 // S is chosen per graph (geometry32): 8 when the prefix holds most cell
 // targets (hub-heavy graphs), 6 — a 4x finer summary at the cost of prefix —
 // when it does not (low-skew graphs such as Erdős–Rényi).
-template <int kS>
+//
+// kHash (hub-heavy graphs, iterations after a sparse one): the summary holds
+// one bit per tail frontier VERTEX at a multiplicative hash of its position
+// instead of one bit per 2^S-vertex group. Frontier vertices and cell targets
+// crowd the same low tail positions (both degree-weighted), so group bits are
+// set where the probes land: at S26 iteration 3 a hashed summary of the same
+// size is set for 5-9x fewer open tail cells (scripts/summary_fp.py). A set
+// bit still only sends the cell to its exact word: no false negatives.
+__device__ __forceinline__ uint32_t summary_hash(int32_t pos, uint32_t bits) {
+  return __umulhi(uint32_t(pos) * 0x9E3779B1u, bits);  // Fibonacci hash into [0, bits)
+}
+
+template <int kS, bool kHash = false>
 struct Probe {
   static constexpr int kShift = kS;
   const uint32_t* sm;  // word 0 = first prefix word; sm[-4..-1] are zero
   const uint32_t* Fc;  // the full frontier in global memory
   int32_t P;           // prefix vertices (multiple of 2^S)
-  int32_t Pt;          // P - (P >> S)
+  int32_t Pt;          // P - (P >> S); kHash: the summary's bit count
 
+  // virtual bit of cell target c (padding c = -1 maps to a zero word)
+  __device__ __forceinline__ int32_t vidx(int32_t c) const {
+    if constexpr (kHash) return c < P ? c : P + int32_t(summary_hash(c, uint32_t(Pt)));
+    else return min(c, (c >> kS) + Pt);
+  }
   // the probe's word rotated so that its bit sits at bit 0
   __device__ __forceinline__ uint32_t vrot(int32_t c) const {
-    const int32_t v = min(c, (c >> kS) + Pt);
+    const int32_t v = vidx(c);
     const uint32_t word = sm[v >> 5];
     return __funnelshift_r(word, word, v);  // bit (v mod 32) -> bit 0
   }
@@ -308,7 +331,7 @@ struct Probe {
     int32_t v[4];
     uint32_t w[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = min(c[q], (c[q] >> kS) + Pt);
+    for (int q = 0; q < 4; ++q) v[q] = vidx(c[q]);
     const uint32_t base = uint32_t(__cvta_generic_to_shared(sm));
     asm volatile(
         "ld.shared.u32 %0, [%4];\n\t"
@@ -409,7 +432,7 @@ __device__ __forceinline__ void take_cells_lean(const int4 v, const Probe& pr, u
   const int32_t c[4] = {v.x, v.y, v.z, v.w};
   int32_t vq[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) vq[q] = min(c[q], (c[q] >> Probe::kShift) + pr.Pt);
+  for (int q = 0; q < 4; ++q) vq[q] = pr.vidx(c[q]);
   uint32_t w[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) w[q] = pr.sm[vq[q] >> 5];  // shared image (padding: the zero words)
@@ -548,7 +571,7 @@ constexpr int32_t kWarpUnitCols = SSB_WARP_UNIT_COLS;  // units at least this lo
 // SlimChunk combine (bfs.cpp:205-220): partial results of a split chunk meet
 // in a scratch slot and the unit that arrives last finalises the chunk —
 // post_process_rows (semiring.cpp:90-124) in 1-bit form.
-template <bool kSelMax>
+template <bool kSelMax, bool kEarly, bool kHash>
 __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t* Fn, uint32_t* Sn,
                                             bool valid, int32_t chunk, int32_t split, uint32_t uvis,
                                             uint32_t ureal, uint32_t m, int32_t (&best)[4], int grp,
@@ -605,6 +628,14 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
           const int64_t row = int64_t(chunk) * 32 + r;
           a.level[row] = k;
           if (kSelMax) a.parent[row] = k == 1 ? a.root_code : best[q];
+          // sparse iterations also build the hashed summary of the tail
+          // frontier (the pointer comes from the parameter space: nothing
+          // extra stays live through the sweep)
+          if (kHash && !kEarly && chunk >= a.PW) {
+            uint32_t* Hn = (k % 3) == 0 ? a.H0 : ((k % 3) == 1 ? a.H1 : a.H2);
+            const uint32_t h = summary_hash(int32_t(row), a.HB);
+            atomicOr(&Hn[h >> 5], 1u << (h & 31));
+          }
         }
       }
     }
@@ -849,7 +880,7 @@ __device__ __forceinline__ int64_t p2p_exchange(const P2PArgs& x, int32_t k, con
 
 // The BFS loop of one rank. vb / nvb: this CTA's index and the CTA count of
 // the rank (the whole grid, except when ranks are emulated in one launch).
-template <bool kSelMax, int kS, bool kP2P>
+template <bool kSelMax, int kS, bool kP2P, bool kHash>
 __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, const int vb,
                                            const int nvb) {
   extern __shared__ uint4 smem_v4[];
@@ -887,6 +918,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
   }
   // every rank has reset its window before anyone stores into it
   if (kP2P) p2p_barrier(x, x.gen_base + 1);
+  bool hash_prev = false;  // the previous iteration (in this launch) built the hashed summary
 
   for (int32_t k = a.k_begin; k < a.k_end; ++k) {
     const int32_t rec = k - a.k_begin;
@@ -900,6 +932,8 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     const uint32_t* Sc = km3 == 0 ? a.S0 : (km3 == 1 ? a.S1 : a.S2);
     uint32_t* Sn = (k % 3) == 0 ? a.S0 : ((k % 3) == 1 ? a.S1 : a.S2);
     uint32_t* Sx = ((k + 1) % 3) == 0 ? a.S0 : (((k + 1) % 3) == 1 ? a.S1 : a.S2);
+    const uint32_t* Hc = km3 == 0 ? a.H0 : (km3 == 1 ? a.H1 : a.H2);
+    uint32_t* Hx = ((k + 1) % 3) == 0 ? a.H0 : (((k + 1) % 3) == 1 ? a.H1 : a.H2);
 
     // sweep mode of this iteration (grid-uniform, from |F_{k-1}|): dense ->
     // early exit; dense and direct -> summary-free probes, whose image is the
@@ -907,6 +941,11 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     const bool dense = front_in > a.dense_thr;
     const bool direct = dense && front_in > a.direct_thr;
     const int32_t img_words = direct ? a.PW + a.SW : a.PW;
+    // hashed summary (hub-heavy graphs): built by sparse iterations (whose
+    // output frontier is small enough for one atomic per tail vertex), probed
+    // by the next one unless it probes exactly; the block summary is always
+    // built, so a launch starting mid-BFS simply uses it
+    const bool use_hash = kHash && hash_prev && dense && !direct && front_in <= a.hash_thr;
     // -- stage the frontier prefix and the summary into shared memory -------
     // One thread issues TMA bulk copies (global -> shared, completion on an
     // mbarrier); everyone else goes on to the per-iteration setup and then
@@ -919,11 +958,13 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         const uint32_t bytes_p = uint32_t(img_words) * 4u, bytes_s = direct ? 0u : uint32_t(a.SW) * 4u;
         mbar_arrive_expect_tx(stage_bar, bytes_p + bytes_s);
         bulk_g2s(sm + 4, Fc, bytes_p, stage_bar);
-        if (bytes_s) bulk_g2s(summ, Sc, bytes_s, stage_bar);
+        if (bytes_s) bulk_g2s(summ, use_hash ? Hc : Sc, bytes_s, stage_bar);
       }
-      // clear the summary buffer of iteration k+1 (last read at k-1)
-      for (int i = vb * kThreads + threadIdx.x; i < a.SW; i += nvb * kThreads)
+      // clear the summary buffers of iteration k+1 (last read at k-1)
+      for (int i = vb * kThreads + threadIdx.x; i < a.SW; i += nvb * kThreads) {
         Sx[i] = 0u;
+        if (kHash) Hx[i] = 0u;
+      }
     }
 #if SSB_LAZY_STAGE
     // The copies land while the warps take their first tasks (task entry,
@@ -943,7 +984,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
 
     // per-warp counters of this iteration (a warp's share fits 32 bits)
     uint32_t c_front = 0, c_proc = 0, c_skip = 0, c_sub = 0, c_cols = 0, c_swept = 0;
-    const Probe<kS> pr{sm + 4, Fc, img_words * 32, a.PW * 32 - ((a.PW * 32) >> kS)};
+    const Probe<kS> prb{sm + 4, Fc, img_words * 32, a.PW * 32 - ((a.PW * 32) >> kS)};
 
     // Active task list: iteration 1 walks every task; later iterations only the
     // tasks kept by the previous one. A task whose units were all skipped
@@ -952,7 +993,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     // forever, and its chunks are counted as skipped through gone_chunks.
     const ssb_tentry* list_in = ((k - 1) & 1) ? a.tlist1 : a.tlist0;
     ssb_tentry* list_out = (k & 1) ? a.tlist1 : a.tlist0;
-    auto run_tasks = [&](auto early_tag, auto direct_tag) {
+    auto run_tasks = [&](auto early_tag, auto direct_tag, const auto& pr) {
     constexpr bool kEarly = decltype(early_tag)::value;
     constexpr bool kDirect = decltype(direct_tag)::value;
     // each warp's first task is its global warp id; the rest come from the
@@ -1141,7 +1182,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         m |= __shfl_xor_sync(0xffffffffu, m, 1);
         m |= __shfl_xor_sync(0xffffffffu, m, 2);
         m |= __shfl_xor_sync(0xffffffffu, m, 4);
-        finish_unit<kSelMax>(a, k, Fn, Sn, grp == 0, chunk, split, uvis, ureal, m, best, grp, lg,
+        finish_unit<kSelMax, kEarly, kHash>(a, k, Fn, Sn, grp == 0, chunk, split, uvis, ureal, m, best, grp, lg,
                              gmask, c_front);
       }
 
@@ -1210,14 +1251,26 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
         m |= __shfl_xor_sync(0xffffffffu, m, 2);
         m |= __shfl_xor_sync(0xffffffffu, m, 4);
 
-        finish_unit<kSelMax>(a, k, Fn, Sn, src >= 0, chunk, split, uvis, ureal, m, best, grp, lg,
+        finish_unit<kSelMax, kEarly, kHash>(a, k, Fn, Sn, src >= 0, chunk, split, uvis, ureal, m, best, grp, lg,
                              gmask, c_front);
       }
     }
     };  // run_tasks
-    if (direct) run_tasks(std::true_type{}, std::true_type{});
-    else if (dense) run_tasks(std::true_type{}, std::false_type{});
-    else run_tasks(std::false_type{}, std::false_type{});
+    if (direct) {
+      run_tasks(std::true_type{}, std::true_type{}, prb);
+    } else if (use_hash) {
+      if constexpr (kHash) {
+        const Probe<kS, true> prh{sm + 4, Fc, img_words * 32, int32_t(a.HB)};
+        run_tasks(std::true_type{}, std::false_type{}, prh);  // (use_hash implies dense)
+      }
+    } else if (dense) {
+      run_tasks(std::true_type{}, std::false_type{}, prb);
+    } else {
+      run_tasks(std::false_type{}, std::false_type{}, prb);
+    }
+    // this (sparse) iteration built the hashed summary (recomputed here from
+    // loop state rather than kept live through the sweep)
+    hash_prev = kHash && !(front_in > a.dense_thr);
     // every warp has seen this phase complete before thread 0 re-arms the
     // barrier for the next iteration (warps without a sweep wait here)
     iw();
@@ -1360,13 +1413,13 @@ __global__ void reset32_kernel(const ResetArgs r) { reset_body(r); }
 
 // One single-GPU BFS launch; the first launch of a BFS also does init_state
 // (one launch less per BFS than a separate reset kernel).
-template <bool kSelMax, int kS>
+template <bool kSelMax, int kS, bool kHash>
 __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a, const ResetArgs r) {
   if (r.active) {
     reset_body(r);
     cg::this_grid().sync();
   }
-  bfs32_body<kSelMax, kS, false>(a, P2PArgs{}, int(blockIdx.x), int(gridDim.x));
+  bfs32_body<kSelMax, kS, false, kHash>(a, P2PArgs{}, int(blockIdx.x), int(gridDim.x));
 }
 
 // Chunk-range shard of a multi-GPU BFS with the frontier exchange fused in:
@@ -1374,12 +1427,12 @@ __global__ void __launch_bounds__(kThreads, 1) bfs32_kernel(const Args32 a, cons
 // one cooperative launch (bfs32p_kernel, rank = blockIdx.x / nvb).
 template <bool kSelMax, int kS>
 __global__ void __launch_bounds__(kThreads, 1) bfs32x_kernel(const Args32 a, const P2PArgs x) {
-  bfs32_body<kSelMax, kS, true>(a, x, int(blockIdx.x), int(gridDim.x));
+  bfs32_body<kSelMax, kS, true, false>(a, x, int(blockIdx.x), int(gridDim.x));
 }
 template <bool kSelMax, int kS>
 __global__ void __launch_bounds__(kThreads, 1) bfs32p_kernel(const __grid_constant__ GroupArgs ga) {
   const int vr = int(blockIdx.x) / ga.nvb;
-  bfs32_body<kSelMax, kS, true>(ga.a[vr], ga.x[vr], int(blockIdx.x) - vr * ga.nvb, ga.nvb);
+  bfs32_body<kSelMax, kS, true, false>(ga.a[vr], ga.x[vr], int(blockIdx.x) - vr * ga.nvb, ga.nvb);
 }
 
 // ---- generic engine (any C) ------------------------------------------------
@@ -1686,9 +1739,12 @@ struct Geometry {
 
 // Summary granularities the kernel is instantiated for.
 using Bfs32Fn = void (*)(const Args32, const ResetArgs);
-Bfs32Fn bfs32_fn(bool sel, int S) {
-  if (S == 6) return sel ? bfs32_kernel<true, 6> : bfs32_kernel<false, 6>;
-  return sel ? bfs32_kernel<true, 8> : bfs32_kernel<false, 8>;
+// hashed: the S = 8 engine that also builds / probes the hashed summary (a
+// separate instantiation, so graphs without it run the leaner kernel)
+Bfs32Fn bfs32_fn(bool sel, int S, bool hashed) {
+  if (S == 6) return sel ? bfs32_kernel<true, 6, false> : bfs32_kernel<false, 6, false>;
+  if (hashed) return sel ? bfs32_kernel<true, 8, true> : bfs32_kernel<false, 8, true>;
+  return sel ? bfs32_kernel<true, 8, false> : bfs32_kernel<false, 8, false>;
 }
 
 Geometry geometry32_for(const ssb_graph& g, int S) {
@@ -1857,20 +1913,23 @@ void build_plan32(ssb_graph& g, int64_t L, const std::vector<int64_t>& segs) {
 // bits layout: visited | F0 | F1 | S0 | S1 | S2 (each region 16-byte aligned)
 struct BitRegions {
   int64_t NW4, SW4;
-  uint32_t *visited, *F0, *F1, *S0, *S1, *S2;
+  uint32_t *visited, *F0, *F1, *S0, *S1, *S2, *H0, *H1, *H2;
 };
 
 BitRegions bit_regions(ssb_graph& g, int64_t SW) {
   BitRegions R;
   R.NW4 = ((g.n_padded + 31) / 32 + 3) & ~int64_t(3);
   R.SW4 = std::max<int64_t>((SW + 3) & ~int64_t(3), 4);
-  g.bits.ensure(size_t(3 * R.NW4 + 3 * R.SW4));
+  g.bits.ensure(size_t(3 * R.NW4 + 6 * R.SW4));
   R.visited = g.bits.p;
   R.F0 = R.visited + R.NW4;
   R.F1 = R.F0 + R.NW4;
   R.S0 = R.F1 + R.NW4;
   R.S1 = R.S0 + R.SW4;
   R.S2 = R.S1 + R.SW4;
+  R.H0 = R.S2 + R.SW4;  // hashed summaries (contiguous with S0..S2: one reset region)
+  R.H1 = R.H0 + R.SW4;
+  R.H2 = R.H1 + R.SW4;
   return R;
 }
 
@@ -1909,6 +1968,7 @@ struct Run32 {
   Args32 a;
   Geometry G;
   bool sel = false;
+  bool hashed = false;           // the hashed-summary kernel (Args32::hash_on)
   int grid = 0;
   int64_t k = 1;                 // next iteration
   int32_t root_pos = 0;
@@ -1986,9 +2046,29 @@ uint32_t* p2p_window_alloc(ssb_graph& g, WinGeom& wg) {
 // init_state (semiring.cpp:56-88) in 1-bit form + kernel arguments for the
 // chunk range [cb, ce) (all chunks for a single-GPU BFS). With a window (a
 // fused multi-GPU shard) the frontier and summaries live in the window.
+// |F_{k-1}| above which an iteration sweeps with early exit.
+int64_t dense_threshold(const ssb_graph& g, const Geometry& G, bool hashed) {
+  // Early-exit sweeps pay off once rows get decided quickly: on hub-heavy
+  // graphs (most probes land in the shared prefix) from |F| > n/4096 on; on
+  // low-skew graphs from |F| > n/128 (A/B on config 3 and config 4: the
+  // batched exact lookups of the early-exit sweep win once the summary is
+  // mostly set, even when few rows exit early).
+  const bool hubby = G.S == 8;
+  // (hub-heavy: n/8192 since the mask-form early-exit step; A/B at S26 /
+  // S22 over 64 roots: 4096 4.455 / 0.434, 8192 4.420 / 0.434, 16384
+  // 4.411 / 0.437 ms per BFS)
+  // With hashed probes the early exit pays from smaller frontiers on (S26
+  // iteration 3 of the |F_2| < 8K roots: their block summary bits were ~99%
+  // false positives, the hashed ones are set for ~0.6% of the open cells):
+  // n/32768 (A/B at S26, 16 roots: 4.234 -> 4.205-4.215 ms per BFS).
+  const int hub_div = env_int("SSB_DENSE_DIV_HUB", hashed ? 32768 : 8192);
+  const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? hub_div : 128));
+  return std::max<int64_t>(1, g.n / div);
+}
+
 Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs_options& o,
                 const std::vector<int64_t>& segs, const P2PHost* p2p = nullptr,
-                cudaEvent_t start = nullptr, bool reset_in_kernel = false) {
+                cudaEvent_t start = nullptr, bool reset_in_kernel = false, bool allow_hash = true) {
   cudaStream_t s = g.sc.s;
   Run32 r;
   r.sel = o.variant == SSB_SELMAX;
@@ -1997,6 +2077,12 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   r.segs = segs;
   r.G = cached_geometry(g);
   const Geometry& G = r.G;
+  // hashed summaries on hub-heavy graphs (S = 8) with a summary of >= 64K
+  // bits (S22's 16K-bit summary is saturated by the frontiers that reach it
+  // either way); not where summary words are exchanged between ranks (p2p
+  // windows, NCCL shards: allow_hash = false)
+  r.hashed = allow_hash && !p2p && G.S == 8 && int64_t(G.SW) * 32 >= 65536 &&
+             env_int("SSB_HASH_SUMMARY", 1) != 0;
   BitRegions R = bit_regions(g, G.SW);
   if (p2p) {
     uint32_t* w = p2p->win[p2p->rank];
@@ -2021,8 +2107,8 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     ra.n16[0] = R.NW4 / 4;
     ra.reg[1] = reinterpret_cast<uint4*>(R.F0);
     ra.n16[1] = R.NW4 / 4;
-    ra.reg[2] = reinterpret_cast<uint4*>(R.S0);       // S0..S2 (contiguous)
-    ra.n16[2] = 3 * R.SW4 / 4;
+    ra.reg[2] = reinterpret_cast<uint4*>(R.S0);       // S0..S2, H0..H2 (contiguous)
+    ra.n16[2] = (p2p ? 3 : 6) * R.SW4 / 4;            // (peer windows hold S only; no hashing there)
     ra.reg[3] = reinterpret_cast<uint4*>(g.dstats.p);  // the first launch's records
     ra.n16[3] = int64_t(g.dstats.bytes() / 16);
     ra.reg[4] = reinterpret_cast<uint4*>(g.dctrl.p);   // and control words
@@ -2066,7 +2152,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
     static std::vector<Cfg> current;
     int dev = 0;
     SSB_CUDA(cudaGetDevice(&dev));
-    const Bfs32Fn fn = bfs32_fn(r.sel, G.S);
+    const Bfs32Fn fn = bfs32_fn(r.sel, G.S, r.hashed);
     std::lock_guard<std::mutex> lock(mu);
     Cfg* c = nullptr;
     for (Cfg& x : current)
@@ -2099,6 +2185,17 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.S0 = R.S0;
   a.S1 = R.S1;
   a.S2 = R.S2;
+  a.H0 = R.H0;
+  a.H1 = R.H1;
+  a.H2 = R.H2;
+  a.HB = uint32_t(G.SW) * 32u;
+  a.hash_on = r.hashed ? 1 : 0;  // (see r.hashed)
+  {
+    // A/B at S26 over 16 roots: HB / 2 4.234, HB 4.205-4.215 ms per BFS
+    // (with the n/32768 dense threshold below), no hashing 4.271
+    const int64_t ht = env_int("SSB_HASH_THR", -1);
+    a.hash_thr = ht >= 0 ? ht : int64_t(a.HB);
+  }
   a.level = g.level.p;
   a.parent = g.parent.p;
   a.stats = g.dstats.p;
@@ -2121,17 +2218,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.gone_base = 0;
   a.front_in = 1;  // F_0 = {root}
   {
-    // Early-exit sweeps pay off once rows get decided quickly: on hub-heavy
-    // graphs (most probes land in the shared prefix) from |F| > n/4096 on; on
-    // low-skew graphs from |F| > n/128 (A/B on config 3 and config 4: the
-    // batched exact lookups of the early-exit sweep win once the summary is
-    // mostly set, even when few rows exit early).
-    const bool hubby = G.S == 8;
-    // (hub-heavy: n/8192 since the mask-form early-exit step; A/B at S26 /
-    // S22 over 64 roots: 4096 4.455 / 0.434, 8192 4.420 / 0.434, 16384
-    // 4.411 / 0.437 ms per BFS)
-    const int div = std::max(1, env_int("SSB_DENSE_DIV", hubby ? 8192 : 128));
-    a.dense_thr = std::max<int64_t>(1, g.n / div);
+    a.dense_thr = dense_threshold(g, G, a.hash_on != 0);
     // once |F| exceeds the summary's bits most of them are set: probe exactly
     const int64_t dt = env_int("SSB_DIRECT_THR", -1);
     a.direct_thr = dt >= 0 ? dt : (G.SW > 0 ? int64_t(G.SW) * 32 : INT64_MAX);
@@ -2201,7 +2288,7 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
   r.start = nullptr;
   SSB_CUDA(cudaEventRecord(g.sc.e0, s));
   SSB_CUDA(cudaLaunchCooperativeKernel(
-      (const void*)bfs32_fn(r.sel, r.G.S), dim3(r.grid),
+      (const void*)bfs32_fn(r.sel, r.G.S, r.hashed), dim3(r.grid),
       dim3(kThreads), params, r.G.smem, s));
   SSB_CUDA(cudaGetLastError());
   SSB_CUDA(cudaEventRecord(g.sc.e1, s));
@@ -2800,7 +2887,9 @@ void shard_begin(ssb_graph& g, int64_t root, const ssb_bfs_options& o, int64_t c
   g.last_kernel_ms = 0;
   g.last_launches = 0;
   g.last_swept = 0;
-  st->r = prepare32(g, root_pos, root_code, o, {cb, ce});
+  // (no hashed summary: the exchange builds the block summary from the
+  // gathered words)
+  st->r = prepare32(g, root_pos, root_code, o, {cb, ce}, nullptr, nullptr, false, false);
   st->r.a.retire_once = 0;  // the exchange counts and summarises frontier words
   st->r.stepping = true;
   owned_mask(g, st->r.segs, st->owned);
@@ -2890,7 +2979,7 @@ void shard_step_async(ssb_graph& g, uint32_t* owned_words) {
   }
   r.zeroed = false;
   void* params[] = {&a, &r.reset};  // (reset.active = 0: begin_async ran the reset kernel)
-  SSB_CUDA(cudaLaunchCooperativeKernel((const void*)bfs32_fn(r.sel, r.G.S), dim3(r.grid), dim3(kThreads),
+  SSB_CUDA(cudaLaunchCooperativeKernel((const void*)bfs32_fn(r.sel, r.G.S, r.hashed), dim3(r.grid), dim3(kThreads),
                                        params, r.G.smem, s));
   SSB_CUDA(cudaGetLastError());
   g.last_launches += 1;
