@@ -128,6 +128,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
       "r"(phase)
       : "memory");
 }
+#ifndef SSB_LAST_GRAB_SKIP
+#define SSB_LAST_GRAB_SKIP 1  // no counter round trip after the first task when n_tasks <= warps
+#endif
 #ifndef SSB_BCAST
 #define SSB_BCAST 1  // per-iteration totals read by one thread per CTA and broadcast in shared memory
 #endif
@@ -1029,6 +1032,10 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
     int32_t t_pend = 0, n_pend = 0;  // warp-uniform: grabbed, not yet started
     for (;;) {
       int32_t t = t_first;
+      if (SSB_LAST_GRAB_SKIP && t < 0 && n_v <= n_warps) {  // every task was some warp's first: nothing to grab
+        if (kBuf && keep_n) flush_kept();
+        break;
+      }
       if (t < 0) {
         if (n_pend == 0) {
           if (lane == 0) t_pend = int32_t(atomicAdd(&a.task_ctr[rec], uint32_t(kGrab))) + n_warps;
@@ -1709,6 +1716,20 @@ __global__ void pack_wire_kernel(const uint32_t* __restrict__ visited,
     const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
     if (lev8) lev8[o] = reached ? uint8_t(level[p]) : uint8_t(255);
     if (par32) par32[o] = reached ? perm[parent[p]] : -1;
+  }
+}
+
+// Packed wire (sel-max, dist and parents wanted): one 32-bit word per vertex,
+// level << bits | parent's original id, all ones where unreached.
+__global__ void pack_wire32_kernel(const uint32_t* __restrict__ visited, const int32_t* __restrict__ level,
+                                   const int32_t* __restrict__ parent, const int32_t* __restrict__ perm,
+                                   const int32_t* __restrict__ inv_perm, int64_t o0, int64_t o1, int bits,
+                                   uint32_t* __restrict__ out) {
+  GRID_STRIDE(i, o1 - o0) {
+    const int64_t o = o0 + i;
+    const int32_t p = inv_perm[o];
+    const bool reached = (visited[p >> 5] >> (p & 31)) & 1u;
+    out[o] = reached ? (uint32_t(level[p]) << bits) | uint32_t(perm[parent[p]]) : 0xffffffffu;
   }
 }
 
@@ -2607,6 +2628,7 @@ struct WireSlot {
   DevBuf<int> flag;        // dp_transform consistency flag of this slot's root
   int* hflag = nullptr;    // ... its pinned host copy
   std::vector<int64_t> bounds;
+  int packed_bits = 0;     // > 0: the packed 4-byte wire (pack_wire32_kernel) of this slot's root
   ~WireSlot() {
     if (host) cudaFreeHost(host);
     if (hflag) cudaFreeHost(hflag);
@@ -2664,13 +2686,23 @@ void wire_launch(ssb_graph& g, WireSlot& S, int K, bool want_dist, bool want_par
   int32_t* hpar = reinterpret_cast<int32_t*>(S.host + poff);
   BitRegions R = bit_regions(g, 0);
   const bool dp = want_parents && !sel;
+  // the packed 4-byte wire when ids and levels fit one word together
+  int idb = 1;
+  while (idb < 32 && (int64_t{1} << idb) < n) ++idb;
+  const bool packed = want_dist && want_parents && sel && idb <= 31 &&
+                      g.last_iterations < int64_t(0xffffffffu >> idb) && env_int("SSB_WIRE_PACKED", 1) != 0;
+  S.packed_bits = packed ? idb : 0;
   *S.hflag = 0;
   if (dp) SSB_CUDA(cudaMemsetAsync(S.flag.p, 0, 4, s));
   S.bounds.assign(size_t(K) + 1, 0);
   for (int c = 0; c <= K; ++c) S.bounds[size_t(c)] = std::min(n, (n * c / K + 63) / 64 * 64);
   for (int c = 0; c < K; ++c) {
     const int64_t b = S.bounds[size_t(c)], len = S.bounds[size_t(c) + 1] - b;
-    if (len > 0) {
+    if (len > 0 && packed) {
+      pack_wire32_kernel<<<grid_for(len), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p, g.inv_perm.p,
+                                                       b, b + len, idb, reinterpret_cast<uint32_t*>(par32));
+      SSB_CUDA(cudaGetLastError());
+    } else if (len > 0) {
       pack_wire_kernel<<<grid_for(len), 256, 0, s>>>(R.visited, g.level.p, g.parent.p, g.perm.p,
                                                      g.inv_perm.p, b, b + len, want_dist ? lev8 : nullptr,
                                                      want_parents && sel ? par32 : nullptr);
@@ -2682,7 +2714,7 @@ void wire_launch(ssb_graph& g, WireSlot& S, int K, bool want_dist, bool want_par
     }
     SSB_CUDA(cudaEventRecord(S.packed[size_t(c)], s));
     SSB_CUDA(cudaStreamWaitEvent(S.copy, S.packed[size_t(c)], 0));
-    if (len > 0 && want_dist)
+    if (len > 0 && want_dist && !packed)
       SSB_CUDA(cudaMemcpyAsync(hlev + b, lev8 + b, size_t(len), cudaMemcpyDeviceToHost, S.copy));
     if (len > 0 && want_parents)
       SSB_CUDA(cudaMemcpyAsync(hpar + b, par32 + b, 4 * size_t(len), cudaMemcpyDeviceToHost, S.copy));
@@ -2696,7 +2728,8 @@ void wire_launch(ssb_graph& g, WireSlot& S, int K, bool want_dist, bool want_par
 void wire_finish(WireSlot& S, int64_t n, int64_t* dist, int64_t* parent) {
   const int K = int(S.bounds.size()) - 1;
   std::vector<cudaEvent_t> ready(S.ready.begin(), S.ready.begin() + K);
-  widen_chunks(S.bounds, ready, S.host, reinterpret_cast<int32_t*>(S.host + wire_poff(n)), dist, parent);
+  widen_chunks(S.bounds, ready, S.host, reinterpret_cast<int32_t*>(S.host + wire_poff(n)), dist, parent,
+               dist && parent ? S.packed_bits : 0);
   SSB_CUDA(cudaStreamSynchronize(S.copy));
   if (*S.hflag) fail(SSB_EINVAL, "inconsistent distances: a reached vertex has no neighbor one level closer");
 }
