@@ -122,7 +122,53 @@ __attribute__((target("avx2"))) void widen_parents_avx2(const int32_t* par, int6
   for (; i < e; ++i) parent[i] = par[i];
 }
 
-void widen(const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent, int64_t b, int64_t e) {
+// Packed wire (sel-max results with dist and parents wanted, ids < 2^bits,
+// levels < 2^(32-bits) - 1): one 32-bit word per vertex, level << bits | id,
+// all ones where unreached — 4 instead of 5 bytes per vertex DMA-written and
+// read back by the host, whose memory traffic bounds the e2e path.
+__attribute__((target("avx2"))) void widen_packed_avx2(const uint32_t* w, int64_t* dist, int64_t* parent,
+                                                      int64_t b, int64_t e, int bits) {
+  const uint32_t lmax = 0xffffffffu >> bits;
+  const uint32_t idmask = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);
+  auto one = [&](int64_t i) {
+    const uint32_t x = w[i], l = x >> bits;
+    dist[i] = l == lmax ? INT64_MAX : int64_t(l);
+    parent[i] = l == lmax ? -1 : int64_t(x & idmask);
+  };
+  int64_t i = b;
+  for (; i < e && ((reinterpret_cast<uintptr_t>(dist + i) | reinterpret_cast<uintptr_t>(parent + i)) & 31); ++i)
+    one(i);
+  const __m128i sh = _mm_cvtsi32_si128(bits);
+  const __m256i vl = _mm256_set1_epi64x(int64_t(lmax)), vm = _mm256_set1_epi64x(int64_t(idmask));
+  const __m256i mx = _mm256_set1_epi64x(INT64_MAX), neg = _mm256_set1_epi64x(-1);
+  for (; i + 4 <= e; i += 4) {
+    const __m256i x = _mm256_cvtepu32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i*>(w + i)));
+    const __m256i l = _mm256_srl_epi64(x, sh);
+    const __m256i un = _mm256_cmpeq_epi64(l, vl);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dist + i), _mm256_blendv_epi8(l, mx, un));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(parent + i),
+                        _mm256_blendv_epi8(_mm256_and_si256(x, vm), neg, un));
+  }
+  for (; i < e; ++i) one(i);
+}
+
+void widen(const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent, int64_t b, int64_t e,
+           int packed_bits) {
+  if (packed_bits > 0) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(par);
+    if (has_avx2()) {
+      widen_packed_avx2(w, dist, parent, b, e, packed_bits);
+      _mm_sfence();
+      return;
+    }
+    const uint32_t lmax = 0xffffffffu >> packed_bits, idmask = (1u << packed_bits) - 1u;
+    for (int64_t i = b; i < e; ++i) {
+      const uint32_t l = w[i] >> packed_bits;
+      dist[i] = l == lmax ? INT64_MAX : int64_t(l);
+      parent[i] = l == lmax ? -1 : int64_t(w[i] & idmask);
+    }
+    return;
+  }
   if (has_avx2()) {
     if (dist) widen_levels_avx2(lev, dist, b, e);
     if (parent) widen_parents_avx2(par, parent, b, e);
@@ -140,7 +186,8 @@ void widen(const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* paren
 // chunk c = entries [bounds[c], bounds[c+1]) of the host wire buffers, ready
 // once ready[c] has completed; every worker widens its share of every chunk.
 void widen_chunks(const std::vector<int64_t>& bounds, const std::vector<cudaEvent_t>& ready,
-                  const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent) {
+                  const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent,
+                  int packed_bits) {
   Pool& p = pool();
   // Pieces of 64K entries (multiples of 64: the workers' stores stay in
   // separate cache lines) handed out in order through one counter, so a
@@ -165,7 +212,7 @@ void widen_chunks(const std::vector<int64_t>& bounds, const std::vector<cudaEven
       }
       const int64_t lo = bounds[c] + (q - first[c]) * kPiece;
       const int64_t hi = std::min(lo + kPiece, bounds[c + 1]);
-      widen(lev, par, dist, parent, lo, hi);
+      widen(lev, par, dist, parent, lo, hi, packed_bits);
     }
   });
 }

@@ -284,8 +284,11 @@ int bfs_p2p(ssb_graph* const* gs, int n_local, const int64_t* bounds, const int6
             int64_t* iterations, double* device_ms);
 // hostio.cpp: widen the uint8 / int32 wire chunks into int64 host arrays on a
 // persistent host thread pool, chunk c once ready[c] has completed
+// (packed_bits > 0: `par` holds packed words level << packed_bits | parent id,
+// all ones = unreached, and `lev` is unused)
 void widen_chunks(const std::vector<int64_t>& bounds, const std::vector<cudaEvent_t>& ready,
-                  const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent);
+                  const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent,
+                  int packed_bits = 0);
 int host_threads();
 // ingest.cu
 void parse_edge_list(std::string_view text, int directive, std::vector<int64_t>& uv, int64_t& n);

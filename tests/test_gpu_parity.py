@@ -699,7 +699,8 @@ def test_fused_p2p_rank_path_world1(ssb, port, monkeypatch):
 
 def test_fetch_wire_format_equals_direct_path(ssb, port, monkeypatch):
     """Whole-result fetches go through the narrow wire format (uint8 levels +
-    int32 parents over PCIe, widened to int64 by host threads); it must equal
+    int32 parents over PCIe — or, for sel-max, one packed 32-bit word of level
+    and parent id — widened to int64 by host threads); it must equal
     the direct int64 path (SSB_WIRE=0) and the oracle, into pageable and
     pinned outputs, for sel-max parents and dp_transform parents, and with the
     chunking pushed to odd sizes."""
@@ -717,9 +718,12 @@ def test_fetch_wire_format_equals_direct_path(ssb, port, monkeypatch):
             o = opts(ssb, v, True, 64)
             b = port.bfs_spmv(L, root, v, True, 64, csr=(row, col))
             outs = []
-            for wire, chunks in (("1", "16"), ("1", "7"), ("0", "16")):
+            # (sel-max with dist and parents: the packed 4-byte wire by
+            # default, the 5-byte one with SSB_WIRE_PACKED=0)
+            for wire, chunks, packed in (("1", "16", "1"), ("1", "7", "1"), ("1", "16", "0"), ("0", "16", "1")):
                 monkeypatch.setenv("SSB_WIRE", wire)
                 monkeypatch.setenv("SSB_WIRE_CHUNKS", chunks)
+                monkeypatch.setenv("SSB_WIRE_PACKED", packed)
                 a = ssb.bfs_spmv(r, root, o, csr)
                 pin_d.fill(-7)
                 pin_p.fill(-7)
