@@ -577,14 +577,21 @@ def main():
         e2e_tot, single_tot = float(t[0].item()), float(t[1].item())
         e2e_max, single_max = float(mx[0].item()), float(mx[1].item())
     wire = os.environ.get("SSB_WIRE", "1") != "0" and n >= 1 << 16  # fetch_rows' wire-format rule
+    # bfs.cu wire_launch: sel-max dist + parents cross as ONE packed 32-bit word
+    # (level << id_bits | parent id) when ids and levels fit (BFS depth here << 2^(32 - id_bits))
+    id_bits = max(1, int(n - 1).bit_length())
+    packed = (wire and parents_out and variant_id == 3 and id_bits <= 31
+              and os.environ.get("SSB_WIRE_PACKED", "1") != "0")
+    per_vertex = (4 if packed else (5 if parents_out else 1)) if wire else (16 if parents_out else 8)
     e2e = {"value": round(e2e_tot / e2e_max / 1e9, 3) if e2e_tot else None, "unit": "GTEPS",
            "h2d_bytes_per_step": 8 * len(roots),
-           "d2h_bytes_per_step": ((5 if parents_out else 1) if wire else (16 if parents_out else 8)) *
-                                 n * len(roots),
+           "d2h_bytes_per_step": per_vertex * n * len(roots),
            "note": "ssb_bfs_spmv_batch over the step's roots: roots in, dist" +
                    ("+parent" if parents_out else "") + " int64[n] per root out to pinned host memory" +
-                   (" (PCIe carries uint8 levels + int32 parents, widened to int64 by host threads "
-                    "while the next root's BFS runs)" if wire else ""),
+                   ((" (PCIe carries one packed 32-bit word per vertex, level << %d | parent id, "
+                     "widened to int64 by host threads while the next root's BFS runs)" % id_bits) if packed else
+                    (" (PCIe carries uint8 levels + int32 parents, widened to int64 by host threads "
+                     "while the next root's BFS runs)" if wire else "")),
            "single_call": {"value": round(single_tot / single_max / 1e9, 3), "unit": "GTEPS",
                            "note": "one ssb_bfs_spmv call per root, same outputs"}}
 
