@@ -135,21 +135,37 @@ __attribute__((target("avx2"))) void widen_packed_avx2(const uint32_t* w, int64_
     dist[i] = l == lmax ? INT64_MAX : int64_t(l);
     parent[i] = l == lmax ? -1 : int64_t(x & idmask);
   };
-  int64_t i = b;
-  for (; i < e && ((reinterpret_cast<uintptr_t>(dist + i) | reinterpret_cast<uintptr_t>(parent + i)) & 31); ++i)
-    one(i);
   const __m128i sh = _mm_cvtsi32_si128(bits);
   const __m256i vl = _mm256_set1_epi64x(int64_t(lmax)), vm = _mm256_set1_epi64x(int64_t(idmask));
   const __m256i mx = _mm256_set1_epi64x(INT64_MAX), neg = _mm256_set1_epi64x(-1);
-  for (; i + 4 <= e; i += 4) {
-    const __m256i x = _mm256_cvtepu32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i*>(w + i)));
-    const __m256i l = _mm256_srl_epi64(x, sh);
-    const __m256i un = _mm256_cmpeq_epi64(l, vl);
-    _mm256_stream_si256(reinterpret_cast<__m256i*>(dist + i), _mm256_blendv_epi8(l, mx, un));
-    _mm256_stream_si256(reinterpret_cast<__m256i*>(parent + i),
-                        _mm256_blendv_epi8(_mm256_and_si256(x, vm), neg, un));
+  // (a macro, not a lambda: lambdas do not inherit the avx2 target)
+#define SSB_PACKED_FOUR(i, d, p)                                                                     \
+  do {                                                                                               \
+    const __m256i x_ = _mm256_cvtepu32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i*>(w + (i)))); \
+    const __m256i l_ = _mm256_srl_epi64(x_, sh);                                                     \
+    const __m256i un_ = _mm256_cmpeq_epi64(l_, vl);                                                  \
+    d = _mm256_blendv_epi8(l_, mx, un_);                                                             \
+    p = _mm256_blendv_epi8(_mm256_and_si256(x_, vm), neg, un_);                                      \
+  } while (0)
+  int64_t i = b;
+  __m256i d, p;
+  if ((reinterpret_cast<uintptr_t>(dist) ^ reinterpret_cast<uintptr_t>(parent)) & 31) {
+    // the two outputs never align together: plain unaligned stores
+    for (; i + 4 <= e; i += 4) {
+      SSB_PACKED_FOUR(i, d, p);
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(dist + i), d);
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(parent + i), p);
+    }
+  } else {
+    for (; i < e && (reinterpret_cast<uintptr_t>(dist + i) & 31); ++i) one(i);
+    for (; i + 4 <= e; i += 4) {
+      SSB_PACKED_FOUR(i, d, p);
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(dist + i), d);
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(parent + i), p);
+    }
   }
   for (; i < e; ++i) one(i);
+#undef SSB_PACKED_FOUR
 }
 
 void widen(const uint8_t* lev, const int32_t* par, int64_t* dist, int64_t* parent, int64_t b, int64_t e,

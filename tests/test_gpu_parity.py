@@ -729,6 +729,12 @@ def test_fetch_wire_format_equals_direct_path(ssb, port, monkeypatch):
                 pin_p.fill(-7)
                 c = ssb.bfs_spmv(r, root, o, csr, pin_d, pin_p)
                 outs.append((a.dist.copy(), a.parent.copy(), c.dist.copy(), c.parent.copy()))
+                # outputs whose addresses differ by 8 bytes mod 32 (no common
+                # alignment for streaming stores)
+                md = np.full(n, -7, np.int64)
+                mp = np.full(n + 1, -7, np.int64)[1:]
+                e = ssb.bfs_spmv(r, root, o, csr, md, mp)
+                outs.append((e.dist.copy(), e.parent.copy(), md.copy(), mp.copy()))
             for d1, p1, d2, p2 in outs:
                 assert np.array_equal(d1, b.dist) and np.array_equal(d2, b.dist), (root, v)
                 assert np.array_equal(p1, b.parent) and np.array_equal(p2, b.parent), (root, v)
