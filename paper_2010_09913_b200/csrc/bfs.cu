@@ -213,6 +213,7 @@ struct Args32 {
   int32_t hash_on;     // sparse iterations also build the hashed summary (Probe kHash), used next
   uint32_t HB;         // hashed summary bits (SW * 32)
   int64_t hash_thr;    // early-exit iterations probe the hashed summary while |F_{k-1}| <= this
+  int32_t hash_prev_in; // iteration k_begin - 1 (a previous launch) built the hashed summary
   uint32_t* H0;        // hashed summaries, rotating like S0..S2
   uint32_t* H1;
   uint32_t* H2;
@@ -921,7 +922,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
   }
   // every rank has reset its window before anyone stores into it
   if (kP2P) p2p_barrier(x, x.gen_base + 1);
-  bool hash_prev = false;  // the previous iteration (in this launch) built the hashed summary
+  bool hash_prev = kHash && a.hash_prev_in;  // the previous iteration built the hashed summary
 
   for (int32_t k = a.k_begin; k < a.k_end; ++k) {
     const int32_t rec = k - a.k_begin;
@@ -2102,8 +2103,8 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   // bits (S22's 16K-bit summary is saturated by the frontiers that reach it
   // either way); not where summary words are exchanged between ranks (p2p
   // windows, NCCL shards: allow_hash = false)
-  r.hashed = allow_hash && !p2p && G.S == 8 && int64_t(G.SW) * 32 >= 65536 &&
-             env_int("SSB_HASH_SUMMARY", 1) != 0;
+  r.hashed = allow_hash && !p2p && G.S == 8 && G.SW > 0 &&
+             int64_t(G.SW) * 32 >= env_int("SSB_HASH_MIN_BITS", 65536) && env_int("SSB_HASH_SUMMARY", 1) != 0;
   BitRegions R = bit_regions(g, G.SW);
   if (p2p) {
     uint32_t* w = p2p->win[p2p->rank];
@@ -2211,6 +2212,7 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.H2 = R.H2;
   a.HB = uint32_t(G.SW) * 32u;
   a.hash_on = r.hashed ? 1 : 0;  // (see r.hashed)
+  a.hash_prev_in = 0;
   {
     // A/B at S26 over 16 roots: HB / 2 4.234, HB 4.205-4.215 ms per BFS
     // (with the n/32768 dense threshold below), no hashing 4.271
@@ -2397,6 +2399,10 @@ int64_t launch32(ssb_graph& g, Run32& r, int64_t kend, std::vector<ssb_iter_stat
   g.sc.sync();
   a.n_tasks = int32_t(outs.back());
   for (auto x : gones) a.gone_base += x;
+  // the launch's last iteration built the hashed summary iff it swept sparse
+  // (its input frontier |F_{k-1}| at most the dense threshold)
+  const int64_t f_in_last = ran >= 2 ? r.rec[size_t(ran - 2) * kStatW] : a.front_in;
+  a.hash_prev_in = (r.hashed && f_in_last <= a.dense_thr) ? 1 : 0;
   a.front_in = r.rec[size_t(ran - 1) * kStatW];
   r.k += ran;
   return ran;

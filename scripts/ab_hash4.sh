@@ -1,4 +1,5 @@
 #!/bin/bash
+# ab/bc1.so: scripts/build_variant.sh $PWD/ab/bc1.so at commit 0ed113d (before the hashed summary)
 # A/B of the tree against ab/bc1.so (the kernel before the hashed summary), then the GPU suite
 {
 bash scripts/ab_libs.sh "--scale 22 --roots 64" $PWD/ab/bc1.so base

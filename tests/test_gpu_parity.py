@@ -364,6 +364,13 @@ def test_errors(ssb):
     {"SSB_DENSE_DIV": "4096"},         # the default switch point
     {"SSB_DENSE_DIV": "1000000000", "SSB_SUMMARY_SHIFT": "6"},  # 64-vertex summary, sparse
     {"SSB_DENSE_DIV": "1", "SSB_SUMMARY_SHIFT": "6"},           # 64-vertex summary, early exit
+    # the hashed summary (built by sparse iterations, probed by the next
+    # early-exit one), also carried across one-iteration launches
+    {"SSB_DENSE_DIV": "4096", "SSB_SUMMARY_SHIFT": "8", "SSB_HASH_MIN_BITS": "1"},
+    {"SSB_DENSE_DIV": "4096", "SSB_SUMMARY_SHIFT": "8", "SSB_HASH_MIN_BITS": "1",
+     "SSB_ITERS_PER_LAUNCH": "1"},
+    {"SSB_DENSE_DIV": "64", "SSB_SUMMARY_SHIFT": "8", "SSB_HASH_MIN_BITS": "1",
+     "SSB_HASH_THR": "1000000000"},
 ])
 def test_sweep_modes_with_small_shared_image(ssb, port, monkeypatch, mode_env):
     """Both sweep modes (sparse / early-exit) with a tiny shared-memory
