@@ -10,7 +10,8 @@ tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
 sass = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, "bfs.sm_100a.cubin")], capture_output=True,
                       text=True).stdout
-fn = f"bfs32_kernelILb{sel}ELi{os.environ.get('KS', '8')}EEEvNS0_6Args32E:"
+# bfs32_kernel<sel, S, hashed> (HASH=0/1: the hashed-summary instantiation)
+fn = f"bfs32_kernelILb{sel}ELi{os.environ.get('KS', '8')}ELb{os.environ.get('HASH', '1')}EEEvNS0_6Args32E:"
 site, on, cur, hdr = {}, False, None, False
 for line in sass.splitlines():
     if line.endswith(fn) and not line.startswith("."):
