@@ -431,7 +431,15 @@ def main():
     if shard == "chunks":
         return main_chunks(a, world, rank, local, log, variant_id, slimwork)
     if shard == "p2p":
-        return main_p2p(a, world, rank, local, log, variant_id, slimwork)
+        why = None
+        try:
+            return main_p2p(a, world, rank, local, log, variant_id, slimwork)
+        except Exception as e:  # every rank raises it together (sharding.P2PShard.attach_dist)
+            if type(e).__name__ != "P2PUnavailable":
+                raise
+            why = str(e)
+        log(f"fused peer exchange unavailable ({why}): --shard chunks")
+        return main_chunks(a, world, rank, local, log, variant_id, slimwork)
 
     import torch
 

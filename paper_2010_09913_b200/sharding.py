@@ -239,6 +239,10 @@ class DeviceShard:
         return _stats_list(st, iterations), float(ms.value)
 
 
+class P2PUnavailable(RuntimeError):
+    """The fused peer exchange cannot be set up on this group of GPUs."""
+
+
 class P2PShard:
     """One rank's shard of the FUSED multi-GPU BFS: the frontier exchange runs
     inside the BFS kernel over peer-mapped windows (ssb_p2p_* / ssb_bfs_p2p),
@@ -274,12 +278,24 @@ class P2PShard:
                                                b.ctypes.data_as(L.i64p), len(self.segs)))
 
     def attach_dist(self, group=None) -> None:
+        """Collective: every rank maps every peer's window. A rank that cannot
+        (e.g. CUDA IPC refused) makes EVERY rank raise P2PUnavailable, so the
+        caller can fall back to the NCCL exchange instead of a hung barrier."""
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         mine = self.window_handle()
         handles = [None] * world
         dist.all_gather_object(handles, mine, group=group)
-        self.attach(rank, world, handles)
+        err = ""
+        try:
+            self.attach(rank, world, handles)
+        except Exception as e:  # noqa: BLE001 - reported to every rank below
+            err = f"rank {rank}: {e}"
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        failed = [x for x in errs if x]
+        if failed:
+            raise P2PUnavailable("; ".join(failed))
         dist.barrier(group=group)  # every window mapped and zeroed before any BFS
 
     def run(self, root: int, opts):

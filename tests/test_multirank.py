@@ -201,6 +201,46 @@ def test_bench_spawner_runs_n_ranks(tmp_path, capfd):
     assert d == {"world": 2, "sum": 3, "argv": ["--gpus", "2", "--steps", "1"]}
 
 
+def test_p2p_attach_failure_is_collective(tmp_path, capfd):
+    """The fused exchange's window mapping is collective: when one rank cannot
+    map its peers' windows, EVERY rank raises P2PUnavailable (bench.py then
+    falls back to the NCCL exchange) instead of the others hanging in the
+    barrier. Gloo ranks with a stand-in shard whose rank-1 attach fails."""
+    import json
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "rank.py"
+    script.write_text(
+        "import json, os, sys\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import torch.distributed as dist\n"
+        "from paper_2010_09913_b200.sharding import P2PShard, P2PUnavailable\n"
+        "dist.init_process_group('gloo')\n"
+        "class Fake:\n"
+        "    def window_handle(self):\n"
+        "        return bytes([dist.get_rank()])\n"
+        "    def attach(self, rank, world, handles):\n"
+        "        assert handles == [bytes([r]) for r in range(world)]\n"
+        "        if rank == 1:\n"
+        "            raise RuntimeError('ipc refused')\n"
+        "out = 'attached'\n"
+        "try:\n"
+        "    P2PShard.attach_dist(Fake())\n"
+        "except P2PUnavailable as e:\n"
+        "    out = str(e)\n"
+        "outs = [None] * dist.get_world_size()\n"
+        "dist.all_gather_object(outs, out)\n"
+        "if dist.get_rank() == 0:\n"
+        "    print(json.dumps(outs))\n"
+        "dist.destroy_process_group()\n")
+    rc = bench.spawn_ranks(2, script=str(script), argv=[])
+    assert rc == 0
+    out = [ln for ln in capfd.readouterr().out.splitlines() if ln.startswith("[")]
+    assert json.loads(out[0]) == ["rank 1: ipc refused"] * 2
+
+
 def test_bench_default_decomposition():
     """N = 1: the single-GPU engine; N > 1: fused peer exchange when every GPU
     pair maps each other's memory and the backend is NCCL, else the NCCL
