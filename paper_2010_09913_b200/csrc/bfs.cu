@@ -211,7 +211,8 @@ struct Args32 {
   unsigned long long* gone_chunks;  // chunks of retired tasks (skipped forever)
   int32_t retire_once; // retire a task the first time all its units are skipped (see run_tasks)
   int32_t hash_on;     // sparse iterations also build the hashed summary (Probe kHash), used next
-  uint32_t HB;         // hashed summary bits (SW * 32)
+  uint32_t HB;         // summary bits (SW * 32)
+  uint32_t hash_arg;   // summary_hash's shift: 32 - log2 of the hashed bits (a power of two <= HB)
   int64_t hash_thr;    // early-exit iterations probe the hashed summary while |F_{k-1}| <= this
   int32_t hash_prev_in; // iteration k_begin - 1 (a previous launch) built the hashed summary
   uint32_t* H0;        // hashed summaries, rotating like S0..S2
@@ -303,8 +304,12 @@ struct GroupArgs {
 // set where the probes land: at S26 iteration 3 a hashed summary of the same
 // size is set for 5-9x fewer open tail cells (scripts/summary_fp.py). A set
 // bit still only sends the cell to its exact word: no false negatives.
-__device__ __forceinline__ uint32_t summary_hash(int32_t pos, uint32_t bits) {
-  return __umulhi(uint32_t(pos) * 0x9E3779B1u, bits);  // Fibonacci hash into [0, bits)
+// Fibonacci hash: the top log2(bits) bits of pos · 2^32/φ, `shift` = 32 -
+// log2(bits) for the largest power of two of bits within the summary (a
+// shift, not a high multiply: A/B at S26 4.301 -> 4.279 ms per BFS, iteration
+// 3 -21 µs, `profiles/r2v_ab_hash_shift.txt`)
+__device__ __forceinline__ uint32_t summary_hash(int32_t pos, uint32_t shift) {
+  return (uint32_t(pos) * 0x9E3779B1u) >> shift;
 }
 
 template <int kS, bool kHash = false>
@@ -313,7 +318,7 @@ struct Probe {
   const uint32_t* sm;  // word 0 = first prefix word; sm[-4..-1] are zero
   const uint32_t* Fc;  // the full frontier in global memory
   int32_t P;           // prefix vertices (multiple of 2^S)
-  int32_t Pt;          // P - (P >> S); kHash: the summary's bit count
+  int32_t Pt;          // P - (P >> S); kHash: summary_hash's shift
 
   // virtual bit of cell target c (padding c = -1 maps to a zero word)
   __device__ __forceinline__ int32_t vidx(int32_t c) const {
@@ -637,7 +642,7 @@ __device__ __forceinline__ void finish_unit(const Args32& a, int32_t k, uint32_t
           // extra stays live through the sweep)
           if (kHash && !kEarly && chunk >= a.PW) {
             uint32_t* Hn = (k % 3) == 0 ? a.H0 : ((k % 3) == 1 ? a.H1 : a.H2);
-            const uint32_t h = summary_hash(int32_t(row), a.HB);
+            const uint32_t h = summary_hash(int32_t(row), a.hash_arg);
             atomicOr(&Hn[h >> 5], 1u << (h & 31));
           }
         }
@@ -1268,7 +1273,7 @@ __device__ __forceinline__ void bfs32_body(const Args32& a, const P2PArgs& x, co
       run_tasks(std::true_type{}, std::true_type{}, prb);
     } else if (use_hash) {
       if constexpr (kHash) {
-        const Probe<kS, true> prh{sm + 4, Fc, img_words * 32, int32_t(a.HB)};
+        const Probe<kS, true> prh{sm + 4, Fc, img_words * 32, int32_t(a.hash_arg)};
         run_tasks(std::true_type{}, std::false_type{}, prh);  // (use_hash implies dense)
       }
     } else if (dense) {
@@ -2212,12 +2217,19 @@ Run32 prepare32(ssb_graph& g, int32_t root_pos, int32_t root_code, const ssb_bfs
   a.H2 = R.H2;
   a.HB = uint32_t(G.SW) * 32u;
   a.hash_on = r.hashed ? 1 : 0;  // (see r.hashed)
+  {
+    // hash into the largest power of two of bits the summary words hold
+    // (every S26/S28 summary is one; otherwise the top words stay zero)
+    int lg = 1;
+    while (lg < 31 && (uint32_t{1} << (lg + 1)) <= a.HB) ++lg;
+    a.hash_arg = uint32_t(32 - lg);
+  }
   a.hash_prev_in = 0;
   {
     // A/B at S26 over 16 roots: HB / 2 4.234, HB 4.205-4.215 ms per BFS
     // (with the n/32768 dense threshold below), no hashing 4.271
     const int64_t ht = env_int("SSB_HASH_THR", -1);
-    a.hash_thr = ht >= 0 ? ht : int64_t(a.HB);
+    a.hash_thr = ht >= 0 ? ht : (int64_t{1} << (32 - a.hash_arg));
   }
   a.level = g.level.p;
   a.parent = g.parent.p;
