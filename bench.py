@@ -244,6 +244,10 @@ def init_dist(torch, ssb, world, local):
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("SSB_BENCH_BACKEND", "nccl")
+        if dist.is_initialized():  # re-entered (the p2p -> NCCL fallback): keep the group
+            if backend != "nccl":
+                RED_DEV = "cpu"
+            return dev
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
